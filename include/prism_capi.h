@@ -1,0 +1,376 @@
+/* prism-b200 C-ABI — the drop-in boundary for the elastic-KV + paged-decode
+ * hot path of Prism (arXiv 2505.04021).
+ *
+ * Plain C: opaque handles, plain pointers and sizes, int status codes; no
+ * exception ever crosses this boundary (C++ exceptions map to PRISM_E_*,
+ * message in prism_last_error()). Every entry point names the reference
+ * interface it replaces (paths relative to /root/reference/proj).
+ *
+ * Two libraries export this ABI:
+ *   paper_2505_04021_b200/libprism_b200.so   the product (host C++ runtime +
+ *                                            CUDA VMM + sm_100a kernels);
+ *   oracle/_ref/libmsim_ref.so               the reference compiled from its
+ *                                            own sources + a thin wrapper
+ *                                            (test oracle only; host subset,
+ *                                            the GPU entry points are absent).
+ * so parity tests drive both through identical calls.
+ *
+ * Threading: one ledger (with its pools / engines) is one serialization
+ * domain (reference include/msim/pagealloc.hpp:42-44); different GPUs'
+ * objects may be used from different threads concurrently.
+ */
+#ifndef PRISM_CAPI_H
+#define PRISM_CAPI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRISM_ABI_VERSION 1
+
+enum prism_status {
+    PRISM_OK = 0,
+    PRISM_E_USAGE = 1,     /* msim::UsageError: misuse, stale/foreign handle, bad size */
+    PRISM_E_PARSE = 2,     /* msim::ParseError: bad trace input */
+    PRISM_E_CONFIG = 3,    /* msim::ConfigError */
+    PRISM_E_PLACEMENT = 4, /* msim::placement::PlacementError: a model fits on no GPU */
+    PRISM_E_CUDA = 5,      /* CUDA / driver failure, or GPU entry point without a device */
+    PRISM_E_ARG = 6,       /* null pointer / output buffer too small */
+    PRISM_E_INTERNAL = 7
+};
+
+int prism_abi_version(void);
+/* Message of the last failing call on this thread ("" if none). */
+const char* prism_last_error(void);
+/* 1 when the library contains the CUDA data path (product), 0 for the oracle. */
+int prism_has_device_path(void);
+
+/* ------------------------------------------------------------------ types */
+
+typedef struct prism_ledger prism_ledger; /* msim::pagealloc::PhysicalLedger */
+typedef struct prism_pool prism_pool;     /* msim::pagealloc::KvPool */
+typedef struct prism_gpu prism_gpu;       /* msim::engine::GpuState */
+typedef struct prism_device prism_device; /* prism::VmmDevice (product only) */
+
+/* msim::pagealloc::TokenSlotHandle (pagealloc.hpp:16-24) */
+typedef struct {
+    uint32_t pool;
+    uint32_t page;
+    uint32_t slot;
+} prism_slot;
+
+/* msim::pagealloc::AllocResult scalars (pagealloc.hpp:104-110) */
+typedef struct {
+    uint64_t shortfall_pages;
+    uint64_t pages_mapped;
+    uint64_t buffer_hits;
+    uint64_t n_handles;
+} prism_alloc_result;
+
+/* msim::pagealloc::AllocEvent (pagealloc.hpp:34-40); kind: 0 map, 1 unmap,
+ * 2 buffer_hit, 3 alloc_fail (AllocEventKind order). */
+typedef struct {
+    int64_t time_us;
+    int32_t gpu_id;
+    int32_t kind;
+    uint64_t pages;
+    char model_id[64];
+} prism_event;
+
+typedef struct {
+    uint64_t capacity_pages, mapped_pages, buffer_pages, weight_pages, free_pages, page_bytes;
+} prism_ledger_stats;
+
+typedef struct {
+    uint32_t id;
+    int32_t alive;
+    uint64_t token_bytes, tokens_per_page, virtual_capacity_pages, mapped_pages, occupied_slots;
+    uint64_t device_base; /* product with a device attached: VA of page 0 */
+} prism_pool_info;
+
+/* msim::engine::ModelSpec (engine.hpp:16-25) + the prism-b200 attention shape */
+typedef struct {
+    const char* model_id;
+    uint64_t weight_bytes;
+    uint64_t token_kv_bytes;
+    double prefill_tps;
+    int32_t chunk_size;
+    double ttft_slo_s;
+    double tpot_slo_s;
+    int32_t tp_degree;
+    int32_t n_layers, n_q_heads, n_kv_heads, head_dim; /* 0: host-only model */
+} prism_model_spec;
+
+/* msim::engine::EngineParams (engine.hpp:27-34) */
+typedef struct {
+    double alpha_ms, beta_ms_per_token, map_latency_ms, engine_init_s, realign_s, reserve_frac;
+} prism_engine_params;
+
+/* msim::engine::ActivationOutcome (engine.hpp:129-135) */
+typedef struct {
+    int32_t engine_index;
+    int64_t init_us, realign_us, load_us;
+} prism_activation;
+
+/* msim::engine::IterationOutcome scalars (engine.hpp:69-78); the id lists
+ * are read with prism_engine_outcome_ids. */
+typedef struct {
+    int64_t duration_us;
+    int32_t chunk_tokens;
+    int32_t decode_tokens;
+    uint64_t pages_mapped_direct;
+    int32_t prefill_paused;
+    uint32_t n_first_tokens, n_completions, n_preemptions;
+} prism_outcome;
+
+/* One request as EngineRequest exposes it (engine.hpp:57-67). */
+typedef struct {
+    uint64_t id;
+    int32_t prompt_tokens, output_tokens, prompt_done, generated;
+    uint64_t admit_seq;
+    uint64_t n_slots; /* kv[0].size() */
+    int64_t table_row;
+} prism_request_info;
+
+/* ------------------------------------------------------------------ defaults / params */
+
+void prism_default_engine_params(prism_engine_params* out);
+void prism_default_model_spec(prism_model_spec* out);
+
+/* ------------------------------------------------------------------ ledger (pagealloc.hpp:45-102, src/pagealloc.cpp:17-106) */
+
+int prism_ledger_create(int gpu_id, uint64_t capacity_pages, uint64_t page_bytes, prism_ledger** out);
+void prism_ledger_destroy(prism_ledger* l);
+int prism_ledger_get_stats(const prism_ledger* l, prism_ledger_stats* out);
+int prism_ledger_pool_mapped_pages(const prism_ledger* l, uint32_t pool_id, uint64_t* out);
+int prism_refill_buffer(prism_ledger* l, uint64_t target_pages, uint64_t* added); /* refill_buffer :193 */
+int prism_ledger_reserve_weights(prism_ledger* l, const char* model_id, uint64_t pages, int* ok);
+int prism_ledger_release_weights(prism_ledger* l, const char* model_id);
+int prism_ledger_weight_pages_of(const prism_ledger* l, const char* model_id, uint64_t* out);
+int prism_ledger_set_time(prism_ledger* l, int64_t now_us);
+int prism_ledger_set_recording(prism_ledger* l, int on);
+int prism_ledger_events(const prism_ledger* l, prism_event* out, size_t cap, size_t* n); /* n = total */
+int prism_ledger_clear_events(prism_ledger* l);
+int prism_ledger_check_invariants(const prism_ledger* l);
+
+/* ------------------------------------------------------------------ pool (pagealloc.hpp:114-191) */
+
+/* alloc_kvcache (pagealloc.hpp:176); placement: 0 most_occupied_first, 1 lowest_index_first */
+int prism_kvcache_alloc(prism_ledger* l, const char* model_id, uint64_t token_bytes, uint64_t virtual_pages,
+                        int placement, prism_pool** out);
+/* free_kvcache (pagealloc.hpp:182); the handle stays valid (dead) until prism_pool_destroy */
+int prism_kvcache_free(prism_ledger* l, prism_pool* p);
+void prism_pool_destroy(prism_pool* p);
+int prism_pool_info_get(const prism_pool* p, prism_pool_info* out);
+/* alloc_kv (pagealloc.hpp:187). out must hold n slots; res.n_handles = n on success, 0 on shortfall. */
+int prism_kv_alloc(prism_pool* p, prism_ledger* l, uint64_t n, prism_slot* out, prism_alloc_result* res);
+/* free_kv (pagealloc.hpp:191); on PRISM_E_USAGE the prefix before the bad handle was applied, as in the reference. */
+int prism_kv_free(prism_pool* p, prism_ledger* l, const prism_slot* handles, size_t n);
+int prism_pool_allocatable_tokens(const prism_pool* p, const prism_ledger* l, uint64_t* out);
+int prism_pool_page_occupied(const prism_pool* p, uint32_t page, uint64_t* out);
+int prism_pool_page_mapped(const prism_pool* p, uint32_t page, int* out);
+/* set_mapped_page_cap (pagealloc.hpp:131); cap < 0 clears it */
+int prism_pool_set_cap(prism_pool* p, int64_t cap);
+
+/* ------------------------------------------------------------------ engines (engine.hpp:82-147) */
+
+int prism_gpu_create(int gpu_id, uint64_t capacity_pages, uint64_t page_bytes, prism_gpu** out);
+void prism_gpu_destroy(prism_gpu* g);
+/* Borrowed view of GpuState::ledger (do not destroy). */
+prism_ledger* prism_gpu_ledger(prism_gpu* g);
+int prism_gpu_engine_count(const prism_gpu* g, int* out);
+/* activate (engine.hpp:140); method 0 naive, 1 parallel; *ok = 0 when the weights do not fit. */
+int prism_gpu_activate(prism_gpu* g, const prism_model_spec* spec, int method, const prism_engine_params* params,
+                       prism_activation* out, int* ok);
+int prism_gpu_finish_activation(prism_gpu* g, int engine_index); /* engine.hpp:143 */
+int prism_gpu_deactivate(prism_gpu* g, int engine_index);        /* engine.hpp:147 */
+int prism_engine_status(const prism_gpu* g, int engine_index, int* status); /* EngineStatus order */
+int prism_engine_push(prism_gpu* g, int engine_index, uint64_t id, int prompt_tokens, int output_tokens);
+/* step (engine.hpp:113) for a single-part engine on this GPU's ledger. */
+int prism_engine_step(prism_gpu* g, int engine_index, const prism_engine_params* params, int64_t now_us,
+                      prism_outcome* out);
+/* Id lists of the last step's outcome: which 0 first_tokens, 1 completions, 2 preemptions. */
+int prism_engine_outcome_ids(const prism_gpu* g, int engine_index, int which, uint64_t* out, size_t cap, size_t* n);
+int prism_engine_counts(const prism_gpu* g, int engine_index, size_t* batch, size_t* queue);
+/* where 0 batch, 1 local_queue; index in that container's order */
+int prism_engine_request(const prism_gpu* g, int engine_index, int where, size_t index, prism_request_info* out);
+/* kv[0] handles of a batch request, token order */
+int prism_engine_request_kv(const prism_gpu* g, int engine_index, uint64_t request_id, prism_slot* out, size_t cap,
+                            size_t* n);
+int prism_engine_mapped_pages(const prism_gpu* g, int engine_index, uint64_t* out);
+int prism_engine_next_chunk_need(const prism_gpu* g, int engine_index, uint64_t* out);
+int prism_engine_has_runnable_work(const prism_gpu* g, int engine_index, int* out);
+int prism_engine_reserved_pages(const prism_gpu* g, int engine_index, double reserve_frac, uint64_t* out);
+/* throughput_of (engine.hpp:162) */
+int prism_throughput_of(uint64_t kv_budget_bytes, const prism_model_spec* spec, int prompt_tokens, int output_tokens,
+                        const prism_engine_params* params, uint64_t page_bytes, double warmup_s, double window_s,
+                        double* tokens_per_s, int* max_batch);
+
+/* ------------------------------------------------------------------ global scheduler (placement.hpp:20-109) */
+
+typedef struct {
+    prism_model_spec spec;
+    double rate;
+    const int32_t* current_gpus; /* n_current entries, one per TP part */
+    int32_t n_current;
+} prism_model_demand;
+
+typedef struct {
+    const char* model_id;
+    double idle_s, ttft_slo_s;
+    uint64_t weight_bytes, weight_pages;
+} prism_resident;
+
+typedef struct {
+    int32_t gpu_id;
+    uint64_t capacity_bytes, weight_bytes;
+    double w_req_rate;
+    uint64_t capacity_pages, free_pages, page_bytes;
+    const prism_resident* residents;
+    int32_t n_residents;
+} prism_gpu_view;
+
+typedef struct {
+    int32_t model_index; /* into the models array */
+    int32_t part_index, from_gpu, to_gpu;
+} prism_migration;
+
+typedef struct {
+    double max_kvpr_after;
+    int32_t critical_gpu;
+    double critical_shared_before_bytes, critical_last_weight_bytes;
+    uint32_t n_migrations;
+} prism_plan_info;
+
+/* kvpr (placement.hpp:45) */
+int prism_kvpr(double w_req_rate, double shared_kv_bytes, double* out);
+/* place_models (placement.hpp:88). assignment: for model i its tp_degree GPUs at
+ * offset sum_{j<i} tp_j (cap = sum tp); kvpr_before/after: n_gpus each. */
+int prism_place_models(const prism_model_demand* models, size_t n_models, const prism_gpu_view* gpus, size_t n_gpus,
+                       double tau_per_gb, int32_t* assignment, size_t assignment_cap, double* kvpr_before,
+                       double* kvpr_after, prism_migration* migrations, size_t migrations_cap, prism_plan_info* info);
+/* eviction_tick (placement.hpp:100) with the common predicate "free_pages <
+ * min_free_pages" (the reference takes a std::function). out: (gpu index,
+ * resident index) pairs in eviction order. */
+int prism_eviction_tick(const prism_gpu_view* gpus, size_t n_gpus, double idle_threshold_s, uint64_t min_free_pages,
+                        int32_t* out_pairs, size_t cap, size_t* n);
+/* activate_on_arrival[_tp] (placement.hpp:104-109); *found = 0 -> nullopt */
+int prism_activate_on_arrival(const prism_model_spec* spec, const prism_gpu_view* gpus, size_t n_gpus, int32_t* gpu,
+                              int* found);
+int prism_activate_on_arrival_tp(const prism_model_spec* spec, const prism_gpu_view* gpus, size_t n_gpus,
+                                 int32_t* out, size_t cap, int* found);
+
+/* ------------------------------------------------------------------ local scheduler (admission.hpp:14-48) */
+
+typedef struct {
+    uint64_t id;
+    const char* model_id;
+    double arrival_s;
+    int32_t prompt_tokens;
+    double ttft_slo_s, exec_estimate_s;
+} prism_queued_request;
+
+/* moore_hodgson (admission.hpp:30): admit / deferred as indices into queue, in decision order. */
+int prism_moore_hodgson(const prism_queued_request* queue, size_t n, double now_s, int32_t* admit, size_t* n_admit,
+                        int32_t* deferred, size_t* n_deferred);
+/* dispatch (admission.hpp:44) over an admit list (indices into reqs); gate returns DispatchStatus (0 dispatched). */
+typedef int (*prism_dispatch_gate)(void* ctx, const prism_queued_request* r);
+int prism_dispatch(const prism_queued_request* reqs, const int32_t* admit, size_t n_admit, prism_dispatch_gate gate,
+                   void* ctx, uint64_t* dispatched, size_t* n_dispatched);
+/* requeue_deferred (admission.hpp:47): out = indices into the concatenation [queue..., deferred...]. */
+int prism_requeue_deferred(const prism_queued_request* deferred, size_t n_deferred, const prism_queued_request* queue,
+                           size_t n_queue, int32_t* out, size_t* n_out);
+
+/* ------------------------------------------------------------------ workload (workload.hpp:14-78) */
+
+typedef struct {
+    double arrival_s;
+    char model_id[64];
+    int32_t prompt_tokens, output_tokens;
+} prism_trace_event;
+
+typedef struct {
+    double start_s, end_s, rate_per_s;
+} prism_rate_segment;
+
+typedef struct {
+    const char* model_id;
+    const prism_rate_segment* segments;
+    int32_t n_segments;
+    double prompt_median, prompt_sigma, output_median, output_sigma;
+} prism_model_profile;
+
+/* synth_trace (workload.hpp:78): n = total events (call with cap 0 to size). */
+int prism_synth_trace(const prism_model_profile* profiles, size_t n_profiles, uint64_t seed, prism_trace_event* out,
+                      size_t cap, size_t* n);
+/* scale_trace (workload.hpp:29) */
+int prism_scale_trace(const prism_trace_event* in, size_t n_in, int factor, uint64_t seed, double jitter_window_s,
+                      prism_trace_event* out, size_t cap, size_t* n);
+/* parse_trace_lines (workload.hpp:24) */
+int prism_parse_trace_text(const char* text, const char* origin, prism_trace_event* out, size_t cap, size_t* n);
+
+/* ------------------------------------------------------------------ GPU data path (product only; no reference counterpart) */
+
+/* prism::VmmDevice on CUDA device `ordinal` (2 MiB pages). */
+int prism_device_open(int ordinal, uint64_t page_bytes, prism_device** out);
+void prism_device_close(prism_device* d);
+/* Ledger capacity in pages after leaving reserve_bytes of free HBM. */
+int prism_device_capacity_pages(const prism_device* d, uint64_t reserve_bytes, uint64_t* out);
+typedef struct {
+    uint64_t maps, revived, creates, unmaps, driver_unmaps;
+    double map_ns_total, unmap_ns_total;
+    double map_ns_p50, map_ns_p99, unmap_ns_p50, unmap_ns_p99;
+    uint64_t buffered, cached, pending;
+} prism_device_stats;
+int prism_device_stats_get(const prism_device* d, prism_device_stats* out);
+int prism_device_reset_stats(prism_device* d);
+int prism_device_reclaim(prism_device* d, int wait);
+int prism_device_synchronize(prism_device* d);
+void* prism_device_stream(const prism_device* d); /* cudaStream_t of the GPU's work stream */
+/* PhysicalLedger::attach_device; before any pool is created on the ledger. */
+int prism_ledger_attach_device(prism_ledger* l, prism_device* d);
+
+/* Pool-level GPU slot mirror (K1 without an engine): replays the pool's
+ * pending alloc/free log on the device; out receives the slot ids
+ * (page * tokens_per_page + slot) of every logged allocation, in order. */
+int prism_pool_attach_mirror(prism_pool* p);
+int prism_pool_sync_mirror(prism_pool* p, int32_t* out, size_t cap, size_t* n);
+int prism_pool_read_mirror(prism_pool* p, uint32_t* occ, size_t occ_cap, uint32_t* bits, size_t bits_cap);
+
+typedef struct {
+    int64_t table_capacity;
+    int32_t max_decode_batch;
+    int32_t max_step_tokens;
+} prism_engine_device_options;
+
+/* prism::attach_engine_device (msim/kvcache_device.hpp). */
+int prism_engine_attach_device(prism_gpu* g, int engine_index, const prism_engine_device_options* opts);
+/* Last step: slots allocated (prefill chunk first, then decodes) and decoded requests. */
+int prism_engine_step_info(const prism_gpu* g, int engine_index, int32_t* n_step_tokens, int32_t* n_decodes);
+int prism_engine_step_decode_ids(const prism_gpu* g, int engine_index, uint64_t* out, size_t cap, size_t* n);
+/* Device copy of the last step's slot ids (synchronous; verifies the device allocator agreed with the host). */
+int prism_engine_step_slots(const prism_gpu* g, int engine_index, int32_t* out, size_t cap, size_t* n);
+int prism_engine_table_row(const prism_gpu* g, int engine_index, int64_t row, int32_t len, int32_t* out);
+/* K2: k, v device bf16 [layer_end-layer_begin][n_step_tokens][n_kv][head_dim] */
+int prism_engine_append_kv(prism_gpu* g, int engine_index, int layer_begin, int layer_end, const void* k,
+                           const void* v);
+int prism_engine_append_kv_synthetic(prism_gpu* g, int engine_index, int layer_begin, int layer_end, uint64_t seed);
+/* K3: q, out device bf16 [n_decodes][n_q_heads][head_dim]; chunk <= 0 picks the split size. */
+int prism_engine_decode_attention(prism_gpu* g, int engine_index, int layer, const void* q, void* out, float scale,
+                                  int32_t chunk);
+int prism_engine_synth_q(prism_gpu* g, int engine_index, int layer, uint64_t seed, float q_scale, void* q);
+/* End-to-end: the same attention with HOST buffers (pinned or pageable);
+ * copies q in, runs K2 for new_k/new_v (host, may be null) over all layers
+ * and K3 for every layer, copies out back; synchronous. q/out: [n_layers][n_decodes][n_q][d]. */
+int prism_engine_decode_host(prism_gpu* g, int engine_index, const void* new_k, const void* new_v, const void* q,
+                             void* out, float scale);
+int prism_engine_synchronize(prism_gpu* g, int engine_index);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* PRISM_CAPI_H */

@@ -1,0 +1,326 @@
+// C-ABI (include/prism_capi.h), GPU data-path subset — product only.
+// VMM device, pool mirror (K1), engine device (K1/K2/K3) and the host-buffer
+// end-to-end entry point.
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "host/pool_state.hpp"
+#include "host/vmm.hpp"
+#include "msim/kvcache_device.hpp"
+#include "prism_capi.h"
+#include "capi_handles.hpp"
+
+namespace pa = msim::pagealloc;
+namespace me = msim::engine;
+
+struct prism_device {
+    std::unique_ptr<prism::VmmDevice> dev;
+};
+
+namespace {
+
+template <class F>
+int dguard(F&& f) {
+    try {
+        f();
+        return PRISM_OK;
+    } catch (const msim::UsageError& e) {
+        prism_capi_detail::set_error(e.what());
+        return PRISM_E_USAGE;
+    } catch (const std::invalid_argument& e) {
+        prism_capi_detail::set_error(e.what());
+        return PRISM_E_ARG;
+    } catch (const std::out_of_range& e) {
+        prism_capi_detail::set_error(e.what());
+        return PRISM_E_ARG;
+    } catch (const std::exception& e) {
+        prism_capi_detail::set_error(e.what());
+        return PRISM_E_CUDA;
+    } catch (...) {
+        prism_capi_detail::set_error("unknown exception");
+        return PRISM_E_INTERNAL;
+    }
+}
+
+void need(const void* p, const char* what) {
+    if (!p) throw std::invalid_argument(std::string("null argument: ") + what);
+}
+
+me::Engine& engine_at(prism_gpu* g, int i) {
+    need(g, "gpu");
+    if (i < 0 || static_cast<std::size_t>(i) >= g->g.engines.size()) throw std::out_of_range("engine index");
+    return g->g.engines[static_cast<std::size_t>(i)];
+}
+const me::Engine& engine_at(const prism_gpu* g, int i) { return engine_at(const_cast<prism_gpu*>(g), i); }
+
+double percentile(std::vector<float> v, double q) {
+    if (v.empty()) return 0.0;
+    const std::size_t k = static_cast<std::size_t>(q * static_cast<double>(v.size() - 1) + 0.5);
+    std::nth_element(v.begin(), v.begin() + static_cast<std::ptrdiff_t>(k), v.end());
+    return v[k];
+}
+
+void check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+}  // namespace
+
+extern "C" {
+
+int prism_has_device_path(void) { return 1; }
+
+int prism_device_open(int ordinal, uint64_t page_bytes, prism_device** out) {
+    return dguard([&] {
+        need(out, "out");
+        auto* d = new prism_device();
+        try {
+            d->dev = prism::VmmDevice::open(ordinal, page_bytes);
+        } catch (...) {
+            delete d;
+            throw;
+        }
+        *out = d;
+    });
+}
+
+void prism_device_close(prism_device* d) { delete d; }
+
+int prism_device_capacity_pages(const prism_device* d, uint64_t reserve_bytes, uint64_t* out) {
+    return dguard([&] {
+        need(d, "device");
+        need(out, "out");
+        *out = d->dev->capacity_pages(reserve_bytes);
+    });
+}
+
+int prism_device_stats_get(const prism_device* d, prism_device_stats* out) {
+    return dguard([&] {
+        need(d, "device");
+        need(out, "out");
+        const prism::VmmStats& s = d->dev->stats();
+        out->maps = s.maps;
+        out->revived = s.revived;
+        out->creates = s.creates;
+        out->unmaps = s.unmaps;
+        out->driver_unmaps = s.driver_unmaps;
+        out->map_ns_total = s.map_ns_total;
+        out->unmap_ns_total = s.unmap_ns_total;
+        out->map_ns_p50 = percentile(s.map_ns, 0.5);
+        out->map_ns_p99 = percentile(s.map_ns, 0.99);
+        out->unmap_ns_p50 = percentile(s.unmap_ns, 0.5);
+        out->unmap_ns_p99 = percentile(s.unmap_ns, 0.99);
+        out->buffered = d->dev->buffered_handles();
+        out->cached = d->dev->cached_handles();
+        out->pending = d->dev->pending_unmaps();
+    });
+}
+
+int prism_device_reset_stats(prism_device* d) {
+    return dguard([&] {
+        need(d, "device");
+        d->dev->reset_stats();
+    });
+}
+
+int prism_device_reclaim(prism_device* d, int wait) {
+    return dguard([&] {
+        need(d, "device");
+        d->dev->reclaim(wait != 0);
+    });
+}
+
+int prism_device_synchronize(prism_device* d) {
+    return dguard([&] {
+        need(d, "device");
+        check(cudaStreamSynchronize(static_cast<cudaStream_t>(d->dev->stream())), "cudaStreamSynchronize");
+    });
+}
+
+void* prism_device_stream(const prism_device* d) { return d ? d->dev->stream() : nullptr; }
+
+int prism_ledger_attach_device(prism_ledger* l, prism_device* d) {
+    return dguard([&] {
+        need(l, "ledger");
+        l->l->attach_device(d ? d->dev.get() : nullptr);
+    });
+}
+
+int prism_pool_attach_mirror(prism_pool* p) {
+    return dguard([&] {
+        need(p, "pool");
+        prism::attach_pool_mirror(p->pool);
+    });
+}
+
+int prism_pool_sync_mirror(prism_pool* p, int32_t* out, size_t cap, size_t* n) {
+    return dguard([&] {
+        need(p, "pool");
+        const auto v = prism::sync_pool_mirror(p->pool);
+        if (n) *n = v.size();
+        if (out) {
+            if (v.size() > cap) throw std::invalid_argument("output buffer too small");
+            std::copy(v.begin(), v.end(), out);
+        }
+    });
+}
+
+int prism_pool_read_mirror(prism_pool* p, uint32_t* occ, size_t occ_cap, uint32_t* bits, size_t bits_cap) {
+    return dguard([&] {
+        need(p, "pool");
+        std::vector<std::uint32_t> o, b;
+        prism::read_pool_mirror(p->pool, o, b);
+        if (occ) {
+            if (o.size() > occ_cap) throw std::invalid_argument("occ buffer too small");
+            std::copy(o.begin(), o.end(), occ);
+        }
+        if (bits) {
+            if (b.size() > bits_cap) throw std::invalid_argument("bits buffer too small");
+            std::copy(b.begin(), b.end(), bits);
+        }
+    });
+}
+
+int prism_engine_attach_device(prism_gpu* g, int engine_index, const prism_engine_device_options* opts) {
+    return dguard([&] {
+        me::Engine& e = engine_at(g, engine_index);
+        prism::EngineDeviceOptions o;
+        if (opts) {
+            if (opts->table_capacity > 0) o.table_capacity = opts->table_capacity;
+            if (opts->max_decode_batch > 0) o.max_decode_batch = opts->max_decode_batch;
+            if (opts->max_step_tokens > 0) o.max_step_tokens = opts->max_step_tokens;
+        }
+        prism::attach_engine_device(e, g->g.ledger, o);
+    });
+}
+
+int prism_engine_step_info(const prism_gpu* g, int engine_index, int32_t* n_step_tokens, int32_t* n_decodes) {
+    return dguard([&] {
+        const me::Engine& e = engine_at(g, engine_index);
+        if (n_step_tokens) *n_step_tokens = prism::last_step_tokens(e);
+        if (n_decodes) *n_decodes = prism::last_step_decodes(e);
+    });
+}
+
+int prism_engine_step_decode_ids(const prism_gpu* g, int engine_index, uint64_t* out, size_t cap, size_t* n) {
+    return dguard([&] {
+        const auto& ids = prism::last_step_decode_ids(engine_at(g, engine_index));
+        if (n) *n = ids.size();
+        if (out) {
+            if (ids.size() > cap) throw std::invalid_argument("output buffer too small");
+            std::copy(ids.begin(), ids.end(), out);
+        }
+    });
+}
+
+int prism_engine_step_slots(const prism_gpu* g, int engine_index, int32_t* out, size_t cap, size_t* n) {
+    return dguard([&] {
+        const auto v = prism::last_step_slots(engine_at(g, engine_index));
+        if (n) *n = v.size();
+        if (out) {
+            if (v.size() > cap) throw std::invalid_argument("output buffer too small");
+            std::copy(v.begin(), v.end(), out);
+        }
+    });
+}
+
+int prism_engine_table_row(const prism_gpu* g, int engine_index, int64_t row, int32_t len, int32_t* out) {
+    return dguard([&] {
+        need(out, "out");
+        const auto v = prism::read_table_row(engine_at(g, engine_index), row, len);
+        std::copy(v.begin(), v.end(), out);
+    });
+}
+
+int prism_engine_append_kv(prism_gpu* g, int engine_index, int layer_begin, int layer_end, const void* k,
+                           const void* v) {
+    return dguard([&] {
+        need(k, "k");
+        need(v, "v");
+        prism::append_step_kv(engine_at(g, engine_index), layer_begin, layer_end, k, v);
+    });
+}
+
+int prism_engine_append_kv_synthetic(prism_gpu* g, int engine_index, int layer_begin, int layer_end, uint64_t seed) {
+    return dguard([&] { prism::append_step_kv_synthetic(engine_at(g, engine_index), layer_begin, layer_end, seed); });
+}
+
+}  // extern "C"
+
+namespace prism {
+void launch_decode_attention(class EngineDeviceImpl& d, int layer, const void* q, void* out, float scale, int chunk);
+EngineDeviceImpl& impl_of(const msim::engine::Engine& eng);
+}  // namespace prism
+
+extern "C" {
+
+int prism_engine_decode_attention(prism_gpu* g, int engine_index, int layer, const void* q, void* out, float scale,
+                                  int32_t chunk) {
+    return dguard([&] {
+        need(q, "q");
+        need(out, "out");
+        prism::launch_decode_attention(prism::impl_of(engine_at(g, engine_index)), layer, q, out, scale, chunk);
+    });
+}
+
+int prism_engine_synth_q(prism_gpu* g, int engine_index, int layer, uint64_t seed, float q_scale, void* q) {
+    return dguard([&] {
+        need(q, "q");
+        prism::synth_decode_q(engine_at(g, engine_index), layer, seed, q_scale, q);
+    });
+}
+
+int prism_engine_decode_host(prism_gpu* g, int engine_index, const void* new_k, const void* new_v, const void* q,
+                             void* out, float scale) {
+    return dguard([&] {
+        need(q, "q");
+        need(out, "out");
+        me::Engine& e = engine_at(g, engine_index);
+        const me::ModelSpec& m = *e.model;
+        auto stream = static_cast<cudaStream_t>(prism::engine_stream(e));
+        const int n_tok = prism::last_step_tokens(e);
+        const int n_dec = prism::last_step_decodes(e);
+        const std::size_t kv_bytes = static_cast<std::size_t>(m.n_layers) * n_tok * m.n_kv_heads * m.head_dim * 2;
+        const std::size_t q_layer = static_cast<std::size_t>(n_dec) * m.n_q_heads * m.head_dim * 2;
+        // Device staging (grown on demand, kept across calls).
+        static thread_local void* d_buf = nullptr;
+        static thread_local std::size_t d_cap = 0;
+        const std::size_t need_bytes = 2 * kv_bytes + 2 * q_layer * m.n_layers + 256;
+        if (need_bytes > d_cap) {
+            if (d_buf) check(cudaFree(d_buf), "cudaFree");
+            check(cudaMalloc(&d_buf, need_bytes), "cudaMalloc");
+            d_cap = need_bytes;
+        }
+        char* dk = static_cast<char*>(d_buf);
+        char* dv = dk + kv_bytes;
+        char* dq = dv + kv_bytes;
+        char* dout = dq + q_layer * m.n_layers;
+        if (new_k && new_v && n_tok) {
+            check(cudaMemcpyAsync(dk, new_k, kv_bytes, cudaMemcpyHostToDevice, stream), "H2D k");
+            check(cudaMemcpyAsync(dv, new_v, kv_bytes, cudaMemcpyHostToDevice, stream), "H2D v");
+            prism::append_step_kv(e, 0, m.n_layers, dk, dv);
+        }
+        if (n_dec) {
+            check(cudaMemcpyAsync(dq, q, q_layer * m.n_layers, cudaMemcpyHostToDevice, stream), "H2D q");
+            for (int layer = 0; layer < m.n_layers; ++layer) {
+                prism::launch_decode_attention(prism::impl_of(e), layer, dq + q_layer * layer, dout + q_layer * layer,
+                                               scale, 0);
+            }
+            check(cudaMemcpyAsync(out, dout, q_layer * m.n_layers, cudaMemcpyDeviceToHost, stream), "D2H out");
+        }
+        check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    });
+}
+
+int prism_engine_synchronize(prism_gpu* g, int engine_index) {
+    return dguard([&] {
+        auto stream = static_cast<cudaStream_t>(prism::engine_stream(engine_at(g, engine_index)));
+        check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+// Private declarations shared by the prism-b200 CUDA translation units:
+// the GPU-resident slot mirror of a pool (DevicePool) and the GPU half of an
+// engine (EngineDeviceImpl).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <unordered_map>
+#include <vector>
+
+#include "cuda/common.cuh"
+#include "host/engine_device.hpp"
+#include "host/pool_state.hpp"
+#include "host/vmm.hpp"
+#include "msim/kvcache_device.hpp"
+
+namespace prism {
+
+// Device copy of msim::pagealloc::detail::DeviceOp (same layout).
+struct DevOp {
+    std::uint32_t kind;
+    std::uint32_t count;
+    std::int64_t dest;
+    std::int64_t first;
+};
+static_assert(sizeof(DevOp) == sizeof(msim::pagealloc::detail::DeviceOp), "DevOp layout");
+
+// Host staging that can be reused only after the copy that read it finished.
+template <typename T>
+struct Staging {
+    T* host = nullptr;    // pinned
+    T* dev = nullptr;
+    std::size_t cap = 0;
+    cudaEvent_t done = nullptr;
+
+    void ensure(std::size_t n) {
+        if (done) PRISM_CUDA(cudaEventSynchronize(done));
+        if (n <= cap) return;
+        release();
+        cap = std::max<std::size_t>(n, 256);
+        PRISM_CUDA(cudaMallocHost(&host, cap * sizeof(T)));
+        PRISM_CUDA(cudaMalloc(&dev, cap * sizeof(T)));
+    }
+    // Copies host[0, n) to dev on stream and marks the staging busy.
+    void upload(std::size_t n, cudaStream_t s) {
+        if (!done) PRISM_CUDA(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        if (n) PRISM_CUDA(cudaMemcpyAsync(dev, host, n * sizeof(T), cudaMemcpyHostToDevice, s));
+        PRISM_CUDA(cudaEventRecord(done, s));
+    }
+    void release() {
+        if (host) cudaFreeHost(host);
+        if (dev) cudaFree(dev);
+        host = nullptr;
+        dev = nullptr;
+        cap = 0;
+    }
+    ~Staging() {
+        release();
+        if (done) cudaEventDestroy(done);
+    }
+};
+
+// GPU-resident slot state of one pool: occupancy per page and slot bitmaps
+// (u32 words). Updated only by K1 from the pool's op log.
+class DevicePool {
+public:
+    DevicePool(const msim::pagealloc::detail::PoolState& s, int device);
+    ~DevicePool();
+    DevicePool(const DevicePool&) = delete;
+    DevicePool& operator=(const DevicePool&) = delete;
+
+    // Replays and clears s.ops / s.freed_slots on `stream`. Slot ids of every
+    // logged allocation are written, in order, to out[0 .. total) (out may be
+    // null when total == 0) and, for ops with dest >= 0, to table[dest + i].
+    // Returns the number of allocated slots.
+    std::int64_t replay(msim::pagealloc::detail::PoolState& s, std::int32_t* table, std::int32_t* out,
+                        std::int64_t out_cap, cudaStream_t stream);
+    int status(cudaStream_t stream);  // 0 = consistent with the host allocator
+
+    std::uint32_t vpages = 0, tpp = 0, words = 0;
+    std::uint32_t* occ = nullptr;   // [vpages]
+    std::uint32_t* bits = nullptr;  // [vpages * words]
+    int* d_status = nullptr;
+    Staging<DevOp> ops;
+    Staging<std::int32_t> freed;
+};
+
+struct TokenMeta {
+    std::uint64_t request;  // ~0ull: dead (its request was preempted in the same step)
+    std::uint32_t pos;
+    std::uint32_t pad;
+};
+
+struct DecodeDesc {
+    std::int64_t row;
+    std::int32_t ctx;
+    std::int32_t pad;
+    std::uint64_t request;
+};
+
+class EngineDeviceImpl final : public EngineDevice {
+public:
+    EngineDeviceImpl(msim::engine::Engine& eng, msim::pagealloc::PhysicalLedger& ledger,
+                     const EngineDeviceOptions& opts);
+    ~EngineDeviceImpl() override;
+
+    std::int64_t acquire_row(std::int64_t capacity) override;
+    void release_row(std::int64_t row) override;
+    void begin_step(msim::engine::Engine& eng) override;
+    void end_step(msim::engine::Engine& eng, const msim::engine::IterationOutcome& out,
+                  const std::vector<StepDecode>& decodes, std::uint64_t prefill_id, std::int64_t prefill_row,
+                  std::int32_t prefill_first, std::int32_t prefill_tokens) override;
+
+    void grow_table(std::int64_t need);
+    float* attn_workspace(std::size_t floats);
+    int* attn_counters(std::size_t n);
+
+    VmmDevice* vmm = nullptr;
+    cudaStream_t stream = nullptr;
+    msim::pagealloc::detail::PoolState* pool = nullptr;
+    KvGeom geom{};
+    int n_q = 0, n_kv = 0, head_dim = 0, group = 0, n_layers = 0;
+    EngineDeviceOptions opts;
+
+    // block table arena
+    std::int32_t* table = nullptr;
+    std::int64_t table_cap = 0;
+    std::map<std::int64_t, std::int64_t> free_ranges;        // offset -> length
+    std::unordered_map<std::int64_t, std::int64_t> row_len;  // offset -> length
+
+    // last step
+    std::int32_t* step_slots = nullptr;  // [max_step_tokens]
+    int step_tokens = 0;
+    int step_decodes = 0;
+    std::vector<std::uint64_t> decode_ids;
+    Staging<TokenMeta> token_meta;
+    Staging<DecodeDesc> decode_desc;
+
+    float* workspace = nullptr;
+    std::size_t workspace_floats = 0;
+    int* counters = nullptr;
+    std::size_t counters_n = 0;
+};
+
+EngineDeviceImpl& impl_of(const msim::engine::Engine& eng);
+
+}  // namespace prism

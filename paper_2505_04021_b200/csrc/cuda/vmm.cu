@@ -1,0 +1,301 @@
+// prism::VmmDevice implementation: CUDA VMM (driver API) behind the ledger.
+// Driver entry points are resolved at run time through the runtime's
+// cudaGetDriverEntryPoint, so the library loads on machines without a driver
+// (the CPU build/test container) and only fails when a device is opened.
+#include <cuda.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+
+#include "cuda/common.cuh"
+#include "host/vmm.hpp"
+
+namespace prism {
+
+namespace {
+
+struct Driver {
+    decltype(&cuMemAddressReserve) reserve = nullptr;
+    decltype(&cuMemAddressFree) addr_free = nullptr;
+    decltype(&cuMemCreate) create = nullptr;
+    decltype(&cuMemRelease) release = nullptr;
+    decltype(&cuMemMap) map = nullptr;
+    decltype(&cuMemUnmap) unmap = nullptr;
+    decltype(&cuMemSetAccess) set_access = nullptr;
+    decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+    decltype(&cuDeviceGetAttribute) attribute = nullptr;
+    bool loaded = false;
+};
+
+Driver& drv() {
+    static Driver d;
+    return d;
+}
+
+template <typename F>
+void resolve(const char* name, F& fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    PRISM_CUDA(cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw std::runtime_error(std::string("driver symbol missing: ") + name);
+    fn = reinterpret_cast<F>(p);
+}
+
+void load_driver() {
+    Driver& d = drv();
+    if (d.loaded) return;
+    resolve("cuMemAddressReserve", d.reserve);
+    resolve("cuMemAddressFree", d.addr_free);
+    resolve("cuMemCreate", d.create);
+    resolve("cuMemRelease", d.release);
+    resolve("cuMemMap", d.map);
+    resolve("cuMemUnmap", d.unmap);
+    resolve("cuMemSetAccess", d.set_access);
+    resolve("cuMemGetAllocationGranularity", d.granularity);
+    resolve("cuDeviceGetAttribute", d.attribute);
+    d.loaded = true;
+}
+
+void cu_check(CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) throw std::runtime_error(std::string("CUDA driver error ") + std::to_string(r) + " in " + what);
+}
+
+using Clock = std::chrono::steady_clock;
+double ns_since(Clock::time_point t0) {
+    return std::chrono::duration<double, std::nano>(Clock::now() - t0).count();
+}
+
+constexpr std::size_t kMaxSamples = 1 << 16;
+
+void sample(std::vector<float>& ring, double ns) {
+    if (ring.size() < kMaxSamples) ring.push_back(static_cast<float>(ns));
+}
+
+CUmemAllocationProp& prop_of(void* p) { return *static_cast<CUmemAllocationProp*>(p); }
+CUmemAccessDesc& access_of(void* p) { return *static_cast<CUmemAccessDesc*>(p); }
+
+}  // namespace
+
+std::unique_ptr<VmmDevice> VmmDevice::open(int ordinal, std::uint64_t page_bytes) {
+    int count = 0;
+    PRISM_CUDA(cudaGetDeviceCount(&count));
+    if (ordinal < 0 || ordinal >= count) throw std::runtime_error("VmmDevice: no CUDA device " + std::to_string(ordinal));
+    PRISM_CUDA(cudaSetDevice(ordinal));
+    PRISM_CUDA(cudaFree(nullptr));  // create the primary context
+    load_driver();
+    int vmm = 0;
+    cu_check(drv().attribute(&vmm, CU_DEVICE_ATTRIBUTE_VIRTUAL_MEMORY_MANAGEMENT_SUPPORTED, ordinal),
+             "cuDeviceGetAttribute");
+    if (!vmm) throw std::runtime_error("VmmDevice: device does not support virtual memory management");
+
+    std::unique_ptr<VmmDevice> dev(new VmmDevice());
+    dev->ordinal_ = ordinal;
+    dev->page_bytes_ = page_bytes;
+    auto* prop = new CUmemAllocationProp();
+    std::memset(prop, 0, sizeof(*prop));
+    prop->type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    prop->location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    prop->location.id = ordinal;
+    dev->prop_ = prop;
+    auto* acc = new CUmemAccessDesc();
+    acc->location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc->location.id = ordinal;
+    acc->flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    dev->access_desc_ = acc;
+    std::size_t gran = 0;
+    cu_check(drv().granularity(&gran, prop, CU_MEM_ALLOC_GRANULARITY_MINIMUM), "cuMemGetAllocationGranularity");
+    if (gran == 0 || page_bytes % gran != 0) {
+        throw std::runtime_error("VmmDevice: page size is not a multiple of the VMM granularity (" +
+                                 std::to_string(gran) + ")");
+    }
+    cudaStream_t s = nullptr;
+    PRISM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    dev->stream_ = s;
+    return dev;
+}
+
+VmmDevice::~VmmDevice() {
+    try {
+        cudaSetDevice(ordinal_);
+        reclaim(true);
+        for (auto& [va, h] : live_) {
+            drv().unmap(va, page_bytes_);
+            drv().release(h);
+        }
+        for (auto h : buffer_) drv().release(h);
+        for (auto h : taken_) drv().release(h);
+        for (auto h : cache_) drv().release(h);
+        for (void* e : fences_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
+        if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
+    } catch (...) {
+    }
+    delete static_cast<CUmemAllocationProp*>(prop_);
+    delete static_cast<CUmemAccessDesc*>(access_desc_);
+}
+
+std::uint64_t VmmDevice::reserve(std::uint64_t pages) {
+    CUdeviceptr va = 0;
+    cu_check(drv().reserve(&va, pages * page_bytes_, page_bytes_, 0, 0), "cuMemAddressReserve");
+    return static_cast<std::uint64_t>(va);
+}
+
+void VmmDevice::release(std::uint64_t va, std::uint64_t pages) {
+    const std::uint64_t end = va + pages * page_bytes_;
+    for (auto it = pending_.begin(); it != pending_.end();) {
+        if (it->first >= va && it->first < end) {
+            driver_unmap(it->first);
+            drop_handle(it->second.handle);
+            it = pending_.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    for (auto it = live_.begin(); it != live_.end();) {
+        if (it->first >= va && it->first < end) {
+            driver_unmap(it->first);
+            drop_handle(it->second);
+            it = live_.erase(it);
+        } else {
+            ++it;
+        }
+    }
+    cu_check(drv().addr_free(static_cast<CUdeviceptr>(va), pages * page_bytes_), "cuMemAddressFree");
+}
+
+std::uint64_t VmmDevice::new_handle() {
+    if (!cache_.empty()) {
+        const std::uint64_t h = cache_.back();
+        cache_.pop_back();
+        return h;
+    }
+    CUmemGenericAllocationHandle h = 0;
+    CUresult r = drv().create(&h, page_bytes_, &prop_of(prop_), 0);
+    if (r == CUDA_ERROR_OUT_OF_MEMORY && !pending_.empty()) {
+        reclaim(true);  // physical pages are parked behind deferred unmaps
+        if (!cache_.empty()) return new_handle();
+        r = drv().create(&h, page_bytes_, &prop_of(prop_), 0);
+    }
+    cu_check(r, "cuMemCreate");
+    ++stats_.creates;
+    return static_cast<std::uint64_t>(h);
+}
+
+void VmmDevice::drop_handle(std::uint64_t h) {
+    if (cache_.size() < cache_limit_) {
+        cache_.push_back(h);
+    } else {
+        drv().release(static_cast<CUmemGenericAllocationHandle>(h));
+    }
+}
+
+void VmmDevice::map(std::uint64_t va, bool from_buffer) {
+    const auto t0 = Clock::now();
+    ++stats_.maps;
+    const auto p = pending_.find(va);
+    if (p != pending_.end()) {
+        // Unmapped logically, never unmapped physically: revive in place and
+        // give the buffer handle (if any) back to the cache.
+        live_.emplace(va, p->second.handle);
+        pending_.erase(p);
+        if (from_buffer && !taken_.empty()) {
+            drop_handle(taken_.back());
+            taken_.pop_back();
+        }
+        ++stats_.revived;
+    } else {
+        std::uint64_t h;
+        if (from_buffer && !taken_.empty()) {
+            h = taken_.back();
+            taken_.pop_back();
+        } else {
+            h = new_handle();
+        }
+        cu_check(drv().map(static_cast<CUdeviceptr>(va), page_bytes_, 0, static_cast<CUmemGenericAllocationHandle>(h), 0),
+                 "cuMemMap");
+        cu_check(drv().set_access(static_cast<CUdeviceptr>(va), page_bytes_, &access_of(access_desc_), 1),
+                 "cuMemSetAccess");
+        live_.emplace(va, h);
+    }
+    const double ns = ns_since(t0);
+    stats_.map_ns_total += ns;
+    sample(stats_.map_ns, ns);
+}
+
+void VmmDevice::unmap(std::uint64_t va) {
+    const auto t0 = Clock::now();
+    const auto it = live_.find(va);
+    if (it == live_.end()) throw std::runtime_error("VmmDevice::unmap: page not mapped");
+    pending_.emplace(va, Pending{it->second, epoch_});
+    live_.erase(it);
+    ++stats_.unmaps;
+    stats_.unmap_ns_total += ns_since(t0);
+}
+
+void VmmDevice::driver_unmap(std::uint64_t va) {
+    const auto t0 = Clock::now();
+    cu_check(drv().unmap(static_cast<CUdeviceptr>(va), page_bytes_), "cuMemUnmap");
+    ++stats_.driver_unmaps;
+    const double ns = ns_since(t0);
+    stats_.unmap_ns_total += ns;
+    sample(stats_.unmap_ns, ns);
+}
+
+void VmmDevice::fence() {
+    cudaEvent_t ev = nullptr;
+    PRISM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    PRISM_CUDA(cudaEventRecord(ev, static_cast<cudaStream_t>(stream_)));
+    fences_.push_back(ev);
+    ++epoch_;
+}
+
+void VmmDevice::reclaim(bool wait) {
+    if (wait) {
+        PRISM_CUDA(cudaDeviceSynchronize());
+        fenced_epoch_ = epoch_;
+    }
+    // Retire completed fences in order. fences_[0] has index fenced_epoch_.
+    std::size_t done = 0;
+    while (done < fences_.size()) {
+        const cudaError_t q = wait ? cudaSuccess : cudaEventQuery(static_cast<cudaEvent_t>(fences_[done]));
+        if (q == cudaErrorNotReady) break;
+        PRISM_CUDA(q);
+        ++done;
+    }
+    for (std::size_t i = 0; i < done; ++i) cudaEventDestroy(static_cast<cudaEvent_t>(fences_[i]));
+    fences_.erase(fences_.begin(), fences_.begin() + static_cast<std::ptrdiff_t>(done));
+    if (!wait) fenced_epoch_ += done;
+    if (pending_.empty()) return;
+    for (auto it = pending_.begin(); it != pending_.end();) {
+        // A page unmapped at epoch e is safe once fence e (the first fence
+        // recorded after the unmap) has completed.
+        if (wait || it->second.epoch < fenced_epoch_) {
+            driver_unmap(it->first);
+            drop_handle(it->second.handle);
+            it = pending_.erase(it);
+        } else {
+            ++it;
+        }
+    }
+}
+
+void VmmDevice::grow_buffer(std::uint64_t n) {
+    for (std::uint64_t i = 0; i < n; ++i) buffer_.push_back(new_handle());
+}
+
+void VmmDevice::take_buffer(std::uint64_t n) {
+    for (std::uint64_t i = 0; i < n && !buffer_.empty(); ++i) {
+        taken_.push_back(buffer_.back());
+        buffer_.pop_back();
+    }
+}
+
+void VmmDevice::reset_stats() { stats_ = VmmStats{}; }
+
+std::uint64_t VmmDevice::capacity_pages(std::uint64_t reserve_bytes) const {
+    std::size_t free_b = 0, total_b = 0;
+    PRISM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    return free_b > reserve_bytes ? (free_b - reserve_bytes) / page_bytes_ : 0;
+}
+
+}  // namespace prism
