@@ -328,6 +328,9 @@ typedef struct {
 int prism_device_stats_get(const prism_device* d, prism_device_stats* out);
 int prism_device_reset_stats(prism_device* d);
 int prism_device_reclaim(prism_device* d, int wait);
+/* Record a fence on the device stream: pages unmapped before it become
+ * reclaimable (cuMemUnmap'ed by prism_device_reclaim(d, 0)) once it passes. */
+int prism_device_fence(prism_device* d);
 int prism_device_synchronize(prism_device* d);
 void* prism_device_stream(const prism_device* d); /* cudaStream_t of the GPU's work stream */
 /* PhysicalLedger::attach_device; before any pool is created on the ledger. */

@@ -134,6 +134,13 @@ int prism_device_reclaim(prism_device* d, int wait) {
     });
 }
 
+int prism_device_fence(prism_device* d) {
+    return dguard([&] {
+        need(d, "device");
+        d->dev->fence();
+    });
+}
+
 int prism_device_synchronize(prism_device* d) {
     return dguard([&] {
         need(d, "device");

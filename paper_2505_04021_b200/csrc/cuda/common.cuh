@@ -26,17 +26,20 @@ struct KvGeom {
     std::uint64_t base;        // device VA of page 0
     std::uint64_t page_bytes;  // 2 MiB
     std::uint32_t tpp;         // tokens per page
-    std::uint32_t magic;       // page = (sid * magic) >> 40, exact for sid * tpp < 2^40
+    std::uint64_t magic;       // page = (sid * magic) >> 40 (see div_magic40)
     std::int32_t n_layers;
     std::int32_t n_kv;
     std::int32_t head_dim;
 };
 
-__host__ __device__ inline std::uint32_t div_magic40(std::uint32_t tpp) {
-    return static_cast<std::uint32_t>((std::uint64_t{1} << 40) / tpp + 1);
+// floor(sid / tpp) as one 64-bit multiply + shift: magic = floor(2^40/tpp)+1
+// is exact for sid * tpp < 2^40; slot ids are < 2^24 and tpp <= 1024 (the
+// device path's limits), and sid * magic < 2^24 * 2^40 fits in 64 bits.
+__host__ __device__ inline std::uint64_t div_magic40(std::uint32_t tpp) {
+    return (std::uint64_t{1} << 40) / tpp + 1;
 }
 
-__device__ __forceinline__ std::uint32_t slot_page(std::uint32_t sid, std::uint32_t magic) {
+__device__ __forceinline__ std::uint32_t slot_page(std::uint32_t sid, std::uint64_t magic) {
     return static_cast<std::uint32_t>((static_cast<std::uint64_t>(sid) * magic) >> 40);
 }
 

@@ -43,7 +43,8 @@ constexpr std::uint32_t kAlloc = 1, kFreeList = 2, kFreeRow = 3;
 struct K1Args {
     std::uint32_t* occ;
     std::uint32_t* bits;
-    std::uint32_t vpages, tpp, words, magic;
+    std::uint32_t vpages, tpp, words;
+    std::uint64_t magic;
     const DevOp* ops;
     int n_ops;
     const std::int32_t* freed;
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_slot_alloc(K1Args a) {
         const DevOp op = a.ops[i];
         if (op.kind != kAlloc) {
             for (std::uint32_t j = tid; j < op.count; j += kThreads) {
-                const std::int32_t sid = op.kind == kFreeRow ? a.table[op.first + j] : a.freed[op.first + j];
+                const std::int32_t sid = op.kind == kFreeRow ? __ldcg(&a.table[op.first + j]) : __ldcg(&a.freed[op.first + j]);
                 free_slot(a, static_cast<std::uint32_t>(sid));
             }
             __syncthreads();
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1) k1_slot_alloc(K1Args a) {
                 const std::uint32_t page = static_cast<std::uint32_t>(keys[tid] & 0xffffffffu);
                 const std::uint32_t f = static_cast<std::uint32_t>(keys[tid] >> 32);
                 const std::uint32_t used = min(f, n - start[tid]);
-                a.occ[page] += used;
+                atomicAdd(&a.occ[page], used);  // L2 RMW: a plain += could read a stale L1 line
             }
             __syncthreads();
             done += n;
@@ -289,7 +290,10 @@ void destroy_device_pool(DevicePool* p) { delete p; }
 
 DevicePool::DevicePool(const msim::pagealloc::detail::PoolState& s, int device) {
     if (s.tpp > kMaxTpp) throw std::runtime_error("device pool: tokens per page above 1024 is not supported");
-    if (s.vpages * s.tpp >= (1ull << 31)) throw std::runtime_error("device pool: slot ids exceed int32");
+    // slot ids are int32 and div_magic40 is exact while sid * tpp < 2^40.
+    if (s.vpages * s.tpp >= (1ull << 31) || s.vpages * s.tpp * s.tpp >= (1ull << 40)) {
+        throw std::runtime_error("device pool: slot id range too large for the device block table");
+    }
     PRISM_CUDA(cudaSetDevice(device));
     vpages = static_cast<std::uint32_t>(s.vpages);
     tpp = static_cast<std::uint32_t>(s.tpp);
