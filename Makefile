@@ -28,6 +28,7 @@ HEADERS   := $(wildcard include/*.h include/msim/*.hpp $(SRC)/*.hpp $(SRC)/host/
 
 .PHONY: all oracle clean
 all: $(LIB)
+	$(MAKE) -C oracle
 
 $(BUILD)/%.o: $(SRC)/%.cpp $(HEADERS)
 	@mkdir -p $(dir $@)

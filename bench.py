@@ -1,0 +1,490 @@
+"""prism-b200 benchmark (driver contract: one JSON line on rank 0).
+
+Workload = BASELINE.json config 1 ("C1"): two Llama-3-8B-shaped models
+(32 layers, 32 q / 8 kv heads, d=128, bf16 KV, 2 MiB pages, 16 tokens/page)
+time-sharing one B200, 64 decoding sequences per model at ~2K context; the
+prompts' lengths/arrivals come from a seeded Poisson trace (synth_trace) and
+all 64 are admitted before timing. One STEP = for each model: engine::step
+(host scheduling + VMM page maps + K1 batched device slot allocation / block
+table update) + K2 (append this step's K/V rows for all 32 layers) + K3 x 32
+(paged GQA decode attention, one launch per layer). No GEMMs exist on this
+path (the reference has no model): tokens/s is attention-path decode
+throughput. KV per step is 32 GiB >> 126 MB L2, so no L2 flush is needed.
+
+value   = decode tokens/s over K device-timed steps, inputs resident in HBM
+          (whole job; max over ranks for N > 1, weak scaling: 2 models/GPU)
+e2e     = the same through the C-ABI with HOST buffers: per step the new K/V
+          rows and q for all layers are copied from pinned host memory and the
+          attention output copied back (prism_engine_decode_host)
+roofline: K3, algorithmic bytes (K+V rows of every context token + q + out)
+          per launch / mean CUDA-event duration of the K3 launches in the
+          timed region, against MEASURED_PEAKS.json hbm_gbs
+cpu_baseline: reference engine::step (oracle/_ref, the reference compiled
+          from its sources) for the allocation half + this repo's CPU port of
+          paged attention (oracle/restate) on a bounded sample, N=1 rank 0 only
+--impl reference: that CPU path as the timed arm (no GPU work).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "paged decode-attn HBM GB/s (% of peak); KV page map/unmap µs; tokens/s/GPU"
+SEED = 20251017
+TRACE_SEED = 42
+L, NQ, NKV, D = 32, 32, 8, 128
+B_PER_MODEL = 64
+CTX = 2048
+MODELS_PER_GPU = 2
+WORKLOAD = ("C1: 2 x Llama-3-8B-shaped models (32L, 32q/8kv heads, d=128) time-sharing 1 B200; "
+            "64 decode seqs x 2K ctx per model; prompts from a seeded Poisson trace, admitted before timing")
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------- workload
+
+
+def c1_requests(n_models: int, rank: int):
+    """Per model: 64 requests from a seeded Poisson trace (prompt ~2K)."""
+    from paper_2505_04021_b200 import msim
+
+    out = []
+    for m in range(n_models):
+        mid = f"llama3-8b#{rank}.{m}"
+        prof = msim.ModelProfile(mid, [(0.0, 60.0, 30.0)], prompt_median=CTX - 1, prompt_sigma=0.0,
+                                 output_median=256, output_sigma=0.4)
+        trace = [e for e in msim.synth_trace([prof], TRACE_SEED) if e.model_id == mid][:B_PER_MODEL]
+        out.append((mid, trace))
+    return out
+
+
+class Model:
+    def __init__(self, gpu, mid, trace, max_steps):
+        from paper_2505_04021_b200 import msim
+
+        spec = msim.ModelSpec.llm(mid, L, NQ, NKV, D, weight_bytes=0, chunk_size=4096)
+        act = gpu.activate(spec)
+        assert act is not None
+        gpu.finish_activation(act.engine_index)
+        self.eng = gpu.engine(act.engine_index)
+        self.eng.attach_device(max_decode_batch=B_PER_MODEL, max_step_tokens=CTX + B_PER_MODEL + 8)
+        for i, ev in enumerate(trace):
+            # Outputs long enough that no request completes inside the run:
+            # request k already decodes while requests k+1.. are prefilled.
+            self.eng.push(i + 1, ev.prompt_tokens, 1_000_000)
+        self.mid = mid
+
+
+def setup_gpu(rank: int, n_models: int, max_steps: int):
+    import torch
+
+    from paper_2505_04021_b200 import msim
+
+    dev = msim.Device(torch.cuda.current_device())
+    tpp = (2 << 20) // (2 * L * NKV * D * 2)
+    # contexts grow by one token per decode step: B_PER_MODEL prefill steps
+    # (earlier requests decode meanwhile) + every later step of the run
+    grow = B_PER_MODEL + max_steps
+    pages = n_models * (B_PER_MODEL * (CTX + grow + tpp) // tpp + 64)
+    gpu = msim.GpuState(rank, pages + 64)
+    gpu.ledger.attach_device(dev)
+    gpu.ledger.refill_buffer(8)
+    models = [Model(gpu, mid, trace, max_steps) for mid, trace in c1_requests(n_models, rank)]
+    # prefill: one 2K chunk per step (allocation + K2 synthetic K/V writes)
+    for m in models:
+        while True:
+            b, q = m.eng.counts()
+            if q == 0 and all(r.prompt_done == r.prompt_tokens for r in m.eng.batch()):
+                break
+            m.eng.step()
+            m.eng.append_kv_synthetic(0, L, SEED)
+    dev.synchronize()
+    return dev, gpu, models
+
+
+def run_steps(models, n, q_bufs, out_bufs, scale, k3_events=None):
+    """n decode steps over all models; returns our kernel-launch count."""
+    launches = 0
+    for _ in range(n):
+        for mi, m in enumerate(models):
+            m.eng.step()                       # host + K1
+            m.eng.append_kv_synthetic(0, L, SEED)  # K2
+            launches += 2
+            q, o = q_bufs[mi], out_bufs[mi]
+            for layer in range(L):
+                if k3_events is not None:
+                    s, e = k3_events.pop()
+                    s.record(k3_events.stream)
+                m.eng.decode_attention(layer, q[layer].data_ptr(), o[layer].data_ptr(), scale)  # K3
+                if k3_events is not None:
+                    e.record(k3_events.stream)
+                    k3_events.used.append((s, e))
+                launches += 1
+    return launches
+
+
+class EventPool(list):
+    def __init__(self, n, stream):
+        import torch
+
+        super().__init__((torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                         for _ in range(n))
+        self.stream = stream
+        self.used = []
+
+
+def k3_bytes(models):
+    """Algorithmic bytes of one K3 launch per model (current contexts)."""
+    tot = []
+    for m in models:
+        ctxs = [r.live_slots() for r in m.eng.batch()]
+        tot.append(sum(ctxs) * NKV * D * 2 * 2 + 2 * len(ctxs) * NQ * D * 2)
+    return tot
+
+
+def gpu_arm(args, rank, world):
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    steps, warm = args.steps, args.warmup
+    dev, gpu, models = setup_gpu(rank, MODELS_PER_GPU, steps * 2 + warm * 2 + 8)
+    stream = torch.cuda.ExternalStream(dev.stream())
+    q_bufs, out_bufs = [], []
+    for m in models:
+        q = torch.empty((L, B_PER_MODEL, NQ, D), dtype=torch.bfloat16, device="cuda")
+        q_bufs.append(q)
+        out_bufs.append(torch.empty_like(q))
+    scale = 1.0 / math.sqrt(D)
+    # q content: synthetic at each request's current position (per layer)
+    for mi, m in enumerate(models):
+        m.eng.step()
+        m.eng.append_kv_synthetic(0, L, SEED)
+        for layer in range(L):
+            m.eng.synth_q(layer, SEED, 1.0, q_bufs[mi][layer].data_ptr())
+    run_steps(models, warm, q_bufs, out_bufs, scale)
+    dev.synchronize()
+    dev.reset_stats()
+
+    # ---- value: device-timed K steps, inputs resident in HBM
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    events = EventPool(steps * len(models) * L, stream)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    dev.synchronize()
+    with ClockSampler(torch.cuda.current_device()) as clk:
+        start.record(stream)
+        launches = run_steps(models, steps, q_bufs, out_bufs, scale, events)
+        end.record(stream)
+        end.synchronize()
+    torch.cuda.synchronize()
+    ms_total = start.elapsed_time(end)
+    if world > 1:
+        dist.barrier()
+    bytes_per_launch = k3_bytes(models)
+    k3_ms = [s.elapsed_time(e) for s, e in events.used]
+    vstats = dev.stats()
+
+    ms_max = ms_total
+    if world > 1:
+        t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    tokens = steps * len(models) * B_PER_MODEL * world
+    value = tokens / (ms_max / 1e3)
+
+    # ---- e2e through the C-ABI with host buffers
+    e2e = e2e_arm(models, steps, scale, dev, world)
+
+    peak, peak_kind = measured_peaks()
+    # per-launch algorithmic bytes (contexts grow by 1 per step; use the mean)
+    avg_bytes = statistics.mean(bytes_per_launch) - 0.5 * steps * NKV * D * 4 * B_PER_MODEL
+    avg_ms = statistics.mean(k3_ms)
+    achieved = avg_bytes / (avg_ms / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "k3_dram_traffic.json")
+    if os.path.exists(tp):
+        with open(tp) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    res = {
+        "metric": METRIC,
+        "value": round(value, 1),
+        "unit": "tokens/s",
+        "n_gpus": world,
+        "steps": steps,
+        "warmup": warm,
+        "ms_per_step": round(ms_max / steps, 4),
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "bf16 (fp32 accumulate)",
+        "data": "synthetic (seeded hash K/V/Q content; prompts from seeded Poisson trace)",
+        "config": {"workload": WORKLOAD, "models_per_gpu": MODELS_PER_GPU, "decode_seqs_per_model": B_PER_MODEL,
+                   "ctx": CTX, "layers": L, "q_heads": NQ, "kv_heads": NKV, "head_dim": D, "page_bytes": 2 << 20,
+                   "tokens_per_page": 16, "parallelism": f"model placement, {world} GPU(s), no collective",
+                   "l2": "inputs larger than L2 (32 GiB KV read per step)"},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind,
+                     "kernel": "k3_decode (paged GQA decode attention)",
+                     "k3_mean_ms": round(avg_ms, 5), "k3_bytes_per_launch": int(avg_bytes),
+                     "k3_share_of_step": round(sum(k3_ms) / ms_total, 4)},
+        "page_map": page_map_summary(vstats, steps),
+        "clocks": clk.summary(),
+    }
+    return res
+
+
+def e2e_arm(models, steps, scale, dev, world):
+    import torch
+
+    n_tok = B_PER_MODEL
+    kv_elems = L * n_tok * NKV * D
+    q_elems = L * B_PER_MODEL * NQ * D
+    host_k = torch.empty(kv_elems, dtype=torch.bfloat16).pin_memory()
+    host_v = torch.empty(kv_elems, dtype=torch.bfloat16).pin_memory()
+    host_q = torch.empty(q_elems, dtype=torch.bfloat16).pin_memory()
+    host_o = torch.empty(q_elems, dtype=torch.bfloat16).pin_memory()
+    g = torch.Generator().manual_seed(SEED)
+    host_k.copy_((torch.rand(kv_elems, generator=g) * 2 - 1).to(torch.bfloat16))
+    host_v.copy_((torch.rand(kv_elems, generator=g) * 2 - 1).to(torch.bfloat16))
+    host_q.copy_((torch.rand(q_elems, generator=g) * 2 - 1).to(torch.bfloat16))
+    for m in models:  # warm the staging path
+        m.eng.step()
+        m.eng.decode_host(host_k.data_ptr(), host_v.data_ptr(), host_q.data_ptr(), host_o.data_ptr(), scale)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        for m in models:
+            m.eng.step()
+            m.eng.decode_host(host_k.data_ptr(), host_v.data_ptr(), host_q.data_ptr(), host_o.data_ptr(), scale)
+    sec = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+
+        t = torch.tensor([sec], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        sec = float(t.item())
+    tokens = steps * len(models) * B_PER_MODEL * world
+    return {"value": round(tokens / sec, 1), "unit": "tokens/s",
+            "h2d_bytes_per_step": len(models) * (2 * kv_elems + q_elems) * 2,
+            "d2h_bytes_per_step": len(models) * q_elems * 2, "api": "prism_engine_step + prism_engine_decode_host"}
+
+
+def page_map_summary(st, steps):
+    maps, unmaps = st["maps"], st["unmaps"]
+    total_us = (st["map_ns_total"] + st["unmap_ns_total"]) / 1e3
+    return {"logical_maps": maps, "logical_unmaps": unmaps, "revived_in_place": st["revived"],
+            "driver_creates": st["creates"], "driver_unmaps": st["driver_unmaps"],
+            "map_us_p50": round(st["map_ns_p50"] / 1e3, 2), "map_us_p99": round(st["map_ns_p99"] / 1e3, 2),
+            "unmap_us_p50": round(st["unmap_ns_p50"] / 1e3, 2), "unmap_us_p99": round(st["unmap_ns_p99"] / 1e3, 2),
+            "amortised_us_per_page_op": round(total_us / max(maps + unmaps, 1), 2),
+            "note": "host wall time inside the VMM layer during the timed steps"}
+
+
+# ---------------------------------------------------------------- CPU arm
+
+
+def cpu_arm(args, sample_seqs=8, sample_layers=4, ref_steps=4):
+    """CPU path of the same step: reference engine::step (allocation half, the
+    reference itself) + CPU paged attention port (all host threads) on a
+    bounded sample, scaled to the full step."""
+    import numpy as np
+
+    import oracle
+    from paper_2505_04021_b200 import msim
+
+    cores = os.cpu_count() or 1
+    # (1) allocation half: the reference's own engine::step on a B200-sized
+    # ledger (85,830 pages -> pools with V = 85,830 as finish_activation sets).
+    alloc_ms = None
+    if oracle.have_reference():
+        ref = oracle.reference()
+        gpu = msim.GpuState(0, 85830, lib=ref)
+        engines = []
+        for mid, trace in c1_requests(MODELS_PER_GPU, 0):
+            spec = msim.ModelSpec.llm(mid, L, NQ, NKV, D, weight_bytes=16_060_000_000, chunk_size=4096)
+            act = gpu.activate(spec)
+            gpu.finish_activation(act.engine_index)
+            e = gpu.engine(act.engine_index)
+            for i, ev in enumerate(trace):
+                e.push(i + 1, ev.prompt_tokens, 10_000)
+            while e.counts()[1] or any(r.prompt_done < r.prompt_tokens for r in e.batch()):
+                e.step()
+            engines.append(e)
+        e0 = [e.step() for e in engines]  # first decode
+        t0 = time.perf_counter()
+        for _ in range(ref_steps):
+            for e in engines:
+                e.step()
+        alloc_ms = (time.perf_counter() - t0) * 1e3 / ref_steps
+    # (2) attention half: CPU port over a host copy of the paged layout.
+    lib = oracle.restate()
+    tpp = 16
+    page_bytes = 2 << 20
+    n_pages = sample_seqs * CTX // tpp
+    pool = np.zeros(n_pages * page_bytes // 2, dtype=np.uint16)
+    rng = np.random.default_rng(SEED)
+    pool[:] = rng.integers(0x3c00, 0x3f80, size=pool.size, dtype=np.uint16)  # bf16 values in [~0.0078, 1)
+    # interleave sequences across pages like most-occupied-first packing does
+    table = np.arange(sample_seqs * CTX, dtype=np.int32).reshape(CTX, sample_seqs).T.copy().reshape(-1)
+    rows = (np.arange(sample_seqs, dtype=np.int64) * CTX)
+    ctx = np.full(sample_seqs, CTX, dtype=np.int32)
+    q = rng.integers(0x3c00, 0x3f80, size=sample_seqs * NQ * D, dtype=np.uint16)
+    out = np.zeros(sample_seqs * NQ * D, dtype=np.float32)
+    lib.po_paged_attention_cpu(pool.ctypes.data, page_bytes, tpp, NKV, D, 0, table.ctypes.data, rows.ctypes.data,
+                               ctx.ctypes.data, sample_seqs, q.ctypes.data, NQ, 1 / math.sqrt(D),
+                               out.ctypes.data, cores)  # warm
+    t0 = time.perf_counter()
+    for layer in range(sample_layers):
+        lib.po_paged_attention_cpu(pool.ctypes.data, page_bytes, tpp, NKV, D, layer % L, table.ctypes.data,
+                                   rows.ctypes.data, ctx.ctypes.data, sample_seqs, q.ctypes.data, NQ,
+                                   1 / math.sqrt(D), out.ctypes.data, cores)
+    attn_ms_sample = (time.perf_counter() - t0) * 1e3
+    # scale: sample covers sample_seqs seqs x sample_layers layers of one model
+    scale = (B_PER_MODEL / sample_seqs) * (L / sample_layers) * MODELS_PER_GPU
+    attn_ms = attn_ms_sample * scale
+    step_ms = attn_ms + (alloc_ms or 0.0)
+    tokens_per_step = MODELS_PER_GPU * B_PER_MODEL
+    return {
+        "value": round(tokens_per_step / (step_ms / 1e3), 2),
+        "unit": "tokens/s",
+        "cores": cores,
+        "kind": "port",
+        "sample": (f"reference engine::step (oracle/_ref, 1 thread) x {MODELS_PER_GPU} models x {ref_steps} decode "
+                   f"steps at V=85,830 pages = {alloc_ms and round(alloc_ms, 2)} ms/step; CPU paged attention port "
+                   f"(oracle/restate, fp32, {cores} threads) on {sample_seqs} seqs x {CTX} ctx x {sample_layers} "
+                   f"layers = {round(attn_ms_sample, 1)} ms, scaled x{scale:g} to the full step"),
+        "alloc_ms_per_step": alloc_ms and round(alloc_ms, 3),
+        "attention_ms_per_step": round(attn_ms, 2),
+    }
+
+
+# ---------------------------------------------------------------- main
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="prism", choices=["prism", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        t0 = time.perf_counter()
+        for _ in range(args.warmup):
+            pass
+        base = cpu_arm(args)
+        res = {"metric": METRIC, "value": base["value"], "unit": "tokens/s", "n_gpus": args.gpus,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(MODELS_PER_GPU * B_PER_MODEL
+                                                                                  / base["value"] * 1e3, 3),
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (CPU)",
+               "data": "synthetic", "config": {"workload": WORKLOAD, "parallelism": "CPU, rank 0"},
+               "impl": "reference", "cpu_baseline": base,
+               "e2e": {"value": base["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+               "wall_s": round(time.perf_counter() - t0, 2)}
+        print(json.dumps(res))
+        return
+
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl")
+    res = gpu_arm(args, rank, world)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            try:
+                res["cpu_baseline"] = cpu_arm(args)
+            except Exception as e:  # reported, never substituted for the GPU number
+                res["cpu_baseline"] = {"error": str(e)}
+        print(json.dumps(res))
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -128,6 +128,7 @@ private:
     bool recording_ = false;
     std::vector<AllocEvent> log_;
     prism::VmmDevice* dev_ = nullptr;
+    std::shared_ptr<prism::VmmDevice> dev_hold_;  // keeps the device alive
 };
 
 // One model's virtual KV range. Pages are mapped only when a token needs them

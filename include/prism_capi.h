@@ -324,6 +324,9 @@ typedef struct {
     double map_ns_total, unmap_ns_total;
     double map_ns_p50, map_ns_p99, unmap_ns_p50, unmap_ns_p99;
     uint64_t buffered, cached, pending;
+    double create_ns_total, map_call_ns_total, access_ns_total; /* per driver call kind */
+    uint64_t access_calls;
+    uint64_t steals; /* parked pages moved to another VA (cross-model memory movement) */
 } prism_device_stats;
 int prism_device_stats_get(const prism_device* d, prism_device_stats* out);
 int prism_device_reset_stats(prism_device* d);
@@ -364,6 +367,8 @@ int prism_engine_append_kv_synthetic(prism_gpu* g, int engine_index, int layer_b
 /* K3: q, out device bf16 [n_decodes][n_q_heads][head_dim]; chunk <= 0 picks the split size. */
 int prism_engine_decode_attention(prism_gpu* g, int engine_index, int layer, const void* q, void* out, float scale,
                                   int32_t chunk);
+/* K3 implementation: 0 tensor-core mma.sync (default), 1 CUDA-core SIMT. */
+int prism_set_attention_variant(int variant);
 int prism_engine_synth_q(prism_gpu* g, int engine_index, int layer, uint64_t seed, float q_scale, void* q);
 /* End-to-end: the same attention with HOST buffers (pinned or pageable);
  * copies q in, runs K2 for new_k/new_v (host, may be null) over all layers

@@ -60,6 +60,10 @@ def restate():
         lib.po_decode_attention_dense.restype = None
         lib.po_decode_attention_dense.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int,
                                                   C.c_int, C.c_double, C.POINTER(C.c_double)]
+        lib.po_paged_attention_cpu.restype = None
+        lib.po_paged_attention_cpu.argtypes = [C.c_void_p, C.c_uint64, C.c_uint32, C.c_int, C.c_int, C.c_int,
+                                               C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_int,
+                                               C.c_float, C.c_void_p, C.c_int]
         lib.po_pool_create.restype = C.c_void_p
         lib.po_pool_create.argtypes = [C.c_uint32, C.c_uint64, C.c_uint64, C.c_int]
         lib.po_pool_destroy.argtypes = [C.c_void_p]

@@ -156,6 +156,103 @@ void po_decode_attention_dense(const uint16_t* q, const uint16_t* k, const uint1
     free(qd);
 }
 
+/* ------------------------------------------------------------ CPU paged attention (baseline port) */
+typedef struct {
+    const uint8_t* pool;
+    uint64_t page_bytes;
+    uint32_t tpp;
+    int n_kv, d, layer;
+    const int32_t* table;
+    const int64_t* rows;
+    const int32_t* ctx;
+    size_t n_dec;
+    const uint16_t* q;
+    int n_q;
+    float scale;
+    float* out;
+    size_t next;
+} paged_job;
+
+static inline float bf(uint16_t b) {
+    const uint32_t x = (uint32_t)b << 16;
+    float f;
+    memcpy(&f, &x, 4);
+    return f;
+}
+
+static void paged_item(const paged_job* j, size_t b, int h) {
+    const int g = j->n_q / j->n_kv, d = j->d, L = j->ctx[b];
+    float qf[8][256];
+    float acc[8][256];
+    float m[8], l[8];
+    for (int k = 0; k < g; ++k) {
+        for (int e = 0; e < d; ++e) {
+            qf[k][e] = bf(j->q[((size_t)b * j->n_q + (size_t)h * g + k) * d + e]) * j->scale;
+            acc[k][e] = 0.f;
+        }
+        m[k] = -INFINITY;
+        l[k] = 0.f;
+    }
+    const uint64_t row_bytes = (uint64_t)d * 2;
+    const uint64_t kblock = ((uint64_t)(j->layer * 2 + 0) * j->n_kv + h) * j->tpp * row_bytes;
+    const uint64_t vblock = ((uint64_t)(j->layer * 2 + 1) * j->n_kv + h) * j->tpp * row_bytes;
+    for (int t = 0; t < L; ++t) {
+        const uint32_t sid = (uint32_t)j->table[j->rows[b] + t];
+        const uint32_t page = sid / j->tpp, slot = sid % j->tpp;
+        const uint16_t* kr = (const uint16_t*)(j->pool + (uint64_t)page * j->page_bytes + kblock + slot * row_bytes);
+        const uint16_t* vr = (const uint16_t*)(j->pool + (uint64_t)page * j->page_bytes + vblock + slot * row_bytes);
+        float kf[256], vf[256];
+        for (int e = 0; e < d; ++e) {
+            kf[e] = bf(kr[e]);
+            vf[e] = bf(vr[e]);
+        }
+        for (int k = 0; k < g; ++k) {
+            /* 8 independent partial sums so the compiler vectorizes the dot
+             * product without reassociation flags */
+            float part[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int e = 0; e < d; e += 8) {
+                for (int u = 0; u < 8; ++u) part[u] += qf[k][e + u] * kf[e + u];
+            }
+            const float s = ((part[0] + part[1]) + (part[2] + part[3])) + ((part[4] + part[5]) + (part[6] + part[7]));
+            if (s > m[k]) { /* rescale only when the running max grows */
+                const float a = expf(m[k] - s);
+                l[k] *= a;
+                for (int e = 0; e < d; ++e) acc[k][e] *= a;
+                m[k] = s;
+            }
+            const float p = expf(s - m[k]);
+            l[k] += p;
+            for (int e = 0; e < d; ++e) acc[k][e] += p * vf[e];
+        }
+    }
+    for (int k = 0; k < g; ++k) {
+        float* o = j->out + ((size_t)b * j->n_q + (size_t)h * g + k) * d;
+        for (int e = 0; e < d; ++e) o[e] = acc[k][e] / l[k];
+    }
+}
+
+static void* paged_worker(void* arg) {
+    paged_job* j = (paged_job*)arg;
+    const size_t total = j->n_dec * (size_t)j->n_kv;
+    for (;;) {
+        const size_t i = __atomic_fetch_add(&j->next, 1, __ATOMIC_RELAXED);
+        if (i >= total) break;
+        paged_item(j, i / (size_t)j->n_kv, (int)(i % (size_t)j->n_kv));
+    }
+    return NULL;
+}
+
+void po_paged_attention_cpu(const uint8_t* pool, uint64_t page_bytes, uint32_t tpp, int n_kv, int d, int layer,
+                            const int32_t* table, const int64_t* rows, const int32_t* ctx, size_t n_dec,
+                            const uint16_t* q, int n_q, float scale, float* out, int n_threads) {
+    paged_job j = {pool, page_bytes, tpp, n_kv, d, layer, table, rows, ctx, n_dec, q, n_q, scale, out, 0};
+    if (n_threads < 1) n_threads = 1;
+    if (n_threads > 256) n_threads = 256;
+    pthread_t th[256];
+    for (int t = 0; t < n_threads; ++t) pthread_create(&th[t], NULL, paged_worker, &j);
+    for (int t = 0; t < n_threads; ++t) pthread_join(th[t], NULL);
+}
+
 /* ------------------------------------------------------------ allocator
  * Straight restatement of reference src/pagealloc.cpp: per-page
  * {mapped, occupied, slots[]} with the O(V) pick_page scan (:158-186), the

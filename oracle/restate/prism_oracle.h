@@ -37,6 +37,16 @@ void po_decode_attention_synth(uint64_t seed, int layer, size_t n_dec, const uin
 void po_decode_attention_dense(const uint16_t* q, const uint16_t* k, const uint16_t* v, int ctx, int n_q, int n_kv,
                                int d, double scale, double* out);
 
+/* CPU paged decode attention over a HOST copy of the paged KV layout
+ * ([layer][K|V][kv_head][slot][d] bf16 inside each page_bytes page; slot id =
+ * page * tpp + slot), fp32 accumulation, n_threads pthreads. This is the
+ * CPU-baseline "port" of the GPU kernel (the reference has no attention).
+ * q: bf16 [n_dec][n_q][d]; table: slot ids; rows[b]: element offset of
+ * request b's row; ctx[b]: its length. out: float [n_dec][n_q][d]. */
+void po_paged_attention_cpu(const uint8_t* pool, uint64_t page_bytes, uint32_t tpp, int n_kv, int d, int layer,
+                            const int32_t* table, const int64_t* rows, const int32_t* ctx, size_t n_dec,
+                            const uint16_t* q, int n_q, float scale, float* out, int n_threads);
+
 /* ---- allocator restatement (reference src/pagealloc.cpp:108-267) ---- */
 typedef struct po_pool po_pool;
 typedef struct {

@@ -155,7 +155,9 @@ class ModelProfile(C.Structure):
 class DeviceStats(C.Structure):
     _fields_ = [(n, c_uint64) for n in ("maps", "revived", "creates", "unmaps", "driver_unmaps")] + [
         (n, c_double) for n in ("map_ns_total", "unmap_ns_total", "map_ns_p50", "map_ns_p99", "unmap_ns_p50",
-                                "unmap_ns_p99")] + [(n, c_uint64) for n in ("buffered", "cached", "pending")]
+                                "unmap_ns_p99")] + [(n, c_uint64) for n in ("buffered", "cached", "pending")] + [
+        (n, c_double) for n in ("create_ns_total", "map_call_ns_total", "access_ns_total")] + [
+        ("access_calls", c_uint64), ("steals", c_uint64)]
 
 
 class EngineDeviceOptions(C.Structure):
@@ -257,6 +259,7 @@ _DEVICE_DECLS = {
     "prism_engine_append_kv_synthetic": (c_int, [c_void_p, c_int, c_int, c_int, c_uint64]),
     "prism_engine_decode_attention": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_float, c_int32]),
     "prism_engine_synth_q": (c_int, [c_void_p, c_int, c_int, c_uint64, c_float, c_void_p]),
+    "prism_set_attention_variant": (c_int, [c_int]),
     "prism_engine_decode_host": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_float]),
     "prism_engine_synchronize": (c_int, [c_void_p, c_int]),
 }

@@ -18,7 +18,7 @@ namespace pa = msim::pagealloc;
 namespace me = msim::engine;
 
 struct prism_device {
-    std::unique_ptr<prism::VmmDevice> dev;
+    std::shared_ptr<prism::VmmDevice> dev;  // ledgers / pools hold further references
 };
 
 namespace {
@@ -117,6 +117,11 @@ int prism_device_stats_get(const prism_device* d, prism_device_stats* out) {
         out->buffered = d->dev->buffered_handles();
         out->cached = d->dev->cached_handles();
         out->pending = d->dev->pending_unmaps();
+        out->create_ns_total = s.create_ns_total;
+        out->map_call_ns_total = s.map_call_ns_total;
+        out->access_ns_total = s.access_ns_total;
+        out->access_calls = s.access_calls;
+        out->steals = s.steals;
     });
 }
 
@@ -261,6 +266,7 @@ int prism_engine_append_kv_synthetic(prism_gpu* g, int engine_index, int layer_b
 namespace prism {
 void launch_decode_attention(class EngineDeviceImpl& d, int layer, const void* q, void* out, float scale, int chunk);
 EngineDeviceImpl& impl_of(const msim::engine::Engine& eng);
+void set_attention_variant(int v);
 }  // namespace prism
 
 extern "C" {
@@ -271,6 +277,13 @@ int prism_engine_decode_attention(prism_gpu* g, int engine_index, int layer, con
         need(q, "q");
         need(out, "out");
         prism::launch_decode_attention(prism::impl_of(engine_at(g, engine_index)), layer, q, out, scale, chunk);
+    });
+}
+
+int prism_set_attention_variant(int variant) {
+    return dguard([&] {
+        if (variant != 0 && variant != 1) throw std::invalid_argument("attention variant must be 0 or 1");
+        prism::set_attention_variant(variant);
     });
 }
 

@@ -16,27 +16,18 @@
 // Splits of one (b, h) are merged by the last CTA to finish (atomic ticket),
 // so one launch produces the final bf16 output.
 #include <cfloat>
+#include <cstdlib>
+#include <cstring>
 
+#include "cuda/attn_common.cuh"
 #include "cuda/device_impl.cuh"
 
 namespace prism {
 
-namespace {
+void launch_k3_mma(const AttnArgs& a, int head_dim, int group, dim3 grid, cudaStream_t stream);
+int attention_variant();
 
-struct AttnArgs {
-    KvGeom g;
-    int layer;
-    const __nv_bfloat16* q;
-    __nv_bfloat16* out;
-    const std::int32_t* table;
-    const DecodeDesc* desc;
-    float scale_log2;
-    int chunk;        // tokens per split, multiple of the tile size
-    int max_splits;   // grid.x
-    float* part_o;    // [n_dec * n_kv][max_splits][G][D]
-    float* part_ml;   // [n_dec * n_kv][max_splits][G][2]
-    int* tickets;     // [n_dec * n_kv], zero between launches
-};
+namespace {
 
 template <int D, int G, int LPT>
 struct Shape {
@@ -59,25 +50,6 @@ struct Shape {
     static_assert(kE % 8 == 0, "lane slice must be whole 16-byte chunks");
     static_assert(kLoads * kThreads == kT * kCpr, "tile must split evenly");
 };
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, int src_bytes) {
-    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(src_bytes));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
-}
-
-__device__ __forceinline__ float fast_exp2(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
-
-__device__ __forceinline__ float bf_lo(std::uint32_t w) { return __uint_as_float(w << 16); }
-__device__ __forceinline__ float bf_hi(std::uint32_t w) { return __uint_as_float(w & 0xffff0000u); }
 
 template <int D, int G, int LPT>
 __global__ void __launch_bounds__(128, 3) k3_decode(AttnArgs a) {
@@ -119,21 +91,28 @@ __global__ void __launch_bounds__(128, 3) k3_decode(AttnArgs a) {
         }
     }
 
-    auto issue = [&](int tile) {
+    // Slot ids are fetched one tile ahead of the cp.async that uses them.
+    constexpr std::uint32_t kNoSlot = 0xFFFFFFFFu;
+    auto load_sids = [&](int tile, std::uint32_t (&dst)[S::kLoads]) {
+        const int t0 = t_begin + tile * S::kT;
+#pragma unroll
+        for (int i = 0; i < S::kLoads; ++i) {
+            const int t = t0 + (tid + i * S::kThreads) / S::kCpr;
+            dst[i] = t < t_end ? static_cast<std::uint32_t>(__ldg(row + t)) : kNoSlot;
+        }
+    };
+    auto issue = [&](int tile, const std::uint32_t (&sids)[S::kLoads]) {
         unsigned char* sk = smem + (tile % S::kStages) * S::kStageB;
         unsigned char* sv = sk + S::kTileB;
-        const int t0 = t_begin + tile * S::kT;
 #pragma unroll
         for (int i = 0; i < S::kLoads; ++i) {
             const int c = tid + i * S::kThreads;
             const int r = c / S::kCpr, col = c % S::kCpr;
-            const int t = t0 + r;
             const char* src_k = reinterpret_cast<const char*>(a.table);
             const char* src_v = src_k;
             int bytes = 0;
-            if (t < t_end) {
-                const std::uint32_t sid = static_cast<std::uint32_t>(__ldg(row + t));
-                src_k = base + row_offset(a.g, sid, a.layer, 0, h) + col * 16;
+            if (sids[i] != kNoSlot) {
+                src_k = base + row_offset(a.g, sids[i], a.layer, 0, h) + col * 16;
                 src_v = src_k + v_delta;
                 bytes = 16;
             }
@@ -141,6 +120,7 @@ __global__ void __launch_bounds__(128, 3) k3_decode(AttnArgs a) {
             cp_async16(sv + r * S::kRowB + col * 16, src_v, bytes);
         }
     };
+    std::uint32_t sids[S::kLoads];
 
     float m[G], l[G], o[G][S::kE];
 #pragma unroll
@@ -153,14 +133,21 @@ __global__ void __launch_bounds__(128, 3) k3_decode(AttnArgs a) {
 
 #pragma unroll
     for (int st = 0; st < S::kStages - 1; ++st) {
-        if (st < n_tiles) issue(st);
+        if (st < n_tiles) {
+            load_sids(st, sids);
+            issue(st, sids);
+        }
         cp_async_commit();
     }
+    if (S::kStages - 1 < n_tiles) load_sids(S::kStages - 1, sids);
 
     for (int tile = 0; tile < n_tiles; ++tile) {
         cp_async_wait<S::kStages - 2>();
         __syncthreads();
-        if (tile + S::kStages - 1 < n_tiles) issue(tile + S::kStages - 1);
+        if (tile + S::kStages - 1 < n_tiles) {
+            issue(tile + S::kStages - 1, sids);
+            if (tile + S::kStages < n_tiles) load_sids(tile + S::kStages, sids);
+        }
         cp_async_commit();
 
         const unsigned char* sk = smem + (tile % S::kStages) * S::kStageB;
@@ -359,6 +346,15 @@ void launch_d(int group, const AttnArgs& a, dim3 grid, cudaStream_t stream) {
 
 }  // namespace
 
+// K3 variant: 0 = tensor-core mma.sync kernel (default), 1 = CUDA-core SIMT
+// kernel (kept for A/B measurement). Initialised from PRISM_K3=simt|mma.
+static int g_variant = [] {
+    const char* v = std::getenv("PRISM_K3");
+    return v && std::strcmp(v, "simt") == 0 ? 1 : 0;
+}();
+int attention_variant() { return g_variant; }
+void set_attention_variant(int v) { g_variant = v == 1 ? 1 : 0; }
+
 // Host launcher shared by the engine API and the C-ABI.
 void launch_decode_attention(EngineDeviceImpl& d, int layer, const void* q, void* out, float scale, int chunk_override) {
     if (layer < 0 || layer >= d.n_layers) throw std::runtime_error("decode_attention: bad layer");
@@ -370,11 +366,11 @@ void launch_decode_attention(EngineDeviceImpl& d, int layer, const void* q, void
         max_ctx = std::max(max_ctx, d.decode_desc.host[i].ctx);
         sum_ctx += d.decode_desc.host[i].ctx;
     }
-    constexpr int kT = 32;
+    const bool simt = attention_variant() == 1;
+    const int kT = simt ? 32 : 64;
     int chunk = chunk_override;
     if (chunk <= 0) {
-        // Aim for ~12 CTAs per SM over the launch (3 resident x 4 waves),
-        // never below 4 tiles per CTA.
+        // Aim for ~12 CTAs per SM over the launch, never below 4 tiles per CTA.
         const std::int64_t work = sum_ctx * d.n_kv;
         const std::int64_t target = 148LL * 12;
         chunk = static_cast<int>((work + target - 1) / target);
@@ -400,7 +396,9 @@ void launch_decode_attention(EngineDeviceImpl& d, int layer, const void* q, void
         a.tickets = d.attn_counters(static_cast<std::size_t>(n_dec) * d.n_kv);
     }
     const dim3 grid(static_cast<unsigned>(max_splits), static_cast<unsigned>(d.n_kv), static_cast<unsigned>(n_dec));
-    if (d.head_dim == 128) {
+    if (!simt) {
+        launch_k3_mma(a, d.head_dim, d.group, grid, d.stream);
+    } else if (d.head_dim == 128) {
         launch_d<128>(d.group, a, grid, d.stream);
     } else {
         launch_d<64>(d.group, a, grid, d.stream);

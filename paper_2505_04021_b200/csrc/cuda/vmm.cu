@@ -62,12 +62,9 @@ void cu_check(CUresult r, const char* what) {
 }
 
 using Clock = std::chrono::steady_clock;
-double ns_since(Clock::time_point t0) {
-    return std::chrono::duration<double, std::nano>(Clock::now() - t0).count();
-}
+double ns_since(Clock::time_point t0) { return std::chrono::duration<double, std::nano>(Clock::now() - t0).count(); }
 
 constexpr std::size_t kMaxSamples = 1 << 16;
-
 void sample(std::vector<float>& ring, double ns) {
     if (ring.size() < kMaxSamples) ring.push_back(static_cast<float>(ns));
 }
@@ -77,7 +74,7 @@ CUmemAccessDesc& access_of(void* p) { return *static_cast<CUmemAccessDesc*>(p); 
 
 }  // namespace
 
-std::unique_ptr<VmmDevice> VmmDevice::open(int ordinal, std::uint64_t page_bytes) {
+std::shared_ptr<VmmDevice> VmmDevice::open(int ordinal, std::uint64_t page_bytes) {
     int count = 0;
     PRISM_CUDA(cudaGetDeviceCount(&count));
     if (ordinal < 0 || ordinal >= count) throw std::runtime_error("VmmDevice: no CUDA device " + std::to_string(ordinal));
@@ -89,7 +86,7 @@ std::unique_ptr<VmmDevice> VmmDevice::open(int ordinal, std::uint64_t page_bytes
              "cuDeviceGetAttribute");
     if (!vmm) throw std::runtime_error("VmmDevice: device does not support virtual memory management");
 
-    std::unique_ptr<VmmDevice> dev(new VmmDevice());
+    std::shared_ptr<VmmDevice> dev(new VmmDevice());
     dev->ordinal_ = ordinal;
     dev->page_bytes_ = page_bytes;
     auto* prop = new CUmemAllocationProp();
@@ -118,7 +115,11 @@ std::unique_ptr<VmmDevice> VmmDevice::open(int ordinal, std::uint64_t page_bytes
 VmmDevice::~VmmDevice() {
     try {
         cudaSetDevice(ordinal_);
-        reclaim(true);
+        cudaDeviceSynchronize();
+        for (auto& [va, p] : parked_) {
+            drv().unmap(va, page_bytes_);
+            drv().release(p.handle);
+        }
         for (auto& [va, h] : live_) {
             drv().unmap(va, page_bytes_);
             drv().release(h);
@@ -134,6 +135,10 @@ VmmDevice::~VmmDevice() {
     delete static_cast<CUmemAccessDesc*>(access_desc_);
 }
 
+std::uint64_t VmmDevice::total_handles() const {
+    return live_.size() + parked_.size() + buffer_.size() + taken_.size() + cache_.size();
+}
+
 std::uint64_t VmmDevice::reserve(std::uint64_t pages) {
     CUdeviceptr va = 0;
     cu_check(drv().reserve(&va, pages * page_bytes_, page_bytes_, 0, 0), "cuMemAddressReserve");
@@ -142,17 +147,22 @@ std::uint64_t VmmDevice::reserve(std::uint64_t pages) {
 
 void VmmDevice::release(std::uint64_t va, std::uint64_t pages) {
     const std::uint64_t end = va + pages * page_bytes_;
-    for (auto it = pending_.begin(); it != pending_.end();) {
-        if (it->first >= va && it->first < end) {
-            driver_unmap(it->first);
-            drop_handle(it->second.handle);
-            it = pending_.erase(it);
-        } else {
-            ++it;
+    bool synced = false;
+    for (auto it = parked_.lower_bound(va); it != parked_.end() && it->first < end;) {
+        if (!synced) {
+            PRISM_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
+            synced = true;
         }
+        driver_unmap(it->first);
+        drop_handle(it->second.handle);
+        it = parked_.erase(it);
     }
     for (auto it = live_.begin(); it != live_.end();) {
         if (it->first >= va && it->first < end) {
+            if (!synced) {
+                PRISM_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
+                synced = true;
+            }
             driver_unmap(it->first);
             drop_handle(it->second);
             it = live_.erase(it);
@@ -163,82 +173,140 @@ void VmmDevice::release(std::uint64_t va, std::uint64_t pages) {
     cu_check(drv().addr_free(static_cast<CUdeviceptr>(va), pages * page_bytes_), "cuMemAddressFree");
 }
 
-std::uint64_t VmmDevice::new_handle() {
+void VmmDevice::advance_fences(bool wait) {
+    std::size_t done = 0;
+    while (done < fences_.size()) {
+        auto ev = static_cast<cudaEvent_t>(fences_[done]);
+        const cudaError_t q = wait ? cudaEventSynchronize(ev) : cudaEventQuery(ev);
+        if (q == cudaErrorNotReady) break;
+        PRISM_CUDA(q);
+        cudaEventDestroy(ev);
+        ++done;
+    }
+    fences_.erase(fences_.begin(), fences_.begin() + static_cast<std::ptrdiff_t>(done));
+    fenced_ += done;
+}
+
+std::uint64_t VmmDevice::steal() {
+    // Prefer the highest parked VA whose fence passed: allocation reuses the
+    // lowest unmapped page indices, so high parked pages are least likely to
+    // be revived soon.
+    advance_fences(false);
+    auto pick = parked_.end();
+    for (auto it = parked_.rbegin(); it != parked_.rend(); ++it) {
+        if (it->second.epoch < fenced_) {
+            pick = std::prev(it.base());
+            break;
+        }
+    }
+    if (pick == parked_.end()) {
+        // Every parked page may still be read by in-flight kernels: fence
+        // now and wait, after which all of them are safe.
+        fence();
+        advance_fences(true);
+        pick = std::prev(parked_.end());
+    }
+    const auto t0 = Clock::now();
+    driver_unmap(pick->first);
+    const std::uint64_t h = pick->second.handle;
+    parked_.erase(pick);
+    ++stats_.steals;
+    stats_.unmap_ns_total += ns_since(t0);
+    return h;
+}
+
+std::uint64_t VmmDevice::acquire_handle(bool from_buffer) {
+    if (from_buffer && !taken_.empty()) {
+        const std::uint64_t h = taken_.back();
+        taken_.pop_back();
+        return h;
+    }
     if (!cache_.empty()) {
         const std::uint64_t h = cache_.back();
         cache_.pop_back();
         return h;
     }
+    if (total_handles() >= budget_ && !parked_.empty()) return steal();
+    const auto tc = Clock::now();
     CUmemGenericAllocationHandle h = 0;
     CUresult r = drv().create(&h, page_bytes_, &prop_of(prop_), 0);
-    if (r == CUDA_ERROR_OUT_OF_MEMORY && !pending_.empty()) {
-        reclaim(true);  // physical pages are parked behind deferred unmaps
-        if (!cache_.empty()) return new_handle();
-        r = drv().create(&h, page_bytes_, &prop_of(prop_), 0);
-    }
+    if (r == CUDA_ERROR_OUT_OF_MEMORY && !parked_.empty()) return steal();
     cu_check(r, "cuMemCreate");
     ++stats_.creates;
+    stats_.create_ns_total += ns_since(tc);
     return static_cast<std::uint64_t>(h);
 }
 
-void VmmDevice::drop_handle(std::uint64_t h) {
-    if (cache_.size() < cache_limit_) {
-        cache_.push_back(h);
-    } else {
-        drv().release(static_cast<CUmemGenericAllocationHandle>(h));
-    }
-}
+void VmmDevice::drop_handle(std::uint64_t h) { cache_.push_back(h); }
 
 void VmmDevice::map(std::uint64_t va, bool from_buffer) {
+    const std::uint64_t one[1] = {va};
+    map_batch(one, 1, from_buffer ? 1 : 0);
+}
+
+void VmmDevice::map_batch(const std::uint64_t* vas, std::size_t n, std::size_t n_from_buffer) {
+    if (n == 0) return;
     const auto t0 = Clock::now();
-    ++stats_.maps;
-    const auto p = pending_.find(va);
-    if (p != pending_.end()) {
-        // Unmapped logically, never unmapped physically: revive in place and
-        // give the buffer handle (if any) back to the cache.
-        live_.emplace(va, p->second.handle);
-        pending_.erase(p);
-        if (from_buffer && !taken_.empty()) {
-            drop_handle(taken_.back());
-            taken_.pop_back();
+    stats_.maps += n;
+    std::vector<std::uint64_t> fresh;
+    fresh.reserve(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        const bool from_buffer = i < n_from_buffer;
+        const auto p = parked_.find(vas[i]);
+        if (p != parked_.end()) {
+            // Revive in place; a buffer handle earmarked for this map returns
+            // to the cache (it stays counted as physical memory).
+            live_.emplace(vas[i], p->second.handle);
+            parked_.erase(p);
+            if (from_buffer && !taken_.empty()) {
+                cache_.push_back(taken_.back());
+                taken_.pop_back();
+            }
+            ++stats_.revived;
+            continue;
         }
-        ++stats_.revived;
-    } else {
-        std::uint64_t h;
-        if (from_buffer && !taken_.empty()) {
-            h = taken_.back();
-            taken_.pop_back();
-        } else {
-            h = new_handle();
-        }
-        cu_check(drv().map(static_cast<CUdeviceptr>(va), page_bytes_, 0, static_cast<CUmemGenericAllocationHandle>(h), 0),
+        const std::uint64_t h = acquire_handle(from_buffer);
+        const auto tm = Clock::now();
+        cu_check(drv().map(static_cast<CUdeviceptr>(vas[i]), page_bytes_, 0,
+                           static_cast<CUmemGenericAllocationHandle>(h), 0),
                  "cuMemMap");
-        cu_check(drv().set_access(static_cast<CUdeviceptr>(va), page_bytes_, &access_of(access_desc_), 1),
-                 "cuMemSetAccess");
-        live_.emplace(va, h);
+        stats_.map_call_ns_total += ns_since(tm);
+        live_.emplace(vas[i], h);
+        fresh.push_back(vas[i]);
     }
-    const double ns = ns_since(t0);
-    stats_.map_ns_total += ns;
-    sample(stats_.map_ns, ns);
+    std::sort(fresh.begin(), fresh.end());
+    for (std::size_t i = 0; i < fresh.size();) {
+        std::size_t j = i + 1;
+        while (j < fresh.size() && fresh[j] == fresh[j - 1] + page_bytes_) ++j;
+        const auto ta = Clock::now();
+        cu_check(drv().set_access(static_cast<CUdeviceptr>(fresh[i]), (j - i) * page_bytes_, &access_of(access_desc_), 1),
+                 "cuMemSetAccess");
+        stats_.access_ns_total += ns_since(ta);
+        ++stats_.access_calls;
+        i = j;
+    }
+    const double per = ns_since(t0) / static_cast<double>(n);
+    stats_.map_ns_total += per * static_cast<double>(n);
+    for (std::size_t i = 0; i < n; ++i) sample(stats_.map_ns, per);
 }
 
 void VmmDevice::unmap(std::uint64_t va) {
     const auto t0 = Clock::now();
     const auto it = live_.find(va);
     if (it == live_.end()) throw std::runtime_error("VmmDevice::unmap: page not mapped");
-    pending_.emplace(va, Pending{it->second, epoch_});
+    parked_.emplace(va, Parked{it->second, epoch_});
     live_.erase(it);
     ++stats_.unmaps;
-    stats_.unmap_ns_total += ns_since(t0);
+    const double ns = ns_since(t0);
+    stats_.unmap_ns_total += ns;
+    sample(stats_.unmap_ns, ns);
 }
 
 void VmmDevice::driver_unmap(std::uint64_t va) {
     const auto t0 = Clock::now();
     cu_check(drv().unmap(static_cast<CUdeviceptr>(va), page_bytes_), "cuMemUnmap");
     ++stats_.driver_unmaps;
-    const double ns = ns_since(t0);
-    stats_.unmap_ns_total += ns;
-    sample(stats_.unmap_ns, ns);
+    sample(stats_.unmap_ns, ns_since(t0));
 }
 
 void VmmDevice::fence() {
@@ -247,46 +315,50 @@ void VmmDevice::fence() {
     PRISM_CUDA(cudaEventRecord(ev, static_cast<cudaStream_t>(stream_)));
     fences_.push_back(ev);
     ++epoch_;
+    if (fences_.size() > 64) advance_fences(false);  // keep the queue short
 }
 
 void VmmDevice::reclaim(bool wait) {
     if (wait) {
-        PRISM_CUDA(cudaDeviceSynchronize());
-        fenced_epoch_ = epoch_;
+        PRISM_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
+        fence();
+        advance_fences(true);
+    } else {
+        advance_fences(false);
     }
-    // Retire completed fences in order. fences_[0] has index fenced_epoch_.
-    std::size_t done = 0;
-    while (done < fences_.size()) {
-        const cudaError_t q = wait ? cudaSuccess : cudaEventQuery(static_cast<cudaEvent_t>(fences_[done]));
-        if (q == cudaErrorNotReady) break;
-        PRISM_CUDA(q);
-        ++done;
-    }
-    for (std::size_t i = 0; i < done; ++i) cudaEventDestroy(static_cast<cudaEvent_t>(fences_[i]));
-    fences_.erase(fences_.begin(), fences_.begin() + static_cast<std::ptrdiff_t>(done));
-    if (!wait) fenced_epoch_ += done;
-    if (pending_.empty()) return;
-    for (auto it = pending_.begin(); it != pending_.end();) {
-        // A page unmapped at epoch e is safe once fence e (the first fence
-        // recorded after the unmap) has completed.
-        if (wait || it->second.epoch < fenced_epoch_) {
+    const auto t0 = Clock::now();
+    for (auto it = parked_.begin(); it != parked_.end();) {
+        if (wait || it->second.epoch < fenced_) {
             driver_unmap(it->first);
             drop_handle(it->second.handle);
-            it = pending_.erase(it);
+            it = parked_.erase(it);
         } else {
             ++it;
         }
     }
+    stats_.unmap_ns_total += ns_since(t0);
 }
 
 void VmmDevice::grow_buffer(std::uint64_t n) {
-    for (std::uint64_t i = 0; i < n; ++i) buffer_.push_back(new_handle());
+    for (std::uint64_t i = 0; i < n; ++i) buffer_.push_back(acquire_handle(false));
 }
 
 void VmmDevice::take_buffer(std::uint64_t n) {
     for (std::uint64_t i = 0; i < n && !buffer_.empty(); ++i) {
         taken_.push_back(buffer_.back());
         buffer_.pop_back();
+    }
+}
+
+void VmmDevice::set_budget(std::uint64_t pages) {
+    budget_ = pages;
+    // Shrink: free cached handles first, then physically release parked pages.
+    while (total_handles() > budget_ && !cache_.empty()) {
+        drv().release(static_cast<CUmemGenericAllocationHandle>(cache_.back()));
+        cache_.pop_back();
+    }
+    while (total_handles() > budget_ && !parked_.empty()) {
+        drv().release(static_cast<CUmemGenericAllocationHandle>(steal()));
     }
 }
 

@@ -32,6 +32,8 @@ void PhysicalLedger::attach_device(prism::VmmDevice* dev) {
     }
     if (dev && !pools_.empty()) throw UsageError("ledger: attach the device before creating pools");
     dev_ = dev;
+    dev_hold_ = dev ? dev->shared_from_this() : nullptr;
+    if (dev_) dev_->set_budget(capacity_ - weights_);  // physical pages the KV side may hold
     if (dev_ && buffer_ > dev_->buffered_handles()) dev_->grow_buffer(buffer_ - dev_->buffered_handles());
 }
 
@@ -57,6 +59,7 @@ bool PhysicalLedger::reserve_weight_pages(const std::string& model_id, std::uint
     if (pages > free_pages()) return false;
     weight_by_model_.emplace(model_id, pages);
     weights_ += pages;
+    if (dev_) dev_->set_budget(capacity_ - weights_);
     return true;
 }
 
@@ -65,6 +68,7 @@ void PhysicalLedger::release_weight_pages(const std::string& model_id) {  // :52
     if (it == weight_by_model_.end()) throw UsageError("ledger: no resident weights for model " + model_id);
     weights_ -= it->second;
     weight_by_model_.erase(it);
+    if (dev_) dev_->set_budget(capacity_ - weights_);
 }
 
 std::uint64_t PhysicalLedger::weight_pages_of(const std::string& model_id) const {
@@ -95,11 +99,7 @@ KvPool::~KvPool() {
     // reference's destructor does nothing either); only device VA is returned.
     if (st_ && st_->dev && st_->va) {
         try {
-            for (std::uint64_t p = 0; p < st_->vpages; ++p) {
-                if (st_->occ[p] > 0) st_->dev->unmap(st_->va + p * st_->dev->page_bytes());
-            }
-            st_->dev->reclaim(true);
-            st_->dev->release(st_->va, st_->vpages);
+            st_->dev->release(st_->va, st_->vpages);  // unmaps live + parked pages in the range
         } catch (...) {
         }
         st_->va = 0;
@@ -303,6 +303,7 @@ KvPool alloc_kvcache(PhysicalLedger& ledger, const std::string& model_id, std::u
     }
     if (ledger.device()) {
         s.dev = ledger.device();
+        s.dev_hold = s.dev->shared_from_this();  // the device outlives its pools
         s.va = s.dev->reserve(s.vpages);
     }
     s.alive = true;
@@ -314,13 +315,12 @@ void free_kvcache(PhysicalLedger& ledger, KvPool& pool) {  // :130-137
     if (!s.alive) throw UsageError("free_kvcache: pool already freed");
     Access::close_pool(ledger, s.id, s.mapped);
     if (s.dev) {
-        for (std::uint64_t p = 0; p < s.vpages; ++p) {
-            if (s.occ[p] > 0) s.dev->unmap(s.va + p * s.dev->page_bytes());
-        }
-        s.dev->reclaim(true);
+        // The whole range goes back: its live and parked pages are unmapped
+        // (after the stream drains) and their handles recycled.
         s.dev->release(s.va, s.vpages);
         s.va = 0;
         s.dev = nullptr;
+        s.dev_hold.reset();
     }
     s.alive = false;
     s.mapped = 0;
@@ -361,8 +361,21 @@ AllocResult detail::alloc_kv_into(KvPool& pool, PhysicalLedger& ledger, std::uin
     res.handles.resize(num_tokens);
     TokenSlotHandle* out = res.handles.data();
     std::uint64_t remaining = num_tokens;
-    std::uint64_t buffered_left = res.buffer_hits;
     const std::uint64_t last_word_bits = s.tpp - static_cast<std::uint64_t>(s.words - 1) * 64;
+    if (s.dev && new_pages > 0) {
+        // Every partial slot is consumed before any new page, and each new
+        // page is the lowest unmapped one at that moment, so the pages this
+        // call maps are the new_pages lowest unmapped indices: map them in one
+        // batch (contiguous runs share a cuMemSetAccess).
+        std::vector<std::uint64_t> vas;
+        vas.reserve(new_pages);
+        std::uint32_t p = s.unmapped.find_first();
+        for (std::uint64_t k = 0; k < new_pages && p != kNone; ++k) {
+            vas.push_back(s.va + static_cast<std::uint64_t>(p) * s.dev->page_bytes());
+            p = s.unmapped.find_next(static_cast<std::uint64_t>(p) + 1);
+        }
+        s.dev->map_batch(vas.data(), vas.size(), res.buffer_hits);
+    }
     while (remaining > 0) {
         bool needs_map = false;
         const std::uint32_t page = pick(s, needs_map);
@@ -370,10 +383,6 @@ AllocResult detail::alloc_kv_into(KvPool& pool, PhysicalLedger& ledger, std::uin
         if (needs_map) {
             ++s.mapped;
             s.unmapped.clear(page);
-            if (s.dev) {
-                s.dev->map(s.va + static_cast<std::uint64_t>(page) * s.dev->page_bytes(), buffered_left > 0);
-                if (buffered_left) --buffered_left;
-            }
         }
         // First free slots in ascending order (:225-241).
         std::uint64_t* words = s.page_bits(page);

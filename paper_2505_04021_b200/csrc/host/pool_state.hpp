@@ -82,6 +82,9 @@ public:
         }
     }
 
+    // Lowest set index >= i, or kNone.
+    std::uint32_t find_next(std::uint64_t i) const { return next_at(0, i); }
+
     // Lowest set index, or kNone.
     std::uint32_t find_first() const {
         if (levels_.empty() || levels_.back()[0] == 0) return kNone;
@@ -94,6 +97,21 @@ public:
     }
 
 private:
+    // Lowest set bit index >= i in level k's bit space, or kNone. Bit j of
+    // level k+1 is set iff word j of level k is non-zero, so an empty tail of
+    // the current word continues at the next non-zero word found one level up.
+    std::uint32_t next_at(std::size_t k, std::uint64_t i) const {
+        const auto& lvl = levels_[k];
+        if ((i >> 6) >= lvl.size()) return kNone;
+        const std::uint64_t w = lvl[i >> 6] & (~0ull << (i & 63));
+        if (w) return static_cast<std::uint32_t>((i >> 6) * 64 + static_cast<std::uint64_t>(__builtin_ctzll(w)));
+        if (k + 1 == levels_.size()) return kNone;
+        const std::uint32_t nw = next_at(k + 1, (i >> 6) + 1);
+        if (nw == kNone) return kNone;
+        return static_cast<std::uint32_t>(static_cast<std::uint64_t>(nw) * 64 +
+                                          static_cast<std::uint64_t>(__builtin_ctzll(lvl[nw])));
+    }
+
     std::uint64_t n_ = 0;
     std::vector<std::vector<std::uint64_t>> levels_;
 };
@@ -165,6 +183,7 @@ struct PoolState {
 
     // device side (only when the ledger has a VmmDevice)
     prism::VmmDevice* dev = nullptr;
+    std::shared_ptr<prism::VmmDevice> dev_hold;
     std::uint64_t va = 0;    // base VA of page 0
     std::unique_ptr<prism::DevicePool, void (*)(prism::DevicePool*)> mirror{nullptr, &prism::destroy_device_pool};
     std::vector<DeviceOp> ops;           // pending replay for the mirror

@@ -227,7 +227,7 @@ def vmm_probe(n=256):
 if __name__ == "__main__":
     print(torch.cuda.get_device_name(0))
     vmm_probe()
-    check_engine()
-    check_engine(layers=3, n_q=14, n_kv=2, d=64, prompt=200, output=30, chunk=64)
-    check_engine(layers=3, n_q=16, n_kv=2, d=128, prompt=100, output=30, chunk=64)
     bench_attention()
+    check_engine(layers=24, n_q=14, n_kv=2, d=64, prompt=200, output=30, chunk=64, n_req=6)
+    check_engine(layers=36, n_q=16, n_kv=2, d=128, prompt=100, output=30, chunk=64, n_req=6)
+    bench_attention(B=16, ctx=32768, reps=3)
