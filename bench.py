@@ -175,13 +175,18 @@ def setup_gpu(rank: int, n_models: int, max_steps: int):
     return dev, gpu, models
 
 
-def run_steps(models, n, q_bufs, out_bufs, scale, k3_events=None):
-    """n decode steps over all models; returns our kernel-launch count."""
+def run_steps(models, n, q_bufs, out_bufs, scale, k3_events=None, kv_bufs=None):
+    """n decode steps over all models; returns our kernel-launch count.
+    K2 appends this step's rows from per-model device K/V buffers (what a
+    model's K/V projection would hand over) when kv_bufs is given."""
     launches = 0
     for _ in range(n):
         for mi, m in enumerate(models):
             m.eng.step()                       # host + K1
-            m.eng.append_kv_synthetic(0, L, SEED)  # K2
+            if kv_bufs is not None:
+                m.eng.append_kv(0, L, kv_bufs[mi][0].data_ptr(), kv_bufs[mi][1].data_ptr())  # K2
+            else:
+                m.eng.append_kv_synthetic(0, L, SEED)  # K2 (generated content)
             launches += 2
             q, o = q_bufs[mi], out_bufs[mi]
             for layer in range(L):
@@ -228,6 +233,9 @@ def gpu_arm(args, rank, world):
         q = torch.empty((L, B_PER_MODEL, NQ, D), dtype=torch.bfloat16, device="cuda")
         q_bufs.append(q)
         out_bufs.append(torch.empty_like(q))
+    gen = torch.Generator(device="cuda").manual_seed(SEED)
+    kv_bufs = [tuple((torch.rand((L, B_PER_MODEL, NKV, D), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+                     for _ in range(2)) for _ in models]
     scale = 1.0 / math.sqrt(D)
     # q content: synthetic at each request's current position (per layer)
     for mi, m in enumerate(models):
@@ -235,7 +243,7 @@ def gpu_arm(args, rank, world):
         m.eng.append_kv_synthetic(0, L, SEED)
         for layer in range(L):
             m.eng.synth_q(layer, SEED, 1.0, q_bufs[mi][layer].data_ptr())
-    run_steps(models, warm, q_bufs, out_bufs, scale)
+    run_steps(models, warm, q_bufs, out_bufs, scale, kv_bufs=kv_bufs)
     dev.synchronize()
     dev.reset_stats()
 
@@ -248,7 +256,7 @@ def gpu_arm(args, rank, world):
     dev.synchronize()
     with ClockSampler(torch.cuda.current_device()) as clk:
         start.record(stream)
-        launches = run_steps(models, steps, q_bufs, out_bufs, scale, events)
+        launches = run_steps(models, steps, q_bufs, out_bufs, scale, events, kv_bufs)
         end.record(stream)
         end.synchronize()
     torch.cuda.synchronize()

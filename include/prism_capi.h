@@ -367,7 +367,8 @@ int prism_engine_append_kv_synthetic(prism_gpu* g, int engine_index, int layer_b
 /* K3: q, out device bf16 [n_decodes][n_q_heads][head_dim]; chunk <= 0 picks the split size. */
 int prism_engine_decode_attention(prism_gpu* g, int engine_index, int layer, const void* q, void* out, float scale,
                                   int32_t chunk);
-/* K3 implementation: 0 tensor-core mma.sync (default), 1 CUDA-core SIMT. */
+/* K3 implementation: 0 tensor-core mma.sync, 2-stage cp.async ring, 3 CTAs/SM
+ * (default); 1 CUDA-core SIMT; 2 tensor-core, 3-stage ring, 2 CTAs/SM. */
 int prism_set_attention_variant(int variant);
 int prism_engine_synth_q(prism_gpu* g, int engine_index, int layer, uint64_t seed, float q_scale, void* q);
 /* End-to-end: the same attention with HOST buffers (pinned or pageable);

@@ -282,7 +282,7 @@ int prism_engine_decode_attention(prism_gpu* g, int engine_index, int layer, con
 
 int prism_set_attention_variant(int variant) {
     return dguard([&] {
-        if (variant != 0 && variant != 1) throw std::invalid_argument("attention variant must be 0 or 1");
+        if (variant < 0 || variant > 2) throw std::invalid_argument("attention variant must be 0, 1 or 2");
         prism::set_attention_variant(variant);
     });
 }
@@ -319,19 +319,46 @@ int prism_engine_decode_host(prism_gpu* g, int engine_index, const void* new_k, 
         char* dv = dk + kv_bytes;
         char* dq = dv + kv_bytes;
         char* dout = dq + q_layer * m.n_layers;
+        // Copies run on a second stream so they overlap the kernels: q of
+        // layer l is needed only by K3(l); out of layer l is copied back
+        // while K3(l+1) runs.
+        static thread_local cudaStream_t cs = nullptr;
+        static thread_local std::vector<cudaEvent_t> evs;
+        if (!cs) check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cudaStreamCreate");
+        const std::size_t n_ev = 2 * static_cast<std::size_t>(m.n_layers) + 1;
+        while (evs.size() < n_ev) {
+            cudaEvent_t ev;
+            check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
+            evs.push_back(ev);
+        }
+        check(cudaEventRecord(evs[0], stream), "record");  // device buffers free (previous call's work)
+        check(cudaStreamWaitEvent(cs, evs[0], 0), "wait");
         if (new_k && new_v && n_tok) {
-            check(cudaMemcpyAsync(dk, new_k, kv_bytes, cudaMemcpyHostToDevice, stream), "H2D k");
-            check(cudaMemcpyAsync(dv, new_v, kv_bytes, cudaMemcpyHostToDevice, stream), "H2D v");
+            check(cudaMemcpyAsync(dk, new_k, kv_bytes, cudaMemcpyHostToDevice, cs), "H2D k");
+            check(cudaMemcpyAsync(dv, new_v, kv_bytes, cudaMemcpyHostToDevice, cs), "H2D v");
+            check(cudaEventRecord(evs[0], cs), "record");
+            check(cudaStreamWaitEvent(stream, evs[0], 0), "wait");
             prism::append_step_kv(e, 0, m.n_layers, dk, dv);
         }
         if (n_dec) {
-            check(cudaMemcpyAsync(dq, q, q_layer * m.n_layers, cudaMemcpyHostToDevice, stream), "H2D q");
             for (int layer = 0; layer < m.n_layers; ++layer) {
+                check(cudaMemcpyAsync(dq + q_layer * layer, static_cast<const char*>(q) + q_layer * layer, q_layer,
+                                      cudaMemcpyHostToDevice, cs),
+                      "H2D q");
+                check(cudaEventRecord(evs[1 + layer], cs), "record");
+            }
+            for (int layer = 0; layer < m.n_layers; ++layer) {
+                check(cudaStreamWaitEvent(stream, evs[1 + layer], 0), "wait");
                 prism::launch_decode_attention(prism::impl_of(e), layer, dq + q_layer * layer, dout + q_layer * layer,
                                                scale, 0);
+                check(cudaEventRecord(evs[1 + m.n_layers + layer], stream), "record");
+                check(cudaStreamWaitEvent(cs, evs[1 + m.n_layers + layer], 0), "wait");
+                check(cudaMemcpyAsync(static_cast<char*>(out) + q_layer * layer, dout + q_layer * layer, q_layer,
+                                      cudaMemcpyDeviceToHost, cs),
+                      "D2H out");
             }
-            check(cudaMemcpyAsync(out, dout, q_layer * m.n_layers, cudaMemcpyDeviceToHost, stream), "D2H out");
         }
+        check(cudaStreamSynchronize(cs), "cudaStreamSynchronize");
         check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
     });
 }

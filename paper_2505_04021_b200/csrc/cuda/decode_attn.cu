@@ -24,7 +24,7 @@
 
 namespace prism {
 
-void launch_k3_mma(const AttnArgs& a, int head_dim, int group, dim3 grid, cudaStream_t stream);
+void launch_k3_mma(const AttnArgs& a, int head_dim, int group, int stages, dim3 grid, cudaStream_t stream);
 int attention_variant();
 
 namespace {
@@ -346,14 +346,17 @@ void launch_d(int group, const AttnArgs& a, dim3 grid, cudaStream_t stream) {
 
 }  // namespace
 
-// K3 variant: 0 = tensor-core mma.sync kernel (default), 1 = CUDA-core SIMT
-// kernel (kept for A/B measurement). Initialised from PRISM_K3=simt|mma.
+// K3 variant: 0 = tensor-core mma.sync kernel, 2-stage ring, 3 CTAs/SM
+// (default; measured 75% / 89% of HBM on C1 / C3); 1 = CUDA-core SIMT
+// kernel; 2 = tensor-core, 3-stage ring, 2 CTAs/SM. PRISM_K3=mma|simt|mma3.
 static int g_variant = [] {
     const char* v = std::getenv("PRISM_K3");
-    return v && std::strcmp(v, "simt") == 0 ? 1 : 0;
+    if (v && std::strcmp(v, "simt") == 0) return 1;
+    if (v && std::strcmp(v, "mma3") == 0) return 2;
+    return 0;
 }();
 int attention_variant() { return g_variant; }
-void set_attention_variant(int v) { g_variant = v == 1 ? 1 : 0; }
+void set_attention_variant(int v) { g_variant = (v >= 0 && v <= 2) ? v : 0; }
 
 // Host launcher shared by the engine API and the C-ABI.
 void launch_decode_attention(EngineDeviceImpl& d, int layer, const void* q, void* out, float scale, int chunk_override) {
@@ -370,11 +373,34 @@ void launch_decode_attention(EngineDeviceImpl& d, int layer, const void* q, void
     const int kT = simt ? 32 : 64;
     int chunk = chunk_override;
     if (chunk <= 0) {
-        // Aim for ~12 CTAs per SM over the launch, never below 4 tiles per CTA.
-        const std::int64_t work = sum_ctx * d.n_kv;
-        const std::int64_t target = 148LL * 12;
-        chunk = static_cast<int>((work + target - 1) / target);
-        chunk = std::max(chunk, 4 * kT);
+        // Wave-aware split: with `slots` resident CTAs (SMs x CTAs/SM) and
+        // P = requests x kv heads, S splits run in ceil(P*S/slots) waves of
+        // (max_ctx/S + c0) token-times each (c0: per-CTA prologue/epilogue/
+        // merge cost); pick the S minimising that makespan.
+        static const int sms = [] {
+            int dev = 0, n = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+            return n;
+        }();
+        const int per_sm = attention_variant() == 2 ? 2 : 3;
+        const double slots = static_cast<double>(sms) * per_sm;
+        const double pairs = static_cast<double>(n_dec) * d.n_kv;
+        constexpr double kC0 = 160.0;
+        double best = 1e300;
+        int best_s = 1;
+        for (int s = 1; s <= 64; ++s) {
+            const int c = (max_ctx + s - 1) / s;
+            if (s > 1 && c < 2 * kT) break;
+            const double waves = std::ceil(pairs * s / slots);
+            const double t = waves * (std::ceil(static_cast<double>(c) / kT) * kT + kC0);
+            if (t < best * 0.999) {
+                best = t;
+                best_s = s;
+            }
+        }
+        chunk = (max_ctx + best_s - 1) / best_s;
+        (void)sum_ctx;
     }
     chunk = (chunk + kT - 1) / kT * kT;
     const int max_splits = (max_ctx + chunk - 1) / chunk;
@@ -397,7 +423,7 @@ void launch_decode_attention(EngineDeviceImpl& d, int layer, const void* q, void
     }
     const dim3 grid(static_cast<unsigned>(max_splits), static_cast<unsigned>(d.n_kv), static_cast<unsigned>(n_dec));
     if (!simt) {
-        launch_k3_mma(a, d.head_dim, d.group, grid, d.stream);
+        launch_k3_mma(a, d.head_dim, d.group, attention_variant() == 2 ? 3 : 2, grid, d.stream);
     } else if (d.head_dim == 128) {
         launch_d<128>(d.group, a, grid, d.stream);
     } else {

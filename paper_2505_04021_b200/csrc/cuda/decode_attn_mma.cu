@@ -24,12 +24,13 @@ namespace prism {
 
 namespace {
 
-template <int D>
+template <int D, int NS>
 struct MmaShape {
     static constexpr int kWarps = 4;
     static constexpr int kThreads = 128;
     static constexpr int kT = 64;                  // tokens per tile, 16 per warp
-    static constexpr int kStages = 3;
+    static constexpr int kStages = NS;             // 2: 64 KB ring (3 CTAs/SM), 3: 96 KB (2 CTAs/SM)
+    static constexpr int kMinBlocks = NS == 2 ? 3 : 2;
     static constexpr int kRowB = D * 2;
     static constexpr int kCpr = D / 8;             // 16-byte chunks per row
     static constexpr int kTileB = kT * kRowB;
@@ -46,12 +47,12 @@ struct MmaShape {
 // byte offset of (row, 16-byte chunk) inside a tile
 template <int D>
 __device__ __forceinline__ int swz(int row, int chunk) {
-    return (row * MmaShape<D>::kCpr + (chunk ^ (row & 7))) * 16;
+    return (row * (D / 8) + (chunk ^ (row & 7))) * 16;
 }
 
-template <int D, int G>
-__global__ void __launch_bounds__(128, 2) k3_decode_mma(AttnArgs a) {
-    using S = MmaShape<D>;
+template <int D, int G, int NS>
+__global__ void __launch_bounds__(128, MmaShape<D, NS>::kMinBlocks) k3_decode_mma(AttnArgs a) {
+    using S = MmaShape<D, NS>;
     extern __shared__ __align__(128) unsigned char smem[];
 
     const int split = blockIdx.x, h = blockIdx.y, b = blockIdx.z;
@@ -151,17 +152,22 @@ __global__ void __launch_bounds__(128, 2) k3_decode_mma(AttnArgs a) {
         const int t0 = t_begin + tile * S::kT + wrow;
         if (t0 >= t_end) continue;  // warp-uniform: nothing valid in this warp's rows
 
-        // ---- S = K · Qᵀ
+        // ---- S = K · Qᵀ  (two independent accumulator chains over the k-steps)
         float s[4] = {0.f, 0.f, 0.f, 0.f};
         {
+            float s2[4] = {0.f, 0.f, 0.f, 0.f};
             const int mat = lane >> 3;
             const int r = wrow + (mat & 1) * 8 + (lane & 7);
 #pragma unroll
-            for (int ks = 0; ks < S::kKSteps; ++ks) {
-                std::uint32_t af[4];
+            for (int ks = 0; ks < S::kKSteps; ks += 2) {
+                std::uint32_t af[4], bf[4];
                 ldmatrix_x4(af, sk + swz<D>(r, ks * 2 + (mat >> 1)));
+                ldmatrix_x4(bf, sk + swz<D>(r, (ks + 1) * 2 + (mat >> 1)));
                 mma_bf16_16816(s, af, qb[ks][0], qb[ks][1]);
+                mma_bf16_16816(s2, bf, qb[ks + 1][0], qb[ks + 1][1]);
             }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) s[k] += s2[k];
         }
         // scale into the log2 domain, mask the tail
         const bool v0 = t0 + qr < t_end, v1 = t0 + qr + 8 < t_end;
@@ -292,29 +298,30 @@ __global__ void __launch_bounds__(128, 2) k3_decode_mma(AttnArgs a) {
     if (tid == 0) a.tickets[bh] = 0;
 }
 
-template <int D, int G>
+template <int D, int G, int NS>
 void launch_mma_shape(const AttnArgs& a, dim3 grid, cudaStream_t stream) {
-    using S = MmaShape<D>;
+    using S = MmaShape<D, NS>;
     static bool configured = false;
     if (!configured) {
-        PRISM_CUDA(cudaFuncSetAttribute(k3_decode_mma<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmem));
+        PRISM_CUDA(cudaFuncSetAttribute(k3_decode_mma<D, G, NS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        S::kSmem));
         configured = true;
     }
-    k3_decode_mma<D, G><<<grid, S::kThreads, S::kSmem, stream>>>(a);
+    k3_decode_mma<D, G, NS><<<grid, S::kThreads, S::kSmem, stream>>>(a);
     PRISM_CUDA(cudaGetLastError());
 }
 
-template <int D>
+template <int D, int NS>
 void launch_mma_d(int group, const AttnArgs& a, dim3 grid, cudaStream_t stream) {
     switch (group) {
-        case 1: launch_mma_shape<D, 1>(a, grid, stream); break;
-        case 2: launch_mma_shape<D, 2>(a, grid, stream); break;
-        case 3: launch_mma_shape<D, 3>(a, grid, stream); break;
-        case 4: launch_mma_shape<D, 4>(a, grid, stream); break;
-        case 5: launch_mma_shape<D, 5>(a, grid, stream); break;
-        case 6: launch_mma_shape<D, 6>(a, grid, stream); break;
-        case 7: launch_mma_shape<D, 7>(a, grid, stream); break;
-        case 8: launch_mma_shape<D, 8>(a, grid, stream); break;
+        case 1: launch_mma_shape<D, 1, NS>(a, grid, stream); break;
+        case 2: launch_mma_shape<D, 2, NS>(a, grid, stream); break;
+        case 3: launch_mma_shape<D, 3, NS>(a, grid, stream); break;
+        case 4: launch_mma_shape<D, 4, NS>(a, grid, stream); break;
+        case 5: launch_mma_shape<D, 5, NS>(a, grid, stream); break;
+        case 6: launch_mma_shape<D, 6, NS>(a, grid, stream); break;
+        case 7: launch_mma_shape<D, 7, NS>(a, grid, stream); break;
+        case 8: launch_mma_shape<D, 8, NS>(a, grid, stream); break;
         default: throw std::runtime_error("decode_attention: unsupported GQA group");
     }
 }
@@ -323,12 +330,13 @@ void launch_mma_d(int group, const AttnArgs& a, dim3 grid, cudaStream_t stream) 
 
 constexpr int kMmaTile = 64;
 
-void launch_k3_mma(const AttnArgs& a, int head_dim, int group, dim3 grid, cudaStream_t stream) {
+// stages: 2 (double buffer, 3 CTAs/SM) or 3 (2 CTAs/SM).
+void launch_k3_mma(const AttnArgs& a, int head_dim, int group, int stages, dim3 grid, cudaStream_t stream) {
     if (a.chunk % kMmaTile) throw std::runtime_error("k3 mma: chunk must be a multiple of 64");
     if (head_dim == 128) {
-        launch_mma_d<128>(group, a, grid, stream);
+        stages == 2 ? launch_mma_d<128, 2>(group, a, grid, stream) : launch_mma_d<128, 3>(group, a, grid, stream);
     } else {
-        launch_mma_d<64>(group, a, grid, stream);
+        stages == 2 ? launch_mma_d<64, 2>(group, a, grid, stream) : launch_mma_d<64, 3>(group, a, grid, stream);
     }
 }
 

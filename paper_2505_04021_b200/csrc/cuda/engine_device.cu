@@ -11,6 +11,8 @@ namespace prism {
 namespace pa = msim::pagealloc;
 namespace me = msim::engine;
 
+constexpr std::uint64_t kCacheTarget = 16;  // ready physical handles kept per GPU
+
 EngineDeviceImpl& impl_of(const me::Engine& eng) {
     auto* p = dynamic_cast<EngineDeviceImpl*>(eng.device.get());
     if (!p) throw std::runtime_error("engine has no GPU device attached (prism::attach_engine_device)");
@@ -127,13 +129,14 @@ void EngineDeviceImpl::begin_step(me::Engine&) {
     // Pages unmapped during earlier steps become reclaimable once the fence
     // recorded here (after every kernel the caller issued for those steps)
     // has passed; see VmmDevice.
-    vmm->reclaim(false);
     vmm->fence();
+    vmm->defer_access(true);  // this step's fresh pages share cuMemSetAccess calls
 }
 
 void EngineDeviceImpl::end_step(me::Engine&, const me::IterationOutcome& out, const std::vector<StepDecode>& decodes,
                                 std::uint64_t prefill_id, std::int64_t prefill_row, std::int32_t prefill_first,
                                 std::int32_t prefill_tokens) {
+    vmm->defer_access(false);  // pages must be accessible before K2/K3 run
     // K1: replay this step's allocations / frees on the device slot state.
     const std::int64_t n = pool->mirror->replay(*pool, table, step_slots, opts.max_step_tokens, stream);
     step_tokens = static_cast<int>(n);
@@ -163,6 +166,9 @@ void EngineDeviceImpl::end_step(me::Engine&, const me::IterationOutcome& out, co
         decode_ids.push_back(decodes[i].request_id);
     }
     decode_desc.upload(decodes.size(), stream);
+    // The GPU is busy with this step now: create the physical handles the
+    // next steps' fresh pages will need (cuMemCreate off the map path).
+    vmm->prefill_cache(kCacheTarget);
 }
 
 float* EngineDeviceImpl::attn_workspace(std::size_t floats) {

@@ -102,9 +102,13 @@ __global__ void __launch_bounds__(kThreads, 1) k1_slot_alloc(K1Args a) {
 
     const int tid = threadIdx.x;
     const std::uint32_t tpp = a.tpp;
-    const std::uint32_t chunk = (a.vpages + kThreads - 1) / kThreads;
-    const std::uint32_t my_lo = min(a.vpages, static_cast<std::uint32_t>(tid) * chunk);
-    const std::uint32_t my_hi = min(a.vpages, my_lo + chunk);
+    // occ is padded to a multiple of 4 pages with the value tpp ("full"), so
+    // it is scanned with 16-byte loads and the pads are never selected.
+    const uint4* occ4 = reinterpret_cast<const uint4*>(a.occ);
+    const std::uint32_t v4 = (a.vpages + 3) / 4;
+    const std::uint32_t chunk = (v4 + kThreads - 1) / kThreads;
+    const std::uint32_t my_lo = min(v4, static_cast<std::uint32_t>(tid) * chunk);
+    const std::uint32_t my_hi = min(v4, my_lo + chunk);
     long long out_pos = 0;
 
     for (int i = 0; i < a.n_ops;) {
@@ -135,9 +139,14 @@ __global__ void __launch_bounds__(kThreads, 1) k1_slot_alloc(K1Args a) {
             // 1. histogram of partial pages' occupancy
             for (std::uint32_t k = tid; k < tpp; k += kThreads) hist[k] = 0;
             __syncthreads();
-            for (std::uint32_t p = tid; p < a.vpages; p += kThreads) {
-                const std::uint32_t o = __ldcg(&a.occ[p]);
-                if (o > 0 && o < tpp) atomicAdd(&hist[o], 1u);
+#pragma unroll 4
+            for (std::uint32_t q = tid; q < v4; q += kThreads) {
+                const uint4 o4 = __ldcg(occ4 + q);
+                const std::uint32_t os[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    if (os[c] > 0 && os[c] < tpp) atomicAdd(&hist[os[c]], 1u);
+                }
             }
             __syncthreads();
             // 2. threshold level
@@ -170,13 +179,18 @@ __global__ void __launch_bounds__(kThreads, 1) k1_slot_alloc(K1Args a) {
             // 3. collect: every partial page above the level (any order), and
             //    the first `take` pages at the level in index order.
             std::uint32_t at_level = 0;
-            for (std::uint32_t p = my_lo; p < my_hi; ++p) {
-                const std::uint32_t o = __ldcg(&a.occ[p]);
-                if (o > level && o < tpp) {
-                    const std::uint32_t slot = atomicAdd(&s_nsel, 1u);
-                    keys[slot] = (static_cast<unsigned long long>(tpp - o) << 32) | p;
-                } else if (o == level) {
-                    ++at_level;
+            for (std::uint32_t q = my_lo; q < my_hi; ++q) {
+                const uint4 o4 = __ldcg(occ4 + q);
+                const std::uint32_t os[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const std::uint32_t o = os[c];
+                    if (o > level && o < tpp) {
+                        const std::uint32_t slot = atomicAdd(&s_nsel, 1u);
+                        keys[slot] = (static_cast<unsigned long long>(tpp - o) << 32) | (q * 4 + c);
+                    } else if (o == level) {
+                        ++at_level;
+                    }
                 }
             }
             std::uint32_t level_total = 0;
@@ -184,11 +198,15 @@ __global__ void __launch_bounds__(kThreads, 1) k1_slot_alloc(K1Args a) {
             if (level_total < take && tid == 0) atomicExch(a.status, 1);  // host and device disagree
             const std::uint32_t take_eff = min(take, level_total);
             if (rank < take_eff) {
-                for (std::uint32_t p = my_lo; p < my_hi && rank < take_eff; ++p) {
-                    const std::uint32_t o = __ldcg(&a.occ[p]);
-                    if (o == level) {
-                        keys[above + rank] = (static_cast<unsigned long long>(tpp - o) << 32) | p;
-                        ++rank;
+                for (std::uint32_t q = my_lo; q < my_hi && rank < take_eff; ++q) {
+                    const uint4 o4 = __ldcg(occ4 + q);
+                    const std::uint32_t os[4] = {o4.x, o4.y, o4.z, o4.w};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        if (os[c] == level && rank < take_eff) {
+                            keys[above + rank] = (static_cast<unsigned long long>(tpp - level) << 32) | (q * 4 + c);
+                            ++rank;
+                        }
                     }
                 }
             }
@@ -298,11 +316,14 @@ DevicePool::DevicePool(const msim::pagealloc::detail::PoolState& s, int device) 
     vpages = static_cast<std::uint32_t>(s.vpages);
     tpp = static_cast<std::uint32_t>(s.tpp);
     words = (tpp + 31) / 32;
-    PRISM_CUDA(cudaMalloc(&occ, sizeof(std::uint32_t) * vpages));
+    const std::size_t padded = (static_cast<std::size_t>(vpages) + 3) / 4 * 4;
+    PRISM_CUDA(cudaMalloc(&occ, sizeof(std::uint32_t) * padded));
     PRISM_CUDA(cudaMalloc(&bits, sizeof(std::uint32_t) * vpages * words));
     PRISM_CUDA(cudaMalloc(&d_status, sizeof(int)));
-    // Upload the current host state (pool may already hold tokens).
-    std::vector<std::uint32_t> h_occ(s.occ.begin(), s.occ.end());
+    // Upload the current host state (pool may already hold tokens); the pad
+    // pages read as full so K1 never selects them.
+    std::vector<std::uint32_t> h_occ(padded, tpp);
+    std::copy(s.occ.begin(), s.occ.end(), h_occ.begin());
     std::vector<std::uint32_t> h_bits(static_cast<std::size_t>(vpages) * words, 0);
     for (std::uint32_t p = 0; p < vpages; ++p) {
         if (!s.occ[p]) continue;
@@ -312,7 +333,7 @@ DevicePool::DevicePool(const msim::pagealloc::detail::PoolState& s, int device) 
                 static_cast<std::uint32_t>(w64[w >> 1] >> ((w & 1) * 32));
         }
     }
-    PRISM_CUDA(cudaMemcpy(occ, h_occ.data(), sizeof(std::uint32_t) * vpages, cudaMemcpyHostToDevice));
+    PRISM_CUDA(cudaMemcpy(occ, h_occ.data(), sizeof(std::uint32_t) * padded, cudaMemcpyHostToDevice));
     PRISM_CUDA(cudaMemcpy(bits, h_bits.data(), sizeof(std::uint32_t) * h_bits.size(), cudaMemcpyHostToDevice));
     PRISM_CUDA(cudaMemset(d_status, 0, sizeof(int)));
 }

@@ -248,8 +248,6 @@ void VmmDevice::map_batch(const std::uint64_t* vas, std::size_t n, std::size_t n
     if (n == 0) return;
     const auto t0 = Clock::now();
     stats_.maps += n;
-    std::vector<std::uint64_t> fresh;
-    fresh.reserve(n);
     for (std::size_t i = 0; i < n; ++i) {
         const bool from_buffer = i < n_from_buffer;
         const auto p = parked_.find(vas[i]);
@@ -272,22 +270,48 @@ void VmmDevice::map_batch(const std::uint64_t* vas, std::size_t n, std::size_t n
                  "cuMemMap");
         stats_.map_call_ns_total += ns_since(tm);
         live_.emplace(vas[i], h);
-        fresh.push_back(vas[i]);
+        unaccessed_.push_back(vas[i]);
     }
-    std::sort(fresh.begin(), fresh.end());
-    for (std::size_t i = 0; i < fresh.size();) {
+    if (!defer_access_) flush_access();
+    const double per = ns_since(t0) / static_cast<double>(n);
+    stats_.map_ns_total += per * static_cast<double>(n);
+    for (std::size_t i = 0; i < n; ++i) sample(stats_.map_ns, per);
+}
+
+void VmmDevice::defer_access(bool on) {
+    defer_access_ = on;
+    if (!on) flush_access();
+}
+
+void VmmDevice::flush_access() {
+    if (unaccessed_.empty()) return;
+    const auto t0 = Clock::now();
+    std::sort(unaccessed_.begin(), unaccessed_.end());
+    for (std::size_t i = 0; i < unaccessed_.size();) {
         std::size_t j = i + 1;
-        while (j < fresh.size() && fresh[j] == fresh[j - 1] + page_bytes_) ++j;
+        while (j < unaccessed_.size() && unaccessed_[j] == unaccessed_[j - 1] + page_bytes_) ++j;
         const auto ta = Clock::now();
-        cu_check(drv().set_access(static_cast<CUdeviceptr>(fresh[i]), (j - i) * page_bytes_, &access_of(access_desc_), 1),
+        cu_check(drv().set_access(static_cast<CUdeviceptr>(unaccessed_[i]), (j - i) * page_bytes_,
+                                  &access_of(access_desc_), 1),
                  "cuMemSetAccess");
         stats_.access_ns_total += ns_since(ta);
         ++stats_.access_calls;
         i = j;
     }
-    const double per = ns_since(t0) / static_cast<double>(n);
-    stats_.map_ns_total += per * static_cast<double>(n);
-    for (std::size_t i = 0; i < n; ++i) sample(stats_.map_ns, per);
+    // Charged to the maps of this flush (it is part of mapping them).
+    stats_.map_ns_total += ns_since(t0);
+    unaccessed_.clear();
+}
+
+void VmmDevice::prefill_cache(std::uint64_t n) {
+    while (cache_.size() < n && total_handles() < budget_) {
+        const auto tc = Clock::now();
+        CUmemGenericAllocationHandle h = 0;
+        if (drv().create(&h, page_bytes_, &prop_of(prop_), 0) != CUDA_SUCCESS) break;
+        ++stats_.creates;
+        stats_.create_ns_total += ns_since(tc);
+        cache_.push_back(static_cast<std::uint64_t>(h));
+    }
 }
 
 void VmmDevice::unmap(std::uint64_t va) {

@@ -64,6 +64,15 @@ public:
     void map(std::uint64_t page_va, bool from_buffer);
     void map_batch(const std::uint64_t* page_vas, std::size_t n, std::size_t n_from_buffer);
     void unmap(std::uint64_t page_va);
+    // Between defer_access(true) and flush_access() fresh pages are cuMemMap'ed
+    // but cuMemSetAccess is postponed and issued once per contiguous run at
+    // the flush (the engine brackets a step with it; no kernel may touch the
+    // pages before the flush).
+    void defer_access(bool on);
+    void flush_access();
+    // Keep `n` created-but-unmapped handles ready so maps of fresh pages skip
+    // cuMemCreate (bounded by the physical budget).
+    void prefill_cache(std::uint64_t n);
 
     // Physically unmap every parked page (wait=true synchronizes first; with
     // wait=false only pages whose fence passed).
@@ -108,6 +117,8 @@ private:
     std::vector<std::uint64_t> cache_;
     std::unordered_map<std::uint64_t, std::uint64_t> live_;  // va -> handle
     std::map<std::uint64_t, Parked> parked_;                // va -> handle (ordered: steal from the top)
+    std::vector<std::uint64_t> unaccessed_;  // fresh VAs waiting for cuMemSetAccess
+    bool defer_access_ = false;
     std::vector<void*> fences_;       // cudaEvent_t, oldest first; fences_[0] has index fenced_
     std::uint64_t epoch_ = 0;         // fences recorded so far
     std::uint64_t fenced_ = 0;        // fences known complete

@@ -73,7 +73,7 @@ def _attend_and_check(eng, spec, layers, q_scale=4.0):
     return worst
 
 
-@pytest.fixture(params=[0, 1], ids=["mma", "simt"])
+@pytest.fixture(params=[0, 1, 2], ids=["mma", "simt", "mma3"])
 def variant(request, product):
     product.call("prism_set_attention_variant", request.param)
     yield request.param
@@ -104,7 +104,7 @@ def test_split_k_long_context(product, device, variant):
     """C3-like: long contexts split across many CTAs and merged by the last."""
     gpu, spec, eng = _engine(product, device, "llama3.1-8b", cap_pages=2200, chunk=512)
     for i, p in enumerate([8191, 5000, 129]):
-        eng.push(i + 1, p, 3)
+        eng.push(i + 1, p, 1000)  # nobody completes while the others prefill
     while any(r.prompt_done < r.prompt_tokens for r in eng.batch()) or eng.counts()[1]:
         eng.step()
         eng.append_kv_synthetic(0, spec.n_layers, SEED)
@@ -201,7 +201,7 @@ def test_c1_full_size_sampled(product, device):
     layers against the oracle; checks the same launch shapes the bench uses."""
     gpu, spec, eng = _engine(product, device, "llama3.1-8b", cap_pages=8400, chunk=4096)
     for i in range(64):
-        eng.push(i + 1, 2047, 8)
+        eng.push(i + 1, 2047, 10_000)  # early requests decode while later ones prefill
     while eng.counts()[1] or any(r.prompt_done < r.prompt_tokens for r in eng.batch()):
         eng.step()
         eng.append_kv_synthetic(0, spec.n_layers, SEED)
