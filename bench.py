@@ -117,13 +117,32 @@ class ClockSampler:
 # ---------------------------------------------------------------- workload
 
 
-def c1_requests(n_models: int, rank: int):
+def model_ids(world: int):
+    return [f"llama3-8b#{i}" for i in range(MODELS_PER_GPU * world)]
+
+
+def placement_for(world: int, rank: int):
+    """Models of this rank: rank 0 runs the global scheduler (Algorithm 1,
+    place_models through the C-ABI) over all GPUs and broadcasts the plan."""
+    if world == 1:
+        return model_ids(1)
+    from paper_2505_04021_b200 import cluster, msim
+
+    plan = None
+    demands = [msim.ModelDemandPy(msim.ModelSpec.llm(mid, L, NQ, NKV, D, weight_bytes=16_060_000_000), rate=30.0)
+               for mid in model_ids(world)]
+    if rank == 0:
+        plan = cluster.plan(demands, world, 180 * 10**9)
+    plan = cluster.broadcast_plan(plan)
+    return [m.spec.model_id for m in cluster.shard(demands, plan, rank)]
+
+
+def c1_requests(mids):
     """Per model: 64 requests from a seeded Poisson trace (prompt ~2K)."""
     from paper_2505_04021_b200 import msim
 
     out = []
-    for m in range(n_models):
-        mid = f"llama3-8b#{rank}.{m}"
+    for mid in mids:
         prof = msim.ModelProfile(mid, [(0.0, 60.0, 30.0)], prompt_median=CTX - 1, prompt_sigma=0.0,
                                  output_median=256, output_sigma=0.4)
         trace = [e for e in msim.synth_trace([prof], TRACE_SEED) if e.model_id == mid][:B_PER_MODEL]
@@ -148,7 +167,7 @@ class Model:
         self.mid = mid
 
 
-def setup_gpu(rank: int, n_models: int, max_steps: int):
+def setup_gpu(rank: int, mids, max_steps: int):
     import torch
 
     from paper_2505_04021_b200 import msim
@@ -158,11 +177,11 @@ def setup_gpu(rank: int, n_models: int, max_steps: int):
     # contexts grow by one token per decode step: B_PER_MODEL prefill steps
     # (earlier requests decode meanwhile) + every later step of the run
     grow = B_PER_MODEL + max_steps
-    pages = n_models * (B_PER_MODEL * (CTX + grow + tpp) // tpp + 64)
+    pages = len(mids) * (B_PER_MODEL * (CTX + grow + tpp) // tpp + 64)
     gpu = msim.GpuState(rank, pages + 64)
     gpu.ledger.attach_device(dev)
     gpu.ledger.refill_buffer(8)
-    models = [Model(gpu, mid, trace, max_steps) for mid, trace in c1_requests(n_models, rank)]
+    models = [Model(gpu, mid, trace, max_steps) for mid, trace in c1_requests(mids)]
     # prefill: one 2K chunk per step (allocation + K2 synthetic K/V writes)
     for m in models:
         while True:
@@ -226,7 +245,8 @@ def gpu_arm(args, rank, world):
 
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
     steps, warm = args.steps, args.warmup
-    dev, gpu, models = setup_gpu(rank, MODELS_PER_GPU, steps * 2 + warm * 2 + 8)
+    mids = placement_for(world, rank)
+    dev, gpu, models = setup_gpu(rank, mids, steps * 2 + warm * 2 + 8)
     stream = torch.cuda.ExternalStream(dev.stream())
     q_bufs, out_bufs = [], []
     for m in models:
@@ -268,11 +288,14 @@ def gpu_arm(args, rank, world):
     vstats = dev.stats()
 
     ms_max = ms_total
+    tokens = steps * len(models) * B_PER_MODEL
     if world > 1:
         t = torch.tensor([ms_total], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
-    tokens = steps * len(models) * B_PER_MODEL * world
+        n = torch.tensor([tokens], device="cuda", dtype=torch.float64)
+        dist.all_reduce(n, op=dist.ReduceOp.SUM)
+        tokens = int(n.item())
     value = tokens / (ms_max / 1e3)
 
     # ---- e2e through the C-ABI with host buffers
@@ -342,16 +365,73 @@ def e2e_arm(models, steps, scale, dev, world):
             m.eng.step()
             m.eng.decode_host(host_k.data_ptr(), host_v.data_ptr(), host_q.data_ptr(), host_o.data_ptr(), scale)
     sec = time.perf_counter() - t0
+    tokens = steps * len(models) * B_PER_MODEL
     if world > 1:
         import torch.distributed as dist
 
-        t = torch.tensor([sec], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        sec = float(t.item())
-    tokens = steps * len(models) * B_PER_MODEL * world
+        t = torch.tensor([sec, tokens], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t[:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:], op=dist.ReduceOp.SUM)
+        sec, tokens = float(t[0].item()), int(t[1].item())
     return {"value": round(tokens / sec, 1), "unit": "tokens/s",
             "h2d_bytes_per_step": len(models) * (2 * kv_elems + q_elems) * 2,
             "d2h_bytes_per_step": len(models) * q_elems * 2, "api": "prism_engine_step + prism_engine_decode_host"}
+
+
+C2_SHAPES = {  # L, n_q, n_kv, d, weight GB
+    "qwen2.5-0.5b": (24, 14, 2, 64, 0.99), "llama3.2-1b": (16, 32, 8, 64, 2.47),
+    "qwen2.5-1.5b": (28, 12, 2, 128, 3.09), "qwen2.5-3b": (36, 16, 2, 128, 6.17),
+    "llama3.2-3b": (28, 24, 8, 128, 6.43), "qwen2.5-7b": (28, 28, 4, 128, 15.23),
+    "mistral-7b": (32, 32, 8, 128, 14.5), "llama3.1-8b": (32, 32, 8, 128, 16.06),
+}
+
+
+def page_churn_c2(max_rounds=2500, kv_pages=6000, horizon_s=60.0):
+    """BASELINE config 2 as a page map/unmap measurement: the 8 model shapes
+    space-share one B200 ledger (weights accounted at their real size, KV
+    budget `kv_pages`), bursty 10 s on / 10 s off arrivals in alternating
+    phases (seeded Poisson, SURVEY Appendix A scenario 2), driven by the
+    shared TraceDriver; every step runs K1 + K2 on the GPU, so every logical
+    map/unmap is real CUDA VMM work (park / revive / steal)."""
+    import torch
+
+    from paper_2505_04021_b200 import msim
+    from paper_2505_04021_b200.driver import TraceDriver
+
+    dev = msim.Device(torch.cuda.current_device())
+    weight_pages = sum(math.ceil(s[4] * 1e9 / (2 << 20)) for s in C2_SHAPES.values())
+    gpu = msim.GpuState(0, weight_pages + kv_pages)
+    gpu.ledger.attach_device(dev)
+    gpu.ledger.refill_buffer(8)
+    engines = {}
+    profiles = []
+    for k, (name, (layers, nq, nkv, d, wgb)) in enumerate(C2_SHAPES.items()):
+        spec = msim.ModelSpec.llm(name, layers, nq, nkv, d, weight_bytes=int(wgb * 1e9), chunk_size=512)
+        act = gpu.activate(spec)
+        gpu.finish_activation(act.engine_index)
+        e = gpu.engine(act.engine_index)
+        e.attach_device(max_step_tokens=512 + 1 + 1024)
+        engines[name] = e
+        segs = [(t, t + 10.0, 12.0 if (int(t // 10) + k) % 2 == 0 else 0.0) for t in range(0, int(horizon_s), 10)]
+        profiles.append(msim.ModelProfile(name, segs, 1024, 0.6, 256, 0.6))
+    trace = msim.synth_trace(profiles, TRACE_SEED)
+    layers_of = {n: s[0] for n, s in C2_SHAPES.items()}
+    dev.reset_stats()
+    t0 = time.perf_counter()
+    drv = TraceDriver(engines, trace, on_step=lambda mid, e, o: e.append_kv_synthetic(0, layers_of[mid], SEED))
+    drv.run(max_rounds)
+    dev.synchronize()
+    wall = time.perf_counter() - t0
+    st = dev.stats()
+    res = page_map_summary(st, len(drv.outcomes))
+    res.update({"workload": f"C2: 8 shapes on one ledger ({weight_pages} weight + {kv_pages} KV pages), bursty "
+                            f"10s on/off, {len(drv.outcomes)} engine steps, {drv.next} arrivals",
+                "steals": st["steals"], "driver_creates": st["creates"], "access_calls": st["access_calls"],
+                "create_us_total": round(st["create_ns_total"] / 1e3, 1),
+                "reference_modelled_us_per_map": 200.0, "wall_s": round(wall, 2),
+                "preemptions": sum(len(o.preemptions) for _, o in drv.outcomes)})
+    dev.close()
+    return res
 
 
 def page_map_summary(st, steps):
@@ -385,7 +465,7 @@ def cpu_arm(args, sample_seqs=8, sample_layers=4, ref_steps=4):
         ref = oracle.reference()
         gpu = msim.GpuState(0, 85830, lib=ref)
         engines = []
-        for mid, trace in c1_requests(MODELS_PER_GPU, 0):
+        for mid, trace in c1_requests(model_ids(1)):
             spec = msim.ModelSpec.llm(mid, L, NQ, NKV, D, weight_bytes=16_060_000_000, chunk_size=4096)
             act = gpu.activate(spec)
             gpu.finish_activation(act.engine_index)
@@ -453,6 +533,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="prism", choices=["prism", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-churn", action="store_true", help="skip the C2 page map/unmap measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -486,6 +567,11 @@ def main():
                 res["cpu_baseline"] = cpu_arm(args)
             except Exception as e:  # reported, never substituted for the GPU number
                 res["cpu_baseline"] = {"error": str(e)}
+        if world == 1 and not args.no_churn:
+            try:
+                res["page_map_c2"] = page_churn_c2()
+            except Exception as e:
+                res["page_map_c2"] = {"error": str(e)}
         print(json.dumps(res))
     if world > 1:
         import torch.distributed as dist

@@ -15,6 +15,7 @@ import json
 import random
 
 from paper_2505_04021_b200 import capi, msim
+from paper_2505_04021_b200.driver import TraceDriver
 
 PAGE = 2 << 20
 
@@ -216,32 +217,11 @@ def engine_trace(lib, name, seed, capacity, models, rate, horizon, prompt, outpu
             segs = [(0.0, horizon, rate)]
         profiles.append(msim.ModelProfile(mid, segs, prompt[0], prompt[1], output[0], output[1]))
     trace = msim.synth_trace(profiles, seed, lib=lib)
-    now = 0
-    nxt = 0
-    outcomes = []
-    params = msim.EngineParams()
-    rid = 0
-    order = list(engines)
-    for _ in range(steps):
-        while nxt < len(trace) and int(trace[nxt].arrival_s * 1e6) <= now:
-            ev = trace[nxt]
-            rid += 1
-            engines[ev.model_id].push(rid, ev.prompt_tokens, ev.output_tokens)
-            nxt += 1
-        ran = False
-        for mid in order:
-            e = engines[mid]
-            if not e.has_runnable_work():
-                continue
-            o = e.step(params, now)
-            now += o.duration_us
-            ran = True
-            outcomes.append([mid, o.duration_us, o.chunk_tokens, o.decode_tokens, o.first_tokens, o.completions,
-                             o.preemptions, o.pages_mapped_direct, o.prefill_paused])
-        if not ran:
-            if nxt >= len(trace):
-                break
-            now = max(now, int(trace[nxt].arrival_s * 1e6))
+    drv = TraceDriver(engines, trace)
+    drv.run(steps)
+    now = drv.now
+    outcomes = [[mid, o.duration_us, o.chunk_tokens, o.decode_tokens, o.first_tokens, o.completions, o.preemptions,
+                 o.pages_mapped_direct, o.prefill_paused] for mid, o in drv.outcomes]
     gpu.ledger.check_invariants()
     tables = {}
     for mid, e in engines.items():
