@@ -56,6 +56,16 @@ void append_step_kv_synthetic(msim::engine::Engine& eng, int layer_begin, int la
 // applied to q·k (pass 1/sqrt(head_dim) for standard attention).
 void decode_attention(msim::engine::Engine& eng, int layer, const void* q, void* out, float scale);
 
+// End-to-end decode with HOST buffers for the last step: H2D of the new K/V
+// rows ([n_layers][last_step_tokens][n_kv][head_dim], may be null) and q
+// ([n_layers][last_step_decodes][n_q][head_dim]) on the engine's copy
+// stream, K2 + one K3 per layer on the compute stream, D2H of out (same shape
+// as q) layer by layer as each K3 finishes. wait=false returns once enqueued
+// (wait_host() blocks until `out` is complete).
+void decode_host(msim::engine::Engine& eng, const void* new_k, const void* new_v, const void* q, void* out,
+                 float scale, bool wait);
+void wait_host(const msim::engine::Engine& eng);
+
 // Fills q [last_step_decodes][n_q][head_dim] with synth content (kind = Q, at
 // each request's newest position) times q_scale.
 void synth_decode_q(msim::engine::Engine& eng, int layer, std::uint64_t seed, float q_scale, void* q);

@@ -327,6 +327,8 @@ typedef struct {
     double create_ns_total, map_call_ns_total, access_ns_total; /* per driver call kind */
     uint64_t access_calls;
     uint64_t steals; /* parked pages moved to another VA (cross-model memory movement) */
+    double steal_ns_total; /* cuMemUnmap time of steals (included in map_ns_total) */
+    double prefill_ns_total; /* handle creation ahead of need, outside the map path */
 } prism_device_stats;
 int prism_device_stats_get(const prism_device* d, prism_device_stats* out);
 int prism_device_reset_stats(prism_device* d);
@@ -367,8 +369,9 @@ int prism_engine_append_kv_synthetic(prism_gpu* g, int engine_index, int layer_b
 /* K3: q, out device bf16 [n_decodes][n_q_heads][head_dim]; chunk <= 0 picks the split size. */
 int prism_engine_decode_attention(prism_gpu* g, int engine_index, int layer, const void* q, void* out, float scale,
                                   int32_t chunk);
-/* K3 implementation: 0 tensor-core mma.sync, 2-stage cp.async ring, 3 CTAs/SM
- * (default); 1 CUDA-core SIMT; 2 tensor-core, 3-stage ring, 2 CTAs/SM. */
+/* K3 implementation: 0 tensor-core mma.sync, 2-stage cp.async ring, 3 CTAs/SM,
+ * split-K (default); 1 CUDA-core SIMT; 2 tensor-core, 3-stage ring, 2 CTAs/SM;
+ * 3 tensor-core stream-K persistent (equal tile ranges per CTA). */
 int prism_set_attention_variant(int variant);
 int prism_engine_synth_q(prism_gpu* g, int engine_index, int layer, uint64_t seed, float q_scale, void* q);
 /* End-to-end: the same attention with HOST buffers (pinned or pageable);
@@ -376,6 +379,11 @@ int prism_engine_synth_q(prism_gpu* g, int engine_index, int layer, uint64_t see
  * and K3 for every layer, copies out back; synchronous. q/out: [n_layers][n_decodes][n_q][d]. */
 int prism_engine_decode_host(prism_gpu* g, int engine_index, const void* new_k, const void* new_v, const void* q,
                              void* out, float scale);
+/* Same, enqueued only (copies on a per-engine copy stream overlapping the
+ * kernels); host buffers must stay valid until prism_engine_wait_host. */
+int prism_engine_decode_host_async(prism_gpu* g, int engine_index, const void* new_k, const void* new_v,
+                                   const void* q, void* out, float scale);
+int prism_engine_wait_host(prism_gpu* g, int engine_index);
 int prism_engine_synchronize(prism_gpu* g, int engine_index);
 
 #ifdef __cplusplus

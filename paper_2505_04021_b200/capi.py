@@ -157,7 +157,8 @@ class DeviceStats(C.Structure):
         (n, c_double) for n in ("map_ns_total", "unmap_ns_total", "map_ns_p50", "map_ns_p99", "unmap_ns_p50",
                                 "unmap_ns_p99")] + [(n, c_uint64) for n in ("buffered", "cached", "pending")] + [
         (n, c_double) for n in ("create_ns_total", "map_call_ns_total", "access_ns_total")] + [
-        ("access_calls", c_uint64), ("steals", c_uint64)]
+        ("access_calls", c_uint64), ("steals", c_uint64), ("steal_ns_total", c_double),
+        ("prefill_ns_total", c_double)]
 
 
 class EngineDeviceOptions(C.Structure):
@@ -262,6 +263,8 @@ _DEVICE_DECLS = {
     "prism_set_attention_variant": (c_int, [c_int]),
     "prism_engine_decode_host": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_float]),
     "prism_engine_synchronize": (c_int, [c_void_p, c_int]),
+    "prism_engine_decode_host_async": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_float]),
+    "prism_engine_wait_host": (c_int, [c_void_p, c_int]),
 }
 
 HOST_SYMBOLS = sorted(_HOST_DECLS)

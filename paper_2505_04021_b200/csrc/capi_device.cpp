@@ -122,6 +122,8 @@ int prism_device_stats_get(const prism_device* d, prism_device_stats* out) {
         out->access_ns_total = s.access_ns_total;
         out->access_calls = s.access_calls;
         out->steals = s.steals;
+        out->steal_ns_total = s.steal_ns_total;
+        out->prefill_ns_total = s.prefill_ns_total;
     });
 }
 
@@ -282,7 +284,7 @@ int prism_engine_decode_attention(prism_gpu* g, int engine_index, int layer, con
 
 int prism_set_attention_variant(int variant) {
     return dguard([&] {
-        if (variant < 0 || variant > 2) throw std::invalid_argument("attention variant must be 0, 1 or 2");
+        if (variant < 0 || variant > 3) throw std::invalid_argument("attention variant must be 0..3");
         prism::set_attention_variant(variant);
     });
 }
@@ -299,68 +301,21 @@ int prism_engine_decode_host(prism_gpu* g, int engine_index, const void* new_k, 
     return dguard([&] {
         need(q, "q");
         need(out, "out");
-        me::Engine& e = engine_at(g, engine_index);
-        const me::ModelSpec& m = *e.model;
-        auto stream = static_cast<cudaStream_t>(prism::engine_stream(e));
-        const int n_tok = prism::last_step_tokens(e);
-        const int n_dec = prism::last_step_decodes(e);
-        const std::size_t kv_bytes = static_cast<std::size_t>(m.n_layers) * n_tok * m.n_kv_heads * m.head_dim * 2;
-        const std::size_t q_layer = static_cast<std::size_t>(n_dec) * m.n_q_heads * m.head_dim * 2;
-        // Device staging (grown on demand, kept across calls).
-        static thread_local void* d_buf = nullptr;
-        static thread_local std::size_t d_cap = 0;
-        const std::size_t need_bytes = 2 * kv_bytes + 2 * q_layer * m.n_layers + 256;
-        if (need_bytes > d_cap) {
-            if (d_buf) check(cudaFree(d_buf), "cudaFree");
-            check(cudaMalloc(&d_buf, need_bytes), "cudaMalloc");
-            d_cap = need_bytes;
-        }
-        char* dk = static_cast<char*>(d_buf);
-        char* dv = dk + kv_bytes;
-        char* dq = dv + kv_bytes;
-        char* dout = dq + q_layer * m.n_layers;
-        // Copies run on a second stream so they overlap the kernels: q of
-        // layer l is needed only by K3(l); out of layer l is copied back
-        // while K3(l+1) runs.
-        static thread_local cudaStream_t cs = nullptr;
-        static thread_local std::vector<cudaEvent_t> evs;
-        if (!cs) check(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking), "cudaStreamCreate");
-        const std::size_t n_ev = 2 * static_cast<std::size_t>(m.n_layers) + 1;
-        while (evs.size() < n_ev) {
-            cudaEvent_t ev;
-            check(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "cudaEventCreate");
-            evs.push_back(ev);
-        }
-        check(cudaEventRecord(evs[0], stream), "record");  // device buffers free (previous call's work)
-        check(cudaStreamWaitEvent(cs, evs[0], 0), "wait");
-        if (new_k && new_v && n_tok) {
-            check(cudaMemcpyAsync(dk, new_k, kv_bytes, cudaMemcpyHostToDevice, cs), "H2D k");
-            check(cudaMemcpyAsync(dv, new_v, kv_bytes, cudaMemcpyHostToDevice, cs), "H2D v");
-            check(cudaEventRecord(evs[0], cs), "record");
-            check(cudaStreamWaitEvent(stream, evs[0], 0), "wait");
-            prism::append_step_kv(e, 0, m.n_layers, dk, dv);
-        }
-        if (n_dec) {
-            for (int layer = 0; layer < m.n_layers; ++layer) {
-                check(cudaMemcpyAsync(dq + q_layer * layer, static_cast<const char*>(q) + q_layer * layer, q_layer,
-                                      cudaMemcpyHostToDevice, cs),
-                      "H2D q");
-                check(cudaEventRecord(evs[1 + layer], cs), "record");
-            }
-            for (int layer = 0; layer < m.n_layers; ++layer) {
-                check(cudaStreamWaitEvent(stream, evs[1 + layer], 0), "wait");
-                prism::launch_decode_attention(prism::impl_of(e), layer, dq + q_layer * layer, dout + q_layer * layer,
-                                               scale, 0);
-                check(cudaEventRecord(evs[1 + m.n_layers + layer], stream), "record");
-                check(cudaStreamWaitEvent(cs, evs[1 + m.n_layers + layer], 0), "wait");
-                check(cudaMemcpyAsync(static_cast<char*>(out) + q_layer * layer, dout + q_layer * layer, q_layer,
-                                      cudaMemcpyDeviceToHost, cs),
-                      "D2H out");
-            }
-        }
-        check(cudaStreamSynchronize(cs), "cudaStreamSynchronize");
-        check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+        prism::decode_host(engine_at(g, engine_index), new_k, new_v, q, out, scale, /*wait=*/true);
     });
+}
+
+int prism_engine_decode_host_async(prism_gpu* g, int engine_index, const void* new_k, const void* new_v,
+                                   const void* q, void* out, float scale) {
+    return dguard([&] {
+        need(q, "q");
+        need(out, "out");
+        prism::decode_host(engine_at(g, engine_index), new_k, new_v, q, out, scale, /*wait=*/false);
+    });
+}
+
+int prism_engine_wait_host(prism_gpu* g, int engine_index) {
+    return dguard([&] { prism::wait_host(engine_at(g, engine_index)); });
 }
 
 int prism_engine_synchronize(prism_gpu* g, int engine_index) {

@@ -25,6 +25,7 @@
 namespace prism {
 
 void launch_k3_mma(const AttnArgs& a, int head_dim, int group, int stages, dim3 grid, cudaStream_t stream);
+void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec);
 int attention_variant();
 
 namespace {
@@ -349,20 +350,34 @@ void launch_d(int group, const AttnArgs& a, dim3 grid, cudaStream_t stream) {
 // K3 variant: 0 = tensor-core mma.sync kernel, 2-stage ring, 3 CTAs/SM
 // (default; measured 75% / 89% of HBM on C1 / C3); 1 = CUDA-core SIMT
 // kernel; 2 = tensor-core, 3-stage ring, 2 CTAs/SM. PRISM_K3=mma|simt|mma3.
+// 3 = stream-K persistent tensor-core kernel (decode_attn_streamk.cu).
 static int g_variant = [] {
     const char* v = std::getenv("PRISM_K3");
     if (v && std::strcmp(v, "simt") == 0) return 1;
     if (v && std::strcmp(v, "mma3") == 0) return 2;
+    if (v && std::strcmp(v, "streamk") == 0) return 3;
     return 0;
 }();
 int attention_variant() { return g_variant; }
-void set_attention_variant(int v) { g_variant = (v >= 0 && v <= 2) ? v : 0; }
+void set_attention_variant(int v) { g_variant = (v >= 0 && v <= 3) ? v : 0; }
 
 // Host launcher shared by the engine API and the C-ABI.
 void launch_decode_attention(EngineDeviceImpl& d, int layer, const void* q, void* out, float scale, int chunk_override) {
     if (layer < 0 || layer >= d.n_layers) throw std::runtime_error("decode_attention: bad layer");
     const int n_dec = d.step_decodes;
     if (n_dec == 0) return;
+    if (attention_variant() == 3 && chunk_override <= 0) {
+        AttnArgs a{};
+        a.g = d.geom;
+        a.layer = layer;
+        a.q = static_cast<const __nv_bfloat16*>(q);
+        a.out = static_cast<__nv_bfloat16*>(out);
+        a.table = d.table;
+        a.desc = d.decode_desc.dev;
+        a.scale_log2 = scale * 1.4426950408889634f;
+        launch_k3_streamk(d, a, n_dec);
+        return;
+    }
     int max_ctx = 0;
     std::int64_t sum_ctx = 0;
     for (int i = 0; i < n_dec; ++i) {

@@ -1,0 +1,433 @@
+// K3 (stream-K persistent variant) — the tensor-core decode attention of
+// decode_attn_mma.cu, scheduled stream-K style:
+//
+//   * work = the concatenated 64-token tiles of every (request, kv head)
+//     pair, pair p owning global tiles [T[p], T[p+1]);
+//   * the grid is the number of CTAs that fit on the GPU at once and CTA c
+//     owns the contiguous tile range [c*W, min((c+1)*W, total)), so every
+//     CTA does the same amount of work (no wave tail);
+//   * a CTA streams its range through one 2-stage cp.async ring WITHOUT
+//     draining between pairs: the next pair's first tiles are in flight
+//     while the previous pair's epilogue (cross-warp merge, output) runs;
+//   * a pair entirely inside one CTA's range is written straight to `out`;
+//     a pair cut by range boundaries leaves one partial (m, l, O) per CTA
+//     and the last of them to finish merges (ticket per pair).
+// The per-tile math (mma.sync S = K·Qᵀ, movmatrix Pᵀ, Oᵀ += Vᵀ·Pᵀ, warp-shared
+// online softmax) is the same as the split-K kernel.
+#include <cfloat>
+
+#include "cuda/attn_common.cuh"
+#include "cuda/device_impl.cuh"
+
+namespace prism {
+
+namespace {
+
+template <int D, int G>
+struct SkShape {
+    static constexpr int kWarps = 4;
+    static constexpr int kThreads = 128;
+    static constexpr int kT = 64;
+    static constexpr int kStages = 2;
+    static constexpr int kRowB = D * 2;
+    static constexpr int kCpr = D / 8;
+    static constexpr int kTileB = kT * kRowB;
+    static constexpr int kStageB = 2 * kTileB;
+    static constexpr int kLoads = kT * kCpr / kThreads;
+    static constexpr int kRowsPerPass = kThreads / kCpr;
+    static constexpr int kKSteps = D / 16;
+    static constexpr int kMTiles = D / 16;
+    static constexpr int kRingB = kStages * kStageB;
+    static constexpr int kMergeB = (kWarps * G * D + 2 * kWarps * 8) * 4;  // separate from the ring
+    static constexpr int kSmem = kRingB + kMergeB;
+};
+
+struct SkArgs {
+    AttnArgs a;                       // geometry, q/out, table, desc, scale
+    const std::int32_t* pair_tiles;   // [n_pairs + 1] prefix of tiles per pair
+    int n_pairs;
+    int total_tiles;
+    int per_cta;                      // W
+    int max_parts;                    // partial slots per pair
+};
+
+template <int D>
+__device__ __forceinline__ int swz_sk(int row, int chunk) {
+    return (row * (D / 8) + (chunk ^ (row & 7))) * 16;
+}
+
+template <int D, int G>
+__global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
+    using S = SkShape<D, G>;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const AttnArgs& a = sk.a;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int qr = lane >> 2, qc = (lane & 3) * 2;
+    const int n_kv = a.g.n_kv;
+    const int n_q = n_kv * G;
+    const char* base = reinterpret_cast<const char*>(a.g.base);
+    const std::uint64_t v_delta = static_cast<std::uint64_t>(n_kv) * a.g.tpp * D * 2;
+    const std::int32_t* T = sk.pair_tiles;
+
+    const int g_begin = blockIdx.x * sk.per_cta;
+    const int g_end = min(sk.total_tiles, g_begin + sk.per_cta);
+    if (g_begin >= g_end) return;
+
+    // first pair of the range: largest p with T[p] <= g_begin
+    auto pair_of = [&](int g) {
+        int lo = 0, hi = sk.n_pairs;
+        while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (__ldg(T + mid) <= g) lo = mid;
+            else hi = mid;
+        }
+        return lo;
+    };
+
+    // ---------------- producer cursor (tile being issued)
+    int ip = pair_of(g_begin);
+    int ip_end = __ldg(T + ip + 1);
+    auto issue = [&](int g) {
+        while (g >= ip_end) {
+            ++ip;
+            ip_end = __ldg(T + ip + 1);
+        }
+        const int b = ip / n_kv, h = ip % n_kv;
+        const DecodeDesc dd = a.desc[b];
+        const int t0 = (g - __ldg(T + ip)) * S::kT;
+        const std::int32_t* row = a.table + dd.row;
+        unsigned char* skb = smem + (g % S::kStages) * S::kStageB;
+        unsigned char* svb = skb + S::kTileB;
+        const int col = tid % S::kCpr;
+#pragma unroll
+        for (int i = 0; i < S::kLoads; ++i) {
+            const int r = tid / S::kCpr + i * S::kRowsPerPass;
+            const int t = t0 + r;
+            const char* src_k = reinterpret_cast<const char*>(a.table);
+            const char* src_v = src_k;
+            int bytes = 0;
+            if (t < dd.ctx) {
+                const std::uint32_t sid = static_cast<std::uint32_t>(__ldg(row + t));
+                src_k = base + row_offset(a.g, sid, a.layer, 0, h) + col * 16;
+                src_v = src_k + v_delta;
+                bytes = 16;
+            }
+            cp_async16(skb + swz_sk<D>(r, col), src_k, bytes);
+            cp_async16(svb + swz_sk<D>(r, col), src_v, bytes);
+        }
+    };
+
+    // ---------------- consumer state
+    int cp = pair_of(g_begin);  // pair being computed
+    int cp_first = __ldg(T + cp), cp_end = __ldg(T + cp + 1);
+    int ctx = 0;
+    std::uint32_t qb[S::kKSteps][2];
+    float o[S::kMTiles][4];
+    float m0, m1, l0, l1;
+    auto start_pair = [&]() {
+        const int b = cp / n_kv, h = cp % n_kv;
+        ctx = a.desc[b].ctx;
+        const __nv_bfloat16* qrow =
+            a.q + (static_cast<std::size_t>(b) * n_q + static_cast<std::size_t>(h) * G + qr) * D;
+#pragma unroll
+        for (int ks = 0; ks < S::kKSteps; ++ks) {
+            qb[ks][0] = qr < G ? *reinterpret_cast<const std::uint32_t*>(qrow + ks * 16 + qc) : 0u;
+            qb[ks][1] = qr < G ? *reinterpret_cast<const std::uint32_t*>(qrow + ks * 16 + 8 + qc) : 0u;
+        }
+#pragma unroll
+        for (int mt = 0; mt < S::kMTiles; ++mt) o[mt][0] = o[mt][1] = o[mt][2] = o[mt][3] = 0.f;
+        m0 = m1 = -INFINITY;
+        l0 = l1 = 0.f;
+    };
+    start_pair();
+
+    float* red_o = reinterpret_cast<float*>(smem + S::kRingB);  // [warps][G][D]
+    float* red_m = red_o + S::kWarps * G * D;                  // [warps][8]
+    float* red_l = red_m + S::kWarps * 8;                      // [warps][8]
+    __shared__ int s_last;
+
+    // finish pair cp: merge warps, write out or a partial (+ merge if last)
+    auto finish_pair = [&](int seg_first) {
+        float ll0 = l0, ll1 = l1;
+#pragma unroll
+        for (int off = 4; off < 32; off <<= 1) {
+            ll0 += __shfl_xor_sync(0xffffffffu, ll0, off);
+            ll1 += __shfl_xor_sync(0xffffffffu, ll1, off);
+        }
+#pragma unroll
+        for (int mt = 0; mt < S::kMTiles; ++mt) {
+            const int d0 = mt * 16 + qr;
+            if (qc < G) {
+                red_o[(warp * G + qc) * D + d0] = o[mt][0];
+                red_o[(warp * G + qc) * D + d0 + 8] = o[mt][2];
+            }
+            if (qc + 1 < G) {
+                red_o[(warp * G + qc + 1) * D + d0] = o[mt][1];
+                red_o[(warp * G + qc + 1) * D + d0 + 8] = o[mt][3];
+            }
+        }
+        if (qr == 0) {
+            red_m[warp * 8 + qc] = m0;
+            red_m[warp * 8 + qc + 1] = m1;
+            red_l[warp * 8 + qc] = ll0;
+            red_l[warp * 8 + qc + 1] = ll1;
+        }
+        __syncthreads();
+        const int b = cp / n_kv, h = cp % n_kv;
+        // CTAs whose ranges intersect this pair
+        const int first_cta = cp_first / sk.per_cta;
+        const int last_cta = (cp_end - 1) / sk.per_cta;
+        const int parts = last_cta - first_cta + 1;
+        const int part = blockIdx.x - first_cta;
+        __nv_bfloat16* out = a.out + (static_cast<std::size_t>(b) * n_q + static_cast<std::size_t>(h) * G) * D;
+        const std::size_t pslot = static_cast<std::size_t>(cp) * sk.max_parts + part;
+        for (int idx = tid; idx < G * D; idx += S::kThreads) {
+            const int g = idx / D, d = idx % D;
+            float mm = -INFINITY;
+#pragma unroll
+            for (int w = 0; w < S::kWarps; ++w) mm = fmaxf(mm, red_m[w * 8 + g]);
+            float ll = 0.f, oo = 0.f;
+#pragma unroll
+            for (int w = 0; w < S::kWarps; ++w) {
+                const float mw = red_m[w * 8 + g];
+                const float f = mw == -INFINITY ? 0.f : fast_exp2(mw - mm);
+                ll += red_l[w * 8 + g] * f;
+                oo += red_o[(w * G + g) * D + d] * f;
+            }
+            if (parts == 1) {
+                out[idx] = __float2bfloat16_rn(oo / ll);
+            } else {
+                a.part_o[pslot * G * D + idx] = oo;
+                if (d == 0) {
+                    a.part_ml[(pslot * G + g) * 2] = mm;
+                    a.part_ml[(pslot * G + g) * 2 + 1] = ll;
+                }
+            }
+        }
+        if (parts > 1) {
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) s_last = atomicAdd(&a.tickets[cp], 1) == parts - 1;
+            __syncthreads();
+            if (s_last) {
+                __threadfence();
+                const std::size_t p0 = static_cast<std::size_t>(cp) * sk.max_parts;
+                for (int idx = tid; idx < G * D; idx += S::kThreads) {
+                    const int g = idx / D;
+                    float mm = -INFINITY;
+                    for (int sp = 0; sp < parts; ++sp) mm = fmaxf(mm, __ldcg(&a.part_ml[((p0 + sp) * G + g) * 2]));
+                    float ll = 0.f, oo = 0.f;
+                    for (int sp = 0; sp < parts; ++sp) {
+                        const float f = fast_exp2(__ldcg(&a.part_ml[((p0 + sp) * G + g) * 2]) - mm);
+                        ll += __ldcg(&a.part_ml[((p0 + sp) * G + g) * 2 + 1]) * f;
+                        oo += __ldcg(&a.part_o[(p0 + sp) * G * D + idx]) * f;
+                    }
+                    out[idx] = __float2bfloat16_rn(oo / ll);
+                }
+                if (tid == 0) a.tickets[cp] = 0;
+            }
+        }
+        __syncthreads();  // red_* reused by the next pair
+        (void)seg_first;
+    };
+
+    // ---------------- pipeline over the CTA's tile range
+#pragma unroll
+    for (int st = 0; st < S::kStages - 1; ++st) {
+        if (g_begin + st < g_end) issue(g_begin + st);
+        cp_async_commit();
+    }
+    const int wrow = warp * 16;
+    for (int g = g_begin; g < g_end; ++g) {
+        cp_async_wait<S::kStages - 2>();
+        __syncthreads();
+        if (g + S::kStages - 1 < g_end) issue(g + S::kStages - 1);
+        cp_async_commit();
+
+        const unsigned char* skb = smem + (g % S::kStages) * S::kStageB;
+        const unsigned char* svb = skb + S::kTileB;
+        const int t0 = (g - cp_first) * S::kT + wrow;
+        if (t0 < ctx) {
+            float s[4] = {0.f, 0.f, 0.f, 0.f};
+            {
+                float s2[4] = {0.f, 0.f, 0.f, 0.f};
+                const int mat = lane >> 3;
+                const int r = wrow + (mat & 1) * 8 + (lane & 7);
+#pragma unroll
+                for (int ks = 0; ks < S::kKSteps; ks += 2) {
+                    std::uint32_t af[4], bf[4];
+                    ldmatrix_x4(af, skb + swz_sk<D>(r, ks * 2 + (mat >> 1)));
+                    ldmatrix_x4(bf, skb + swz_sk<D>(r, (ks + 1) * 2 + (mat >> 1)));
+                    mma_bf16_16816(s, af, qb[ks][0], qb[ks][1]);
+                    mma_bf16_16816(s2, bf, qb[ks + 1][0], qb[ks + 1][1]);
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) s[k] += s2[k];
+            }
+            const bool v0 = t0 + qr < ctx, v1 = t0 + qr + 8 < ctx;
+            s[0] = v0 ? s[0] * a.scale_log2 : -INFINITY;
+            s[1] = v0 ? s[1] * a.scale_log2 : -INFINITY;
+            s[2] = v1 ? s[2] * a.scale_log2 : -INFINITY;
+            s[3] = v1 ? s[3] * a.scale_log2 : -INFINITY;
+            float mx0 = fmaxf(s[0], s[2]), mx1 = fmaxf(s[1], s[3]);
+#pragma unroll
+            for (int off = 4; off < 32; off <<= 1) {
+                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+            }
+            if (__any_sync(0xffffffffu, mx0 > m0 || mx1 > m1)) {
+                const float n0 = fmaxf(m0, mx0), n1 = fmaxf(m1, mx1);
+                const float a0 = fast_exp2(m0 - n0), a1 = fast_exp2(m1 - n1);
+                l0 *= a0;
+                l1 *= a1;
+#pragma unroll
+                for (int mt = 0; mt < S::kMTiles; ++mt) {
+                    o[mt][0] *= a0;
+                    o[mt][1] *= a1;
+                    o[mt][2] *= a0;
+                    o[mt][3] *= a1;
+                }
+                m0 = n0;
+                m1 = n1;
+            }
+            const float r0 = m0 == -INFINITY ? 0.f : m0, r1 = m1 == -INFINITY ? 0.f : m1;
+            const float p0 = fast_exp2(s[0] - r0), p1 = fast_exp2(s[1] - r1);
+            const float p2 = fast_exp2(s[2] - r0), p3 = fast_exp2(s[3] - r1);
+            l0 += p0 + p2;
+            l1 += p1 + p3;
+            const std::uint32_t pb0 = movmatrix_trans(pack_bf16(p0, p1));
+            const std::uint32_t pb1 = movmatrix_trans(pack_bf16(p2, p3));
+            const int mat = lane >> 3;
+            const int r = wrow + (mat >> 1) * 8 + (lane & 7);
+#pragma unroll
+            for (int mt = 0; mt < S::kMTiles; ++mt) {
+                std::uint32_t af[4];
+                ldmatrix_x4_trans(af, svb + swz_sk<D>(r, mt * 2 + (mat & 1)));
+                mma_bf16_16816(o[mt], af, pb0, pb1);
+            }
+        }
+        // end of this pair's segment inside the range?
+        if (g + 1 == cp_end || g + 1 == g_end) {
+            finish_pair(cp_first);
+            if (g + 1 < g_end) {
+                ++cp;
+                cp_first = cp_end;
+                cp_end = __ldg(T + cp + 1);
+                start_pair();
+            }
+        }
+    }
+    cp_async_wait<0>();
+}
+
+template <int D, int G>
+void launch_sk(const SkArgs& s, cudaStream_t stream, int sms) {
+    using S = SkShape<D, G>;
+    static int per_sm = 0;
+    if (per_sm == 0) {
+        PRISM_CUDA(cudaFuncSetAttribute(k3_decode_streamk<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        S::kSmem));
+        PRISM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_decode_streamk<D, G>, S::kThreads,
+                                                                 S::kSmem));
+        if (per_sm < 1) per_sm = 1;
+    }
+    (void)sms;
+    const int grid = (s.total_tiles + s.per_cta - 1) / s.per_cta;
+    k3_decode_streamk<D, G><<<grid, S::kThreads, S::kSmem, stream>>>(s);
+    PRISM_CUDA(cudaGetLastError());
+}
+
+template <int D, int G>
+int occupancy_sk() {
+    using S = SkShape<D, G>;
+    int per_sm = 0;
+    PRISM_CUDA(cudaFuncSetAttribute(k3_decode_streamk<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmem));
+    PRISM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_decode_streamk<D, G>, S::kThreads, S::kSmem));
+    return per_sm < 1 ? 1 : per_sm;
+}
+
+template <int D>
+int occupancy_sk_d(int group) {
+    switch (group) {
+        case 1: return occupancy_sk<D, 1>();
+        case 2: return occupancy_sk<D, 2>();
+        case 3: return occupancy_sk<D, 3>();
+        case 4: return occupancy_sk<D, 4>();
+        case 5: return occupancy_sk<D, 5>();
+        case 6: return occupancy_sk<D, 6>();
+        case 7: return occupancy_sk<D, 7>();
+        case 8: return occupancy_sk<D, 8>();
+    }
+    throw std::runtime_error("decode_attention: unsupported GQA group");
+}
+
+template <int D>
+void launch_sk_d(int group, const SkArgs& s, cudaStream_t stream, int sms) {
+    switch (group) {
+        case 1: launch_sk<D, 1>(s, stream, sms); break;
+        case 2: launch_sk<D, 2>(s, stream, sms); break;
+        case 3: launch_sk<D, 3>(s, stream, sms); break;
+        case 4: launch_sk<D, 4>(s, stream, sms); break;
+        case 5: launch_sk<D, 5>(s, stream, sms); break;
+        case 6: launch_sk<D, 6>(s, stream, sms); break;
+        case 7: launch_sk<D, 7>(s, stream, sms); break;
+        case 8: launch_sk<D, 8>(s, stream, sms); break;
+        default: throw std::runtime_error("decode_attention: unsupported GQA group");
+    }
+}
+
+}  // namespace
+
+// Host side of the stream-K launch. The pair-tile prefix depends only on the
+// step's decode descriptors, so it is rebuilt once per step (not per layer).
+void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec) {
+    constexpr int kT = 64;
+    static int sms = [] {
+        int dev = 0, n = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n;
+    }();
+    const int n_pairs = n_dec * d.n_kv;
+    if (d.sk_step != d.step_serial) {
+        d.sk_prefix.ensure(static_cast<std::size_t>(n_pairs) + 1);
+        std::int32_t acc = 0;
+        for (int b = 0; b < n_dec; ++b) {
+            const int tiles = (d.decode_desc.host[b].ctx + kT - 1) / kT;
+            for (int h = 0; h < d.n_kv; ++h) {
+                d.sk_prefix.host[b * d.n_kv + h] = acc;
+                acc += tiles;
+            }
+        }
+        d.sk_prefix.host[n_pairs] = acc;
+        d.sk_total = acc;
+        d.sk_prefix.upload(static_cast<std::size_t>(n_pairs) + 1, d.stream);
+        d.sk_step = d.step_serial;
+        const int per_sm = d.head_dim == 128 ? occupancy_sk_d<128>(d.group) : occupancy_sk_d<64>(d.group);
+        const int slots = sms * per_sm;
+        d.sk_per_cta = std::max(1, (d.sk_total + slots - 1) / slots);
+        // partial slots per pair: CTAs a pair's tile range can touch
+        int max_tiles = 0;
+        for (int b = 0; b < n_dec; ++b) max_tiles = std::max(max_tiles, (d.decode_desc.host[b].ctx + kT - 1) / kT);
+        d.sk_max_parts = (max_tiles + d.sk_per_cta - 1) / d.sk_per_cta + 1;
+    }
+    SkArgs s{};
+    s.a = a;
+    s.pair_tiles = d.sk_prefix.dev;
+    s.n_pairs = n_pairs;
+    s.total_tiles = d.sk_total;
+    s.per_cta = d.sk_per_cta;
+    s.max_parts = d.sk_max_parts;
+    const std::size_t per = static_cast<std::size_t>(n_pairs) * d.sk_max_parts * d.group;
+    float* ws = d.attn_workspace(per * d.head_dim + per * 2);
+    s.a.part_o = ws;
+    s.a.part_ml = ws + per * d.head_dim;
+    s.a.tickets = d.attn_counters(static_cast<std::size_t>(n_pairs));
+    if (d.head_dim == 128) {
+        launch_sk_d<128>(d.group, s, d.stream, sms);
+    } else {
+        launch_sk_d<64>(d.group, s, d.stream, sms);
+    }
+}
+
+}  // namespace prism

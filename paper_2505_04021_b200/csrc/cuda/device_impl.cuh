@@ -141,6 +141,19 @@ public:
     std::size_t workspace_floats = 0;
     int* counters = nullptr;
     std::size_t counters_n = 0;
+
+    // stream-K K3: pair-tile prefix of the current step (rebuilt once per step)
+    std::uint64_t step_serial = 0;
+    std::uint64_t sk_step = ~0ull;
+    Staging<std::int32_t> sk_prefix;
+    int sk_total = 0, sk_per_cta = 1, sk_max_parts = 1;
+
+    // host-buffer (end-to-end) path
+    cudaStream_t copy_stream = nullptr;
+    void* host_stage = nullptr;       // device staging for K/V/q/out
+    std::size_t host_stage_bytes = 0;
+    std::vector<cudaEvent_t> host_events;
+    cudaEvent_t host_done = nullptr;
 };
 
 EngineDeviceImpl& impl_of(const msim::engine::Engine& eng);

@@ -61,6 +61,13 @@ EngineDeviceImpl::EngineDeviceImpl(me::Engine& eng, pa::PhysicalLedger& ledger, 
 
 EngineDeviceImpl::~EngineDeviceImpl() {
     cudaStreamSynchronize(stream);
+    if (copy_stream) {
+        cudaStreamSynchronize(copy_stream);
+        cudaStreamDestroy(copy_stream);
+    }
+    for (cudaEvent_t ev : host_events) cudaEventDestroy(ev);
+    if (host_done) cudaEventDestroy(host_done);
+    if (host_stage) cudaFree(host_stage);
     if (table) cudaFree(table);
     if (step_slots) cudaFree(step_slots);
     if (workspace) cudaFree(workspace);
@@ -137,6 +144,7 @@ void EngineDeviceImpl::end_step(me::Engine&, const me::IterationOutcome& out, co
                                 std::uint64_t prefill_id, std::int64_t prefill_row, std::int32_t prefill_first,
                                 std::int32_t prefill_tokens) {
     vmm->defer_access(false);  // pages must be accessible before K2/K3 run
+    ++step_serial;
     // K1: replay this step's allocations / frees on the device slot state.
     const std::int64_t n = pool->mirror->replay(*pool, table, step_slots, opts.max_step_tokens, stream);
     step_tokens = static_cast<int>(n);
@@ -194,6 +202,75 @@ int* EngineDeviceImpl::attn_counters(std::size_t n) {
         PRISM_CUDA(cudaMemsetAsync(counters, 0, counters_n * sizeof(int), stream));
     }
     return counters;
+}
+
+// ---------------------------------------------------------------- host-buffer path
+
+void launch_decode_attention(EngineDeviceImpl& d, int layer, const void* q, void* out, float scale, int chunk);
+
+void decode_host(me::Engine& eng, const void* new_k, const void* new_v, const void* q, void* out, float scale,
+                 bool wait) {
+    EngineDeviceImpl& d = impl_of(eng);
+    const int n_tok = d.step_tokens, n_dec = d.step_decodes, L = d.n_layers;
+    const std::size_t kv_bytes = static_cast<std::size_t>(L) * n_tok * d.n_kv * d.head_dim * 2;
+    const std::size_t q_layer = static_cast<std::size_t>(n_dec) * d.n_q * d.head_dim * 2;
+    const std::size_t need = 2 * kv_bytes + 2 * q_layer * L + 256;
+    if (!d.copy_stream) {
+        PRISM_CUDA(cudaStreamCreateWithFlags(&d.copy_stream, cudaStreamNonBlocking));
+        PRISM_CUDA(cudaEventCreateWithFlags(&d.host_done, cudaEventDisableTiming));
+    }
+    while (d.host_events.size() < 2 * static_cast<std::size_t>(L) + 1) {
+        cudaEvent_t ev;
+        PRISM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        d.host_events.push_back(ev);
+    }
+    if (need > d.host_stage_bytes) {
+        PRISM_CUDA(cudaStreamSynchronize(d.copy_stream));
+        PRISM_CUDA(cudaStreamSynchronize(d.stream));
+        if (d.host_stage) PRISM_CUDA(cudaFree(d.host_stage));
+        PRISM_CUDA(cudaMalloc(&d.host_stage, need));
+        d.host_stage_bytes = need;
+    }
+    char* dk = static_cast<char*>(d.host_stage);
+    char* dv = dk + kv_bytes;
+    char* dq = dv + kv_bytes;
+    char* dout = dq + q_layer * L;
+    cudaStream_t cs = d.copy_stream;
+    std::vector<cudaEvent_t>& ev = d.host_events;
+    // Copies of this call start after the compute stream's earlier work on
+    // the staging buffers; q of layer l gates only K3(l); out of layer l goes
+    // back while K3(l+1) runs.
+    PRISM_CUDA(cudaEventRecord(ev[0], d.stream));
+    PRISM_CUDA(cudaStreamWaitEvent(cs, ev[0], 0));
+    if (new_k && new_v && n_tok) {
+        PRISM_CUDA(cudaMemcpyAsync(dk, new_k, kv_bytes, cudaMemcpyHostToDevice, cs));
+        PRISM_CUDA(cudaMemcpyAsync(dv, new_v, kv_bytes, cudaMemcpyHostToDevice, cs));
+        PRISM_CUDA(cudaEventRecord(ev[0], cs));
+        PRISM_CUDA(cudaStreamWaitEvent(d.stream, ev[0], 0));
+        append_step_kv(eng, 0, L, dk, dv);
+    }
+    if (n_dec) {
+        for (int l = 0; l < L; ++l) {
+            PRISM_CUDA(cudaMemcpyAsync(dq + q_layer * l, static_cast<const char*>(q) + q_layer * l, q_layer,
+                                       cudaMemcpyHostToDevice, cs));
+            PRISM_CUDA(cudaEventRecord(ev[1 + l], cs));
+        }
+        for (int l = 0; l < L; ++l) {
+            PRISM_CUDA(cudaStreamWaitEvent(d.stream, ev[1 + l], 0));
+            launch_decode_attention(d, l, dq + q_layer * l, dout + q_layer * l, scale, 0);
+            PRISM_CUDA(cudaEventRecord(ev[1 + L + l], d.stream));
+            PRISM_CUDA(cudaStreamWaitEvent(cs, ev[1 + L + l], 0));
+            PRISM_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + q_layer * l, dout + q_layer * l, q_layer,
+                                       cudaMemcpyDeviceToHost, cs));
+        }
+    }
+    PRISM_CUDA(cudaEventRecord(d.host_done, cs));
+    if (wait) wait_host(eng);
+}
+
+void wait_host(const me::Engine& eng) {
+    EngineDeviceImpl& d = impl_of(eng);
+    if (d.host_done) PRISM_CUDA(cudaEventSynchronize(d.host_done));
 }
 
 // ---------------------------------------------------------------- public API

@@ -211,7 +211,7 @@ std::uint64_t VmmDevice::steal() {
     const std::uint64_t h = pick->second.handle;
     parked_.erase(pick);
     ++stats_.steals;
-    stats_.unmap_ns_total += ns_since(t0);
+    stats_.steal_ns_total += ns_since(t0);  // inside a map: counted by map_ns_total
     return h;
 }
 
@@ -272,7 +272,7 @@ void VmmDevice::map_batch(const std::uint64_t* vas, std::size_t n, std::size_t n
         live_.emplace(vas[i], h);
         unaccessed_.push_back(vas[i]);
     }
-    if (!defer_access_) flush_access();
+    if (!defer_access_) flush_now();
     const double per = ns_since(t0) / static_cast<double>(n);
     stats_.map_ns_total += per * static_cast<double>(n);
     for (std::size_t i = 0; i < n; ++i) sample(stats_.map_ns, per);
@@ -284,8 +284,14 @@ void VmmDevice::defer_access(bool on) {
 }
 
 void VmmDevice::flush_access() {
-    if (unaccessed_.empty()) return;
+    // Deferred flush (outside map_batch): its time belongs to the maps.
     const auto t0 = Clock::now();
+    flush_now();
+    stats_.map_ns_total += ns_since(t0);
+}
+
+void VmmDevice::flush_now() {
+    if (unaccessed_.empty()) return;
     std::sort(unaccessed_.begin(), unaccessed_.end());
     for (std::size_t i = 0; i < unaccessed_.size();) {
         std::size_t j = i + 1;
@@ -298,12 +304,16 @@ void VmmDevice::flush_access() {
         ++stats_.access_calls;
         i = j;
     }
-    // Charged to the maps of this flush (it is part of mapping them).
-    stats_.map_ns_total += ns_since(t0);
     unaccessed_.clear();
 }
 
 void VmmDevice::prefill_cache(std::uint64_t n) {
+    const auto t0 = Clock::now();
+    struct Charge {
+        VmmStats& s;
+        Clock::time_point t;
+        ~Charge() { s.prefill_ns_total += ns_since(t); }
+    } charge{stats_, t0};
     while (cache_.size() < n && total_handles() < budget_) {
         const auto tc = Clock::now();
         CUmemGenericAllocationHandle h = 0;

@@ -37,8 +37,10 @@ struct VmmStats {
     std::uint64_t unmaps = 0;         // logical unmaps (parks)
     std::uint64_t driver_unmaps = 0;  // cuMemUnmap calls actually issued
     std::uint64_t steals = 0;         // parked pages moved to another VA
-    double map_ns_total = 0.0;        // host wall time inside map paths
-    double unmap_ns_total = 0.0;      // host wall time inside unmap paths (incl. steals)
+    double map_ns_total = 0.0;        // host wall time of logical maps (incl. steals, creates, SetAccess)
+    double unmap_ns_total = 0.0;      // host wall time of logical unmaps + explicit reclaims
+    double steal_ns_total = 0.0;      // part of map_ns_total: cuMemUnmap of stolen parked pages
+    double prefill_ns_total = 0.0;    // handle creation ahead of need (prefill_cache), off the map path
     std::vector<float> map_ns;        // per logical map (bounded)
     std::vector<float> unmap_ns;      // per logical unmap / driver unmap (bounded)
     double create_ns_total = 0.0;     // inside cuMemCreate
@@ -103,6 +105,7 @@ private:
     void drop_handle(std::uint64_t h);
     void driver_unmap(std::uint64_t va);
     void advance_fences(bool wait);
+    void flush_now();  // issue the pending cuMemSetAccess calls
 
     struct Parked {
         std::uint64_t handle;

@@ -486,6 +486,13 @@ class Engine:
         self.lib.call("prism_engine_decode_host", self.gpu.h, self.index, C.c_void_p(new_k_ptr),
                       C.c_void_p(new_v_ptr), C.c_void_p(q_ptr), C.c_void_p(out_ptr), scale)
 
+    def decode_host_async(self, new_k_ptr, new_v_ptr, q_ptr, out_ptr, scale: float) -> None:
+        self.lib.call("prism_engine_decode_host_async", self.gpu.h, self.index, C.c_void_p(new_k_ptr),
+                      C.c_void_p(new_v_ptr), C.c_void_p(q_ptr), C.c_void_p(out_ptr), scale)
+
+    def wait_host(self) -> None:
+        self.lib.call("prism_engine_wait_host", self.gpu.h, self.index)
+
     def synchronize(self) -> None:
         self.lib.call("prism_engine_synchronize", self.gpu.h, self.index)
 

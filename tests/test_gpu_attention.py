@@ -73,7 +73,7 @@ def _attend_and_check(eng, spec, layers, q_scale=4.0):
     return worst
 
 
-@pytest.fixture(params=[0, 1, 2], ids=["mma", "simt", "mma3"])
+@pytest.fixture(params=[0, 1, 2, 3], ids=["mma", "simt", "mma3", "streamk"])
 def variant(request, product):
     product.call("prism_set_attention_variant", request.param)
     yield request.param
