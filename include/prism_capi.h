@@ -328,11 +328,16 @@ typedef struct {
     uint64_t access_calls;
     uint64_t steals; /* parked pages moved to another VA (cross-model memory movement) */
     double steal_ns_total; /* cuMemUnmap time of steals (included in map_ns_total) */
-    double prefill_ns_total; /* handle creation ahead of need, outside the map path */
+    double background_ns_total; /* worker-thread driver time (pre-maps, creates, moves); off the caller's path */
+    uint64_t premaps;           /* pages the worker mapped ahead of need */
+    uint64_t premapped_hits;    /* logical maps satisfied by a pre-mapped page */
+    uint64_t batched_unmaps;    /* cuMemUnmap calls covering a run of >1 pages */
 } prism_device_stats;
 int prism_device_stats_get(const prism_device* d, prism_device_stats* out);
 int prism_device_reset_stats(prism_device* d);
 int prism_device_reclaim(prism_device* d, int wait);
+/* Block until the device's background worker is idle (tests, benchmarks). */
+int prism_device_quiesce(prism_device* d);
 /* Record a fence on the device stream: pages unmapped before it become
  * reclaimable (cuMemUnmap'ed by prism_device_reclaim(d, 0)) once it passes. */
 int prism_device_fence(prism_device* d);

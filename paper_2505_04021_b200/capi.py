@@ -158,7 +158,7 @@ class DeviceStats(C.Structure):
                                 "unmap_ns_p99")] + [(n, c_uint64) for n in ("buffered", "cached", "pending")] + [
         (n, c_double) for n in ("create_ns_total", "map_call_ns_total", "access_ns_total")] + [
         ("access_calls", c_uint64), ("steals", c_uint64), ("steal_ns_total", c_double),
-        ("prefill_ns_total", c_double)]
+        ("background_ns_total", c_double)] + [(n, c_uint64) for n in ("premaps", "premapped_hits", "batched_unmaps")]
 
 
 class EngineDeviceOptions(C.Structure):
@@ -244,6 +244,7 @@ _DEVICE_DECLS = {
     "prism_device_stats_get": (c_int, [c_void_p, P(DeviceStats)]),
     "prism_device_reset_stats": (c_int, [c_void_p]),
     "prism_device_reclaim": (c_int, [c_void_p, c_int]),
+    "prism_device_quiesce": (c_int, [c_void_p]),
     "prism_device_fence": (c_int, [c_void_p]),
     "prism_device_synchronize": (c_int, [c_void_p]),
     "prism_device_stream": (c_void_p, [c_void_p]),

@@ -102,7 +102,7 @@ int prism_device_stats_get(const prism_device* d, prism_device_stats* out) {
     return dguard([&] {
         need(d, "device");
         need(out, "out");
-        const prism::VmmStats& s = d->dev->stats();
+        const prism::VmmStats s = d->dev->stats();
         out->maps = s.maps;
         out->revived = s.revived;
         out->creates = s.creates;
@@ -123,7 +123,10 @@ int prism_device_stats_get(const prism_device* d, prism_device_stats* out) {
         out->access_calls = s.access_calls;
         out->steals = s.steals;
         out->steal_ns_total = s.steal_ns_total;
-        out->prefill_ns_total = s.prefill_ns_total;
+        out->background_ns_total = s.background_ns_total;
+        out->premaps = s.premaps;
+        out->premapped_hits = s.premapped_hits;
+        out->batched_unmaps = s.batched_unmaps;
     });
 }
 
@@ -138,6 +141,13 @@ int prism_device_reclaim(prism_device* d, int wait) {
     return dguard([&] {
         need(d, "device");
         d->dev->reclaim(wait != 0);
+    });
+}
+
+int prism_device_quiesce(prism_device* d) {
+    return dguard([&] {
+        need(d, "device");
+        d->dev->quiesce();
     });
 }
 

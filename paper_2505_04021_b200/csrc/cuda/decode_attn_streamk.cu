@@ -84,31 +84,41 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
         return lo;
     };
 
-    // ---------------- producer cursor (tile being issued)
-    int ip = pair_of(g_begin);
-    int ip_end = __ldg(T + ip + 1);
-    auto issue = [&](int g) {
-        while (g >= ip_end) {
-            ++ip;
-            ip_end = __ldg(T + ip + 1);
+    // ---------------- prefetch cursor: slot ids (and kv head) of the next
+    // tile to issue are loaded one tile ahead of its cp.async, crossing pair
+    // boundaries as the CTA's range does.
+    constexpr std::uint32_t kNoSlot = 0xFFFFFFFFu;
+    int pf = pair_of(g_begin);
+    int pf_first = __ldg(T + pf), pf_end = __ldg(T + pf + 1);
+    DecodeDesc pf_desc = a.desc[pf / n_kv];
+    auto load_sids = [&](int g, std::uint32_t (&dst)[S::kLoads], int& dst_h) {
+        while (g >= pf_end) {
+            ++pf;
+            pf_first = pf_end;
+            pf_end = __ldg(T + pf + 1);
+            pf_desc = a.desc[pf / n_kv];
         }
-        const int b = ip / n_kv, h = ip % n_kv;
-        const DecodeDesc dd = a.desc[b];
-        const int t0 = (g - __ldg(T + ip)) * S::kT;
-        const std::int32_t* row = a.table + dd.row;
+        dst_h = pf % n_kv;
+        const int t0 = (g - pf_first) * S::kT;
+        const std::int32_t* row = a.table + pf_desc.row;
+#pragma unroll
+        for (int i = 0; i < S::kLoads; ++i) {
+            const int t = t0 + tid / S::kCpr + i * S::kRowsPerPass;
+            dst[i] = t < pf_desc.ctx ? static_cast<std::uint32_t>(__ldg(row + t)) : kNoSlot;
+        }
+    };
+    auto issue = [&](int g, const std::uint32_t (&sids)[S::kLoads], int h) {
         unsigned char* skb = smem + (g % S::kStages) * S::kStageB;
         unsigned char* svb = skb + S::kTileB;
         const int col = tid % S::kCpr;
 #pragma unroll
         for (int i = 0; i < S::kLoads; ++i) {
             const int r = tid / S::kCpr + i * S::kRowsPerPass;
-            const int t = t0 + r;
             const char* src_k = reinterpret_cast<const char*>(a.table);
             const char* src_v = src_k;
             int bytes = 0;
-            if (t < dd.ctx) {
-                const std::uint32_t sid = static_cast<std::uint32_t>(__ldg(row + t));
-                src_k = base + row_offset(a.g, sid, a.layer, 0, h) + col * 16;
+            if (sids[i] != kNoSlot) {
+                src_k = base + row_offset(a.g, sids[i], a.layer, 0, h) + col * 16;
                 src_v = src_k + v_delta;
                 bytes = 16;
             }
@@ -232,16 +242,25 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
     };
 
     // ---------------- pipeline over the CTA's tile range
+    std::uint32_t sids[S::kLoads];
+    int sid_h = 0;
 #pragma unroll
     for (int st = 0; st < S::kStages - 1; ++st) {
-        if (g_begin + st < g_end) issue(g_begin + st);
+        if (g_begin + st < g_end) {
+            load_sids(g_begin + st, sids, sid_h);
+            issue(g_begin + st, sids, sid_h);
+        }
         cp_async_commit();
     }
+    if (g_begin + S::kStages - 1 < g_end) load_sids(g_begin + S::kStages - 1, sids, sid_h);
     const int wrow = warp * 16;
     for (int g = g_begin; g < g_end; ++g) {
         cp_async_wait<S::kStages - 2>();
         __syncthreads();
-        if (g + S::kStages - 1 < g_end) issue(g + S::kStages - 1);
+        if (g + S::kStages - 1 < g_end) {
+            issue(g + S::kStages - 1, sids, sid_h);
+            if (g + S::kStages < g_end) load_sids(g + S::kStages, sids, sid_h);
+        }
         cp_async_commit();
 
         const unsigned char* skb = smem + (g % S::kStages) * S::kStageB;
@@ -340,10 +359,15 @@ void launch_sk(const SkArgs& s, cudaStream_t stream, int sms) {
 template <int D, int G>
 int occupancy_sk() {
     using S = SkShape<D, G>;
-    int per_sm = 0;
-    PRISM_CUDA(cudaFuncSetAttribute(k3_decode_streamk<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmem));
-    PRISM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_decode_streamk<D, G>, S::kThreads, S::kSmem));
-    return per_sm < 1 ? 1 : per_sm;
+    static int per_sm = 0;  // resident CTAs per SM (queried once)
+    if (per_sm == 0) {
+        PRISM_CUDA(cudaFuncSetAttribute(k3_decode_streamk<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        S::kSmem));
+        PRISM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_decode_streamk<D, G>, S::kThreads,
+                                                                 S::kSmem));
+        if (per_sm < 1) per_sm = 1;
+    }
+    return per_sm;
 }
 
 template <int D>

@@ -189,6 +189,11 @@ using detail::Access;
 using detail::kNone;
 using detail::PoolState;
 
+// Look-ahead window handed to VmmDevice::premap when a pool grows: twice the
+// pages the growing call mapped, within [8, 64] pages (16-128 MiB).
+constexpr std::uint64_t kPremapMin = 8;
+constexpr std::uint64_t kPremapMax = 64;
+
 inline bool is_candidate(const PoolState& s, std::uint32_t page) {
     return s.occ[page] > 0 && s.occ[page] < s.tpp;
 }
@@ -375,6 +380,16 @@ AllocResult detail::alloc_kv_into(KvPool& pool, PhysicalLedger& ledger, std::uin
             p = s.unmapped.find_next(static_cast<std::uint64_t>(p) + 1);
         }
         s.dev->map_batch(vas.data(), vas.size(), res.buffer_hits);
+        // The pool is growing: its next maps will be the following lowest
+        // unmapped pages. Hand them to the device's worker thread to map
+        // (and make accessible) ahead of time, so those maps become revives.
+        const std::uint64_t ahead = std::min<std::uint64_t>(kPremapMax, std::max<std::uint64_t>(kPremapMin, 2 * new_pages));
+        vas.clear();
+        for (std::uint64_t k = 0; k < ahead && p != kNone; ++k) {
+            vas.push_back(s.va + static_cast<std::uint64_t>(p) * s.dev->page_bytes());
+            p = s.unmapped.find_next(static_cast<std::uint64_t>(p) + 1);
+        }
+        s.dev->premap(s.va, vas.data(), vas.size());
     }
     while (remaining > 0) {
         bool needs_map = false;

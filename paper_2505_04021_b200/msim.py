@@ -536,6 +536,10 @@ class Device:
     def reset_stats(self) -> None:
         self.lib.call("prism_device_reset_stats", self.h)
 
+    def quiesce(self) -> None:
+        """Wait until the background VMM worker has no queued work."""
+        self.lib.call("prism_device_quiesce", self.h)
+
     def reclaim(self, wait: bool) -> None:
         self.lib.call("prism_device_reclaim", self.h, 1 if wait else 0)
 

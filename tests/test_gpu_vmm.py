@@ -89,3 +89,78 @@ def test_weights_shrink_the_physical_budget(product, device):
     # 32 more weight pages: parked pages beyond the new budget are released
     assert gpu.ledger.reserve_weight_pages("big", 32)
     gpu.ledger.release_weight_pages("big")
+
+
+def test_worker_premaps_the_next_pages(product, device):
+    """A growing pool hands its next lowest unmapped pages to the device's
+    worker thread, which maps them ahead of need: the pool's next maps are
+    revives of those pre-mapped pages (no driver call on the caller)."""
+    gpu = msim.GpuState(0, 200, lib=product)
+    gpu.ledger.attach_device(device)
+    pool = msim.alloc_kvcache(gpu.ledger, "pm", 131072, 400)  # 16 tokens per page
+    device.reset_stats()
+    first = msim.alloc_kv(pool, gpu.ledger, 16)  # maps page 0, hints pages 1..8
+    device.quiesce()
+    st = device.stats()
+    assert st["maps"] == 1 and st["premaps"] == 8, st
+    grow = msim.alloc_kv(pool, gpu.ledger, 8 * 16)  # pages 1..8
+    st = device.stats()
+    assert st["premapped_hits"] == 8 and st["revived"] == 8, st
+    assert sorted({h.page for h in grow.handles}) == list(range(1, 9))
+    msim.free_kv(pool, gpu.ledger, first.handles + grow.handles)
+    device.quiesce()
+    device.reclaim(True)
+    assert device.stats()["pending"] == 0
+    msim.free_kvcache(gpu.ledger, pool)
+
+
+def test_worker_stays_within_the_physical_budget(product, device):
+    cap = 12
+    gpu = msim.GpuState(0, cap, lib=product)
+    gpu.ledger.attach_device(device)
+    device.reclaim(True)
+    pool = msim.alloc_kvcache(gpu.ledger, "tight", 131072, 400)
+    device.reset_stats()
+    held = msim.alloc_kv(pool, gpu.ledger, 10 * 16).handles  # 10 pages; hint asks for 20 more
+    device.quiesce()
+    st = device.stats()
+    assert st["premaps"] <= cap - 10, st
+    # the rest of the ledger still maps (revives / steals of pre-mapped pages)
+    more = msim.alloc_kv(pool, gpu.ledger, 2 * 16)
+    assert more.shortfall_pages == 0
+    assert msim.alloc_kv(pool, gpu.ledger, 1).shortfall_pages == 1
+    msim.free_kv(pool, gpu.ledger, held + more.handles)
+    device.quiesce()
+    device.reclaim(True)
+    msim.free_kvcache(gpu.ledger, pool)
+
+
+def test_concurrent_pools_with_worker_keep_data(product, device):
+    """Two models alternate bursts on a tight ledger while the worker
+    pre-maps and moves pages between them; attention stays exact."""
+    gpu = msim.GpuState(0, 20, lib=product)
+    gpu.ledger.attach_device(device)
+    engines = []
+    for mid in ("x", "y"):
+        spec = S.shape_spec("llama3.1-8b", mid, chunk=64, weight_scale=0.0)
+        act = gpu.activate(spec)
+        gpu.finish_activation(act.engine_index)
+        e = gpu.engine(act.engine_index)
+        e.attach_device()
+        engines.append((e, spec))
+    rid = 0
+    for rnd in range(4):
+        for e, spec in engines:
+            rid += 1
+            e.push(rid, 40 + 9 * rnd, 30)
+        steps = 0
+        while any(sum(e.counts()) for e, _ in engines) and steps < 600:
+            for e, spec in engines:
+                if sum(e.counts()):
+                    e.step()
+                    e.append_kv_synthetic(0, spec.n_layers, SEED)
+                    if steps % 7 == 0:
+                        _attn_ok(e, spec)
+            steps += 1
+        assert gpu.ledger.mapped_pages() == 0
+    device.quiesce()
