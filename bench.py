@@ -191,6 +191,10 @@ def setup_gpu(rank: int, mids, max_steps: int):
             m.eng.step()
             m.eng.append_kv_synthetic(0, L, SEED)
     dev.synchronize()
+    # The prefill burst leaves the VMM worker a backlog of look-ahead maps;
+    # let it drain (as it would between a serving system's admission burst
+    # and steady decode) so timing starts from steady state.
+    dev.quiesce()
     return dev, gpu, models
 
 
@@ -299,7 +303,7 @@ def gpu_arm(args, rank, world):
     value = tokens / (ms_max / 1e3)
 
     # ---- e2e through the C-ABI with host buffers
-    e2e = e2e_arm(models, steps, scale, dev, world)
+    e2e = e2e_arm(models, steps, warm, scale, dev, world)
 
     peak, peak_kind = measured_peaks()
     # per-launch algorithmic bytes (contexts grow by 1 per step; use the mean)
@@ -341,7 +345,7 @@ def gpu_arm(args, rank, world):
     return res
 
 
-def e2e_arm(models, steps, scale, dev, world):
+def e2e_arm(models, steps, warm, scale, dev, world):
     import torch
 
     n_tok = B_PER_MODEL
@@ -357,22 +361,29 @@ def e2e_arm(models, steps, scale, dev, world):
 
     # per model: new K/V rows, q for every layer (in), attention out (back)
     bufs = [(pinned(kv_elems), pinned(kv_elems), pinned(q_elems), pinned(q_elems, False)) for _ in models]
-    for m, (hk, hv, hq, ho) in zip(models, bufs):  # warm the staging path
-        m.eng.step()
-        m.eng.decode_host(hk.data_ptr(), hv.data_ptr(), hq.data_ptr(), ho.data_ptr(), scale)
+    for _ in range(warm):  # warm the staging path
+        for m, (hk, hv, hq, ho) in zip(models, bufs):
+            m.eng.step()
+            m.eng.decode_host(hk.data_ptr(), hv.data_ptr(), hq.data_ptr(), ho.data_ptr(), scale)
     torch.cuda.synchronize()
+    dev.reset_stats()
+    step_ms = []
     t0 = time.perf_counter()
     for _ in range(steps):
         # Serving-loop order: each model's step is enqueued (its copies run on
         # its own copy stream, overlapping the other model's kernels), and a
         # model's outputs are awaited before its next step.
+        ts = time.perf_counter()
         for m, (hk, hv, hq, ho) in zip(models, bufs):
             m.eng.wait_host()
             m.eng.step()
             m.eng.decode_host_async(hk.data_ptr(), hv.data_ptr(), hq.data_ptr(), ho.data_ptr(), scale)
+        step_ms.append((time.perf_counter() - ts) * 1e3)
     for m in models:
         m.eng.wait_host()
     sec = time.perf_counter() - t0
+    st = dev.stats()
+    step_ms.sort()
     tokens = steps * len(models) * B_PER_MODEL
     if world > 1:
         import torch.distributed as dist
@@ -383,7 +394,11 @@ def e2e_arm(models, steps, scale, dev, world):
         sec, tokens = float(t[0].item()), int(t[1].item())
     return {"value": round(tokens / sec, 1), "unit": "tokens/s",
             "h2d_bytes_per_step": len(models) * (2 * kv_elems + q_elems) * 2,
-            "d2h_bytes_per_step": len(models) * q_elems * 2, "api": "prism_engine_step + prism_engine_decode_host"}
+            "d2h_bytes_per_step": len(models) * q_elems * 2, "api": "prism_engine_step + prism_engine_decode_host",
+            "host_ms_per_step": {"p50": round(step_ms[len(step_ms) // 2], 3), "max": round(step_ms[-1], 3)},
+            "vmm": {"maps": st["maps"], "premapped_hits": st["premapped_hits"], "urgent": st["urgent"],
+                    "caller_ms": round((st["map_ns_total"] + st["unmap_ns_total"]) / 1e6, 3),
+                    "worker_ms": round(st["background_ns_total"] / 1e6, 3), "premaps": st["premaps"]}}
 
 
 C2_SHAPES = {  # L, n_q, n_kv, d, weight GB
@@ -444,28 +459,30 @@ def page_churn_c2(max_rounds=2500, kv_pages=6000, horizon_s=60.0):
 
 def page_map_summary(st, steps):
     """amortised_us_per_page_op = host time the CALLER's thread (the engine /
-    scheduler loop) spends in the VMM layer — logical maps incl. unanticipated
-    steals / SetAccess / creates, and logical unmaps — per logical map+unmap.
-    background_us_per_page_op = driver time of the per-GPU worker thread
-    (pre-maps, handle creation, memory moved between models), which runs
-    beside the engine loop (tools/vmm_interference.py: it does not slow
-    kernels or launches). The breakdown counts driver calls on both threads."""
+    scheduler loop) spends in the VMM layer per logical map+unmap: revives,
+    queueing, and waiting at the step's sync point for pages the per-GPU
+    worker maps on demand. Every per-page driver call runs on the worker;
+    background_us_per_page_op is its driver time, beside the engine loop
+    (tools/vmm_interference.py: it does not slow kernels or launches). The
+    breakdown is per driver call kind (worker thread)."""
     maps, unmaps = st["maps"], st["unmaps"]
     total_us = (st["map_ns_total"] + st["unmap_ns_total"]) / 1e3
     ops = max(maps + unmaps, 1)
     return {"logical_maps": maps, "logical_unmaps": unmaps, "revived_in_place": st["revived"],
-            "premapped_hits": st["premapped_hits"], "premaps": st["premaps"],
+            "premapped_hits": st["premapped_hits"], "premaps": st["premaps"], "urgent_maps": st["urgent"],
             "driver_creates": st["creates"], "driver_unmaps": st["driver_unmaps"], "steals": st["steals"],
             "map_us_p50": round(st["map_ns_p50"] / 1e3, 2), "map_us_p99": round(st["map_ns_p99"] / 1e3, 2),
             "unmap_us_p50": round(st["unmap_ns_p50"] / 1e3, 2), "unmap_us_p99": round(st["unmap_ns_p99"] / 1e3, 2),
             "amortised_us_per_page_op": round(total_us / ops, 2),
+            "caller_wait_us_per_page_op": round(st["wait_ns_total"] / 1e3 / ops, 2),
             "background_us_per_page_op": round(st["background_ns_total"] / 1e3 / ops, 2),
             "breakdown_us_per_page_op": {
                 "cuMemSetAccess": round(st["access_ns_total"] / 1e3 / ops, 2),
                 "cuMemMap": round(st["map_call_ns_total"] / 1e3 / ops, 2),
                 "cuMemCreate": round(st["create_ns_total"] / 1e3 / ops, 2),
-                "cuMemUnmap_caller_steals": round(st["steal_ns_total"] / 1e3 / ops, 2)},
-            "note": "amortised = caller-thread time in the VMM layer; background = worker-thread driver time"}
+                "cuMemUnmap_steals": round(st["steal_ns_total"] / 1e3 / ops, 2)},
+            "steals_of_premapped": st["caller_steals_clean"],
+            "note": "amortised = engine-thread time in the VMM layer (incl. waits); background = worker-thread driver time"}
 
 
 # ---------------------------------------------------------------- CPU arm

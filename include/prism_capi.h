@@ -327,11 +327,14 @@ typedef struct {
     double create_ns_total, map_call_ns_total, access_ns_total; /* per driver call kind */
     uint64_t access_calls;
     uint64_t steals; /* parked pages moved to another VA (cross-model memory movement) */
-    double steal_ns_total; /* cuMemUnmap time of steals (included in map_ns_total) */
-    double background_ns_total; /* worker-thread driver time (pre-maps, creates, moves); off the caller's path */
+    double steal_ns_total; /* cuMemUnmap time of steals (worker thread) */
+    double background_ns_total; /* worker-thread driver time (all per-page driver calls run there) */
     uint64_t premaps;           /* pages the worker mapped ahead of need */
     uint64_t premapped_hits;    /* logical maps satisfied by a pre-mapped page */
     uint64_t batched_unmaps;    /* cuMemUnmap calls covering a run of >1 pages */
+    uint64_t caller_steals_clean; /* steals that took a pre-mapped page */
+    double wait_ns_total;       /* caller time waiting for the worker's queued maps (inside map_ns_total) */
+    uint64_t urgent;            /* pages the worker mapped on demand (not anticipated by the look-ahead) */
 } prism_device_stats;
 int prism_device_stats_get(const prism_device* d, prism_device_stats* out);
 int prism_device_reset_stats(prism_device* d);

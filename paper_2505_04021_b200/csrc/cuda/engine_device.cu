@@ -11,7 +11,7 @@ namespace prism {
 namespace pa = msim::pagealloc;
 namespace me = msim::engine;
 
-constexpr std::uint64_t kCacheTarget = 16;  // ready physical handles kept per GPU
+constexpr std::uint64_t kCacheTarget = 32;  // ready physical handles kept per GPU
 
 EngineDeviceImpl& impl_of(const me::Engine& eng) {
     auto* p = dynamic_cast<EngineDeviceImpl*>(eng.device.get());

@@ -76,9 +76,14 @@ void sample(std::vector<float>& ring, double ns) {
     if (ring.size() < kMaxSamples) ring.push_back(static_cast<float>(ns));
 }
 
-// How many parked entries the worker inspects when looking for released
-// memory to move (bounds its time under mu_).
+// How many in-window parked entries a steal skips over looking for a page
+// outside every look-ahead window (bounds the scan).
 constexpr int kStealScan = 256;
+// Longest contiguous run the worker maps before one cuMemSetAccess.
+constexpr std::size_t kPremapRun = 8;
+// At most this many pre-mapped (clean parked) pages per device (1 GiB).
+constexpr std::uint64_t kMaxClean = 512;
+
 
 CUmemAllocationProp& prop_of(void* p) { return *static_cast<CUmemAllocationProp*>(p); }
 CUmemAccessDesc& access_of(void* p) { return *static_cast<CUmemAccessDesc*>(p); }
@@ -155,45 +160,269 @@ VmmDevice::~VmmDevice() {
 
 // ---------------------------------------------------------------- worker
 
+bool VmmDevice::take_handle(Lock& lk, std::uint64_t va, bool urgent, std::uint64_t& h) {
+    // A handle for `va`; it stays counted in inflight_handles_ until it lands
+    // in live_ / parked_ (or back in cache_). Urgent maps use the buffer
+    // handle the caller earmarked, then the cache, a new handle within the
+    // budget, and finally a released page moved from elsewhere; look-ahead
+    // maps only use free budget.
+    if (urgent) {
+        const auto p = pending_.find(va);
+        if (p != pending_.end() && p->second) {
+            h = p->second;
+            p->second = 0;
+            --earmarked_;
+            ++inflight_handles_;
+            return true;
+        }
+    }
+    if (!cache_.empty()) {
+        h = cache_.back();
+        cache_.pop_back();
+        ++inflight_handles_;
+        return true;
+    }
+    if (total_locked() < budget_) {
+        ++inflight_handles_;
+        lk.unlock();
+        CUmemGenericAllocationHandle ch = 0;
+        const auto tc = Clock::now();
+        const CUresult r = drv().create(&ch, page_bytes_, &prop_of(prop_), 0);
+        const double ns = ns_since(tc);
+        lk.lock();
+        if (r == CUDA_SUCCESS) {
+            h = static_cast<std::uint64_t>(ch);
+            ++stats_.creates;
+            stats_.create_ns_total += ns;
+            return true;
+        }
+        --inflight_handles_;
+        if (!urgent) return false;
+    }
+    if (!urgent) return false;
+    if (steal_for_worker(lk, h)) return true;
+    // Nothing parked to move (the ledger never maps past the budget, so this
+    // means the budget shrank under queued maps): create past it.
+    ++inflight_handles_;
+    CUmemGenericAllocationHandle ch = 0;
+    const CUresult r = drv().create(&ch, page_bytes_, &prop_of(prop_), 0);
+    if (r != CUDA_SUCCESS) {
+        --inflight_handles_;
+        return false;
+    }
+    ++stats_.creates;
+    h = static_cast<std::uint64_t>(ch);
+    return true;
+}
+
+bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h) {
+    // Move the highest parked page that is safe (pre-mapped and never read,
+    // or released before a fence that passed), preferring pages outside every
+    // pool's look-ahead window: allocation reuses the lowest unmapped page
+    // indices, so high parked pages are the least likely to be revived soon.
+    while (!stop_) {
+        advance_fences(false);
+        auto pick = parked_.end(), fallback = parked_.end();
+        int scanned = 0;
+        for (auto it = parked_.rbegin(); it != parked_.rend(); ++it) {
+            if (!(it->second.clean || it->second.epoch < fenced_)) continue;
+            if (fallback == parked_.end()) fallback = std::prev(it.base());
+            if (!in_window(it->first)) {
+                pick = std::prev(it.base());
+                break;
+            }
+            if (++scanned >= kStealScan) break;
+        }
+        if (pick == parked_.end()) pick = fallback;
+        if (pick != parked_.end()) {
+            const std::uint64_t victim = pick->first;
+            const Parked saved = pick->second;
+            if (saved.clean) ++stats_.caller_steals_clean;
+            unpark(pick);
+            inflight_.insert(victim);
+            ++inflight_handles_;
+            lk.unlock();
+            const auto t0 = Clock::now();
+            const CUresult r = drv().unmap(static_cast<CUdeviceptr>(victim), page_bytes_);
+            const double ns = ns_since(t0);
+            lk.lock();
+            inflight_.erase(victim);
+            if (r != CUDA_SUCCESS) {
+                --inflight_handles_;
+                park(victim, saved);
+                failed_ = "cuMemUnmap failed (" + std::to_string(r) + ")";
+                done_cv_.notify_all();
+                return false;
+            }
+            ++stats_.driver_unmaps;
+            ++stats_.steals;
+            stats_.steal_ns_total += ns;
+            // its owner may have mapped the page again meanwhile
+            if (pending_.count(victim)) urgent_.push_back(victim);
+            h = saved.handle;
+            done_cv_.notify_all();
+            return true;
+        }
+        if (parked_.empty()) return false;
+        // Every parked page may still be read by queued kernels: fence and
+        // poll until that fence passes.
+        fence_locked();
+        lk.unlock();
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+        lk.lock();
+    }
+    return false;
+}
+
+void VmmDevice::map_run(Lock& lk, std::vector<std::uint64_t>& run, std::vector<std::uint64_t>& hs, bool urgent) {
+    // `run`: contiguous VAs already in inflight_, one handle each in hs.
+    lk.unlock();
+    std::size_t mapped = 0;
+    CUresult r = CUDA_SUCCESS;
+    const auto tm = Clock::now();
+    for (; mapped < run.size(); ++mapped) {
+        r = drv().map(static_cast<CUdeviceptr>(run[mapped]), page_bytes_, 0,
+                      static_cast<CUmemGenericAllocationHandle>(hs[mapped]), 0);
+        if (r != CUDA_SUCCESS) break;
+    }
+    const double map_ns = ns_since(tm);
+    double acc_ns = 0.0;
+    if (r == CUDA_SUCCESS) {
+        const auto ta = Clock::now();
+        r = drv().set_access(static_cast<CUdeviceptr>(run[0]), run.size() * page_bytes_, &access_of(access_desc_), 1);
+        acc_ns = ns_since(ta);
+    }
+    if (r != CUDA_SUCCESS) {
+        for (std::size_t i = 0; i < mapped; ++i) drv().unmap(static_cast<CUdeviceptr>(run[i]), page_bytes_);
+    }
+    lk.lock();
+    inflight_handles_ -= run.size();
+    for (std::size_t i = 0; i < run.size(); ++i) {
+        inflight_.erase(run[i]);
+        if (r != CUDA_SUCCESS) {
+            cache_.push_back(hs[i]);
+            continue;
+        }
+        const auto p = pending_.find(run[i]);
+        if (p != pending_.end()) {
+            // logically mapped meanwhile (or urgent): straight to live
+            if (p->second) {
+                cache_.push_back(p->second);
+                --earmarked_;
+            }
+            pending_.erase(p);
+            live_.emplace(run[i], hs[i]);
+        } else {
+            park(run[i], Parked{hs[i], 0, true});
+        }
+    }
+    stats_.map_call_ns_total += map_ns;
+    stats_.access_ns_total += acc_ns;
+    if (acc_ns > 0.0) ++stats_.access_calls;
+    if (r != CUDA_SUCCESS) {
+        if (urgent) failed_ = "cuMemMap/cuMemSetAccess failed (" + std::to_string(r) + ")";
+        hints_.clear();
+    } else if (urgent) {
+        stats_.urgent += run.size();
+    } else {
+        stats_.premaps += run.size();
+    }
+}
+
 void VmmDevice::worker_main() {
     if (cudaSetDevice(ordinal_) != cudaSuccess) return;
+    const auto free_va = [&](std::uint64_t v) {
+        return !live_.count(v) && !parked_.count(v) && !inflight_.count(v) && !pending_.count(v);
+    };
     Lock lk(mu_);
-    for (;;) {
-        // Next job: the first hinted VA that is neither live, parked nor in
-        // flight; otherwise top up the created-handle cache.
-        std::uint64_t va = 0;
-        bool have_va = false;
-        for (auto it = hints_.begin(); it != hints_.end() && !have_va;) {
+    while (!stop_) {
+        // 1. urgent maps, in runs of contiguous VAs
+        std::vector<std::uint64_t> run, hs;
+        while (!urgent_.empty() && run.size() < kPremapRun) {
+            const std::uint64_t v = urgent_.front();
+            if (!pending_.count(v) || inflight_.count(v)) {  // resolved by a look-ahead map
+                urgent_.pop_front();
+                continue;
+            }
+            if (!run.empty() && v != run.back() + page_bytes_) break;
+            run.push_back(v);
+            urgent_.pop_front();
+        }
+        if (!run.empty()) {
+            ++worker_busy_;
+            const auto t0 = Clock::now();
+            for (std::uint64_t v : run) inflight_.insert(v);
+            for (std::uint64_t v : run) {
+                std::uint64_t h = 0;
+                if (!take_handle(lk, v, true, h)) break;
+                hs.push_back(h);
+            }
+            if (hs.size() < run.size()) {
+                for (std::size_t i = hs.size(); i < run.size(); ++i) inflight_.erase(run[i]);
+                if (failed_.empty()) failed_ = "VmmDevice: out of physical memory for a queued map";
+                run.resize(hs.size());
+            }
+            if (!run.empty()) map_run(lk, run, hs, true);
+            stats_.background_ns_total += ns_since(t0);
+            --worker_busy_;
+            done_cv_.notify_all();
+            continue;
+        }
+        // 2. look-ahead: a run of up to kPremapRun contiguous hinted VAs
+        if (clean_ >= kMaxClean) hints_.clear();  // enough memory is pre-mapped already
+        const std::size_t max_run =
+            static_cast<std::size_t>(std::min<std::uint64_t>(kPremapRun, kMaxClean - std::min(clean_, kMaxClean)));
+        for (auto it = hints_.begin(); it != hints_.end() && run.empty();) {
             auto& list = it->second;
-            while (!list.empty()) {
+            while (!list.empty() && run.empty()) {
                 const std::uint64_t v = list.back();
                 list.pop_back();
-                if (!live_.count(v) && !parked_.count(v) && !inflight_.count(v)) {
-                    va = v;
-                    have_va = true;
-                    break;
-                }
+                if (free_va(v)) run.push_back(v);
+            }
+            while (!run.empty() && run.size() < max_run && !list.empty() && list.back() == run.back() + page_bytes_ &&
+                   free_va(list.back())) {
+                run.push_back(list.back());
+                list.pop_back();
             }
             it = list.empty() ? hints_.erase(it) : std::next(it);
         }
-        const bool want_cache = cache_.size() < cache_target_ && total_locked() < budget_;
-        if (!have_va && !want_cache) {
-            if (stop_) return;
-            done_cv_.notify_all();  // quiesce() waiters
-            cv_.wait(lk);
-            if (stop_) return;
+        if (!run.empty()) {
+            ++worker_busy_;
+            const auto t0 = Clock::now();
+            for (std::uint64_t v : run) {
+                std::uint64_t h = 0;
+                if (!take_handle(lk, v, false, h)) {
+                    hints_.clear();  // no free budget: look-ahead waits for the next hint
+                    break;
+                }
+                hs.push_back(h);
+            }
+            // creating handles may have dropped the lock: keep the prefix
+            // that is still free (a caller may have queued one urgently)
+            std::size_t keep = 0;
+            while (keep < hs.size() && free_va(run[keep])) ++keep;
+            for (std::size_t i = keep; i < hs.size(); ++i) {
+                cache_.push_back(hs[i]);
+                --inflight_handles_;
+            }
+            run.resize(keep);
+            hs.resize(keep);
+            for (std::uint64_t v : run) inflight_.insert(v);
+            if (!run.empty()) map_run(lk, run, hs, false);
+            stats_.background_ns_total += ns_since(t0);
+            --worker_busy_;
+            done_cv_.notify_all();
             continue;
         }
-        ++worker_busy_;
-        const auto t0 = Clock::now();
-        if (!have_va) {
-            // Create one handle for the cache.
+        // 3. ready handles
+        if (cache_.size() < cache_target_ && total_locked() < budget_) {
+            ++worker_busy_;
+            const auto t0 = Clock::now();
             ++inflight_handles_;
             lk.unlock();
             CUmemGenericAllocationHandle h = 0;
-            const auto tc = Clock::now();
             const CUresult r = drv().create(&h, page_bytes_, &prop_of(prop_), 0);
-            const double ns = ns_since(tc);
+            const double ns = ns_since(t0);
             lk.lock();
             --inflight_handles_;
             if (r == CUDA_SUCCESS) {
@@ -201,114 +430,22 @@ void VmmDevice::worker_main() {
                 ++stats_.creates;
                 stats_.create_ns_total += ns;
             } else {
-                cache_target_ = 0;  // out of memory: stop trying until asked again
+                cache_target_ = 0;  // out of memory: stop until asked again
             }
-            stats_.background_ns_total += ns_since(t0);
+            stats_.background_ns_total += ns;
             --worker_busy_;
             done_cv_.notify_all();
             continue;
         }
-        // Pre-map `va`: needs a handle — cached, newly created within the
-        // budget, or moved from a released (dirty, fence-passed) parked page.
-        inflight_.insert(va);
-        std::uint64_t h = 0;
-        bool ok = false;
-        std::uint64_t stolen_va = 0;
-        // A handle taken below stays counted in inflight_handles_ until it
-        // lands in parked_ (or back in cache_).
-        if (!cache_.empty()) {
-            h = cache_.back();
-            cache_.pop_back();
-            ++inflight_handles_;
-            ok = true;
-        } else if (total_locked() < budget_) {
-            ++inflight_handles_;
-            lk.unlock();
-            CUmemGenericAllocationHandle ch = 0;
-            const auto tc = Clock::now();
-            const CUresult r = drv().create(&ch, page_bytes_, &prop_of(prop_), 0);
-            const double ns = ns_since(tc);
-            lk.lock();
-            if (r == CUDA_SUCCESS) {
-                h = static_cast<std::uint64_t>(ch);
-                ok = true;
-                ++stats_.creates;
-                stats_.create_ns_total += ns;
-            } else {
-                --inflight_handles_;
-            }
-        } else {
-            advance_fences(false);
-            int scanned = 0;
-            for (auto it = parked_.rbegin(); it != parked_.rend() && scanned < kStealScan; ++it, ++scanned) {
-                if (!it->second.clean && it->second.epoch < fenced_ && !inflight_.count(it->first)) {
-                    stolen_va = it->first;
-                    break;
-                }
-            }
-            if (stolen_va) {
-                const auto p = parked_.find(stolen_va);
-                h = p->second.handle;
-                parked_.erase(p);
-                inflight_.insert(stolen_va);
-                ++inflight_handles_;
-                lk.unlock();
-                const CUresult r = drv().unmap(static_cast<CUdeviceptr>(stolen_va), page_bytes_);
-                lk.lock();
-                inflight_.erase(stolen_va);
-                ok = r == CUDA_SUCCESS;
-                if (ok) {
-                    ++stats_.driver_unmaps;
-                    ++stats_.steals;
-                } else {
-                    --inflight_handles_;
-                    parked_.emplace(stolen_va, Parked{h, 0, false});  // still mapped: leave it parked
-                }
-                done_cv_.notify_all();
-            }
-        }
-        if (!ok) {
-            // No physical memory to move: drop the remaining hints until the
-            // next premap() call (they are best effort).
-            inflight_.erase(va);
-            hints_.clear();
-            --worker_busy_;
-            done_cv_.notify_all();
-            continue;
-        }
-        lk.unlock();
-        const auto tm = Clock::now();
-        CUresult r = drv().map(static_cast<CUdeviceptr>(va), page_bytes_, 0, static_cast<CUmemGenericAllocationHandle>(h), 0);
-        const double map_ns = ns_since(tm);
-        double acc_ns = 0.0;
-        if (r == CUDA_SUCCESS) {
-            const auto ta = Clock::now();
-            r = drv().set_access(static_cast<CUdeviceptr>(va), page_bytes_, &access_of(access_desc_), 1);
-            acc_ns = ns_since(ta);
-            if (r != CUDA_SUCCESS) drv().unmap(static_cast<CUdeviceptr>(va), page_bytes_);
-        }
-        lk.lock();
-        --inflight_handles_;
-        inflight_.erase(va);
-        stats_.map_call_ns_total += map_ns;
-        stats_.access_ns_total += acc_ns;
-        ++stats_.access_calls;
-        if (r == CUDA_SUCCESS) {
-            parked_.emplace(va, Parked{h, 0, true});
-            ++stats_.premaps;
-        } else {
-            cache_.push_back(h);
-            hints_.clear();
-        }
-        stats_.background_ns_total += ns_since(t0);
-        --worker_busy_;
-        done_cv_.notify_all();
+        done_cv_.notify_all();  // idle: quiesce() waiters
+        cv_.wait(lk);
     }
 }
 
 void VmmDevice::premap(std::uint64_t owner, const std::uint64_t* vas, std::size_t n) {
     {
         Lock lk(mu_);
+        if (n) window_[owner] = {vas[0], vas[n - 1] + page_bytes_};
         auto& list = hints_[owner];
         // stored reversed: the worker pops from the back, lowest VA first
         list.assign(std::make_reverse_iterator(vas + n), std::make_reverse_iterator(vas));
@@ -320,6 +457,7 @@ void VmmDevice::premap(std::uint64_t owner, const std::uint64_t* vas, std::size_
 void VmmDevice::forget(std::uint64_t owner) {
     Lock lk(mu_);
     hints_.erase(owner);
+    window_.erase(owner);
 }
 
 void VmmDevice::prefill_cache(std::uint64_t n) {
@@ -334,19 +472,41 @@ void VmmDevice::quiesce() {
     Lock lk(mu_);
     cv_.notify_one();
     done_cv_.wait(lk, [&] {
-        return worker_busy_ == 0 && hints_.empty() &&
-               !(cache_.size() < cache_target_ && total_locked() < budget_);
+        return !failed_.empty() ||
+               (worker_busy_ == 0 && hints_.empty() && urgent_.empty() && pending_.empty() &&
+                !(cache_.size() < cache_target_ && total_locked() < budget_));
     });
-}
-
-void VmmDevice::wait_inflight(Lock& lk, std::uint64_t va) {
-    while (inflight_.count(va)) done_cv_.wait(lk);
+    check_failed();
 }
 
 // ---------------------------------------------------------------- caller side
 
+void VmmDevice::check_failed() const {
+    if (!failed_.empty()) throw std::runtime_error("VmmDevice worker: " + failed_);
+}
+
+void VmmDevice::wait_pending(Lock& lk) {
+    if (pending_.empty()) return;
+    const auto tw = Clock::now();
+    cv_.notify_one();
+    done_cv_.wait(lk, [&] { return pending_.empty() || !failed_.empty(); });
+    stats_.wait_ns_total += ns_since(tw);
+    check_failed();
+}
+
+bool VmmDevice::busy_in(std::uint64_t lo, std::uint64_t hi) const {
+    for (const auto& kv : pending_) {
+        if (kv.first >= lo && kv.first < hi) return true;
+    }
+    for (std::uint64_t v : inflight_) {
+        if (v >= lo && v < hi) return true;
+    }
+    return false;
+}
+
 std::uint64_t VmmDevice::total_locked() const {
-    return live_.size() + parked_.size() + buffer_.size() + taken_.size() + cache_.size() + inflight_handles_;
+    return live_.size() + parked_.size() + buffer_.size() + taken_.size() + cache_.size() + inflight_handles_ +
+           earmarked_;
 }
 
 std::uint64_t VmmDevice::total_handles() const {
@@ -366,9 +526,20 @@ std::uint64_t VmmDevice::pending_unmaps() const {
     return parked_.size();
 }
 
+bool VmmDevice::in_window(std::uint64_t va) const {
+    auto r = ranges_.upper_bound(va);
+    if (r == ranges_.begin()) return false;
+    --r;
+    if (va >= r->second) return false;
+    const auto w = window_.find(r->first);
+    return w != window_.end() && va >= w->second.first && va < w->second.second;
+}
+
 std::uint64_t VmmDevice::reserve(std::uint64_t pages) {
     CUdeviceptr va = 0;
     cu_check(drv().reserve(&va, pages * page_bytes_, page_bytes_, 0, 0), "cuMemAddressReserve");
+    Lock lk(mu_);
+    ranges_[static_cast<std::uint64_t>(va)] = static_cast<std::uint64_t>(va) + pages * page_bytes_;
     return static_cast<std::uint64_t>(va);
 }
 
@@ -376,13 +547,10 @@ void VmmDevice::release(std::uint64_t va, std::uint64_t pages) {
     Lock lk(mu_);
     const std::uint64_t end = va + pages * page_bytes_;
     hints_.erase(va);
-    // the worker may be mapping into (or stealing from) this range
-    done_cv_.wait(lk, [&] {
-        for (std::uint64_t v : inflight_) {
-            if (v >= va && v < end) return false;
-        }
-        return true;
-    });
+    window_.erase(va);
+    // the worker may be mapping into (or moving a page out of) this range
+    done_cv_.wait(lk, [&] { return !busy_in(va, end) || !failed_.empty(); });
+    ranges_.erase(va);
     bool synced = false;
     const auto sync = [&] {
         if (!synced) PRISM_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
@@ -392,7 +560,7 @@ void VmmDevice::release(std::uint64_t va, std::uint64_t pages) {
         if (!it->second.clean) sync();
         driver_unmap(it->first);
         cache_.push_back(it->second.handle);
-        it = parked_.erase(it);
+        it = unpark(it);
     }
     for (auto it = live_.begin(); it != live_.end();) {
         if (it->first >= va && it->first < end) {
@@ -421,11 +589,10 @@ void VmmDevice::advance_fences(bool wait) {
     fenced_ += done;
 }
 
-std::uint64_t VmmDevice::steal(Lock& lk) {
-    // Prefer the highest parked VA that is safe to move (pre-mapped and never
-    // read, or released before a fence that passed): allocation reuses the
-    // lowest unmapped page indices, so high parked pages are least likely to
-    // be revived soon.
+std::uint64_t VmmDevice::steal_now(Lock& lk) {
+    // Caller-side move (budget shrink): the highest safe parked page, after
+    // draining the stream if none is safe yet.
+    (void)lk;
     advance_fences(false);
     auto pick = parked_.end();
     for (auto it = parked_.rbegin(); it != parked_.rend(); ++it) {
@@ -435,83 +602,15 @@ std::uint64_t VmmDevice::steal(Lock& lk) {
         }
     }
     if (pick == parked_.end()) {
-        // Every parked page may still be read by in-flight kernels: fence
-        // now and wait, after which all of them are safe.
         fence_locked();
         advance_fences(true);
         pick = std::prev(parked_.end());
     }
-    const auto t0 = Clock::now();
     driver_unmap(pick->first);
     const std::uint64_t h = pick->second.handle;
-    parked_.erase(pick);
+    unpark(pick);
     ++stats_.steals;
-    stats_.steal_ns_total += ns_since(t0);  // inside a map: counted by map_ns_total
-    (void)lk;
     return h;
-}
-
-void VmmDevice::steal_batch(Lock& lk, std::size_t k) {
-    if (k == 0 || parked_.empty()) return;
-    advance_fences(false);
-    std::vector<std::uint64_t> vas;
-    vas.reserve(k);
-    for (auto it = parked_.rbegin(); it != parked_.rend() && vas.size() < k; ++it) {
-        if (it->second.clean || it->second.epoch < fenced_) vas.push_back(it->first);
-    }
-    if (vas.size() < k) {
-        fence_locked();
-        advance_fences(true);  // every parked page is now safe
-        vas.clear();
-        for (auto it = parked_.rbegin(); it != parked_.rend() && vas.size() < k; ++it) vas.push_back(it->first);
-    }
-    const auto t0 = Clock::now();
-    std::sort(vas.begin(), vas.end());
-    for (std::size_t i = 0; i < vas.size();) {
-        std::size_t j = i + 1;
-        while (j < vas.size() && vas[j] == vas[j - 1] + page_bytes_) ++j;
-        // One cuMemUnmap for a run of whole mappings; per page if refused.
-        bool done = false;
-        if (j - i > 1) {
-            done = drv().unmap(static_cast<CUdeviceptr>(vas[i]), (j - i) * page_bytes_) == CUDA_SUCCESS;
-            if (done) {
-                ++stats_.driver_unmaps;
-                ++stats_.batched_unmaps;
-            }
-        }
-        for (std::size_t x = i; x < j; ++x) {
-            if (!done) driver_unmap(vas[x]);
-            const auto p = parked_.find(vas[x]);
-            cache_.push_back(p->second.handle);
-            parked_.erase(p);
-            ++stats_.steals;
-        }
-        i = j;
-    }
-    stats_.steal_ns_total += ns_since(t0);
-    (void)lk;
-}
-
-std::uint64_t VmmDevice::acquire_handle(Lock& lk, bool from_buffer) {
-    if (from_buffer && !taken_.empty()) {
-        const std::uint64_t h = taken_.back();
-        taken_.pop_back();
-        return h;
-    }
-    if (!cache_.empty()) {
-        const std::uint64_t h = cache_.back();
-        cache_.pop_back();
-        return h;
-    }
-    if (total_locked() >= budget_ && !parked_.empty()) return steal(lk);
-    const auto tc = Clock::now();
-    CUmemGenericAllocationHandle h = 0;
-    CUresult r = drv().create(&h, page_bytes_, &prop_of(prop_), 0);
-    if (r == CUDA_ERROR_OUT_OF_MEMORY && !parked_.empty()) return steal(lk);
-    cu_check(r, "cuMemCreate");
-    ++stats_.creates;
-    stats_.create_ns_total += ns_since(tc);
-    return static_cast<std::uint64_t>(h);
 }
 
 void VmmDevice::map(std::uint64_t va, bool from_buffer) {
@@ -523,43 +622,19 @@ void VmmDevice::map_batch(const std::uint64_t* vas, std::size_t n, std::size_t n
     if (n == 0) return;
     const auto t0 = Clock::now();
     Lock lk(mu_);
-    for (std::size_t i = 0; i < n; ++i) wait_inflight(lk, vas[i]);
+    check_failed();
     stats_.maps += n;
-    {
-        // Handles this batch must obtain by stealing (budget exhausted):
-        // steal them together so contiguous parked runs share a cuMemUnmap.
-        std::size_t fresh = 0, buffered = 0;
-        for (std::size_t i = 0; i < n; ++i) {
-            if (parked_.find(vas[i]) != parked_.end()) continue;
-            ++fresh;
-            if (i < n_from_buffer) ++buffered;
-        }
-        const std::size_t have = std::min(buffered, taken_.size()) + cache_.size();
-        const std::uint64_t total = total_locked();
-        const std::uint64_t room = budget_ > total ? budget_ - total : 0;
-        if (fresh > have + room) {
-            // never steal a page this batch is about to revive
-            std::vector<std::pair<std::uint64_t, Parked>> keep;
-            for (std::size_t i = 0; i < n; ++i) {
-                const auto p = parked_.find(vas[i]);
-                if (p != parked_.end()) {
-                    keep.emplace_back(*p);
-                    parked_.erase(p);
-                }
-            }
-            steal_batch(lk, fresh - have - room);
-            for (auto& kv : keep) parked_.emplace(kv.first, kv.second);
-        }
-    }
+    bool queued = false;
     for (std::size_t i = 0; i < n; ++i) {
+        const std::uint64_t va = vas[i];
         const bool from_buffer = i < n_from_buffer;
-        const auto p = parked_.find(vas[i]);
+        const auto p = parked_.find(va);
         if (p != parked_.end()) {
             // Revive in place; a buffer handle earmarked for this map returns
             // to the cache (it stays counted as physical memory).
             if (p->second.clean) ++stats_.premapped_hits;
-            live_.emplace(vas[i], p->second.handle);
-            parked_.erase(p);
+            live_.emplace(va, p->second.handle);
+            unpark(p);
             if (from_buffer && !taken_.empty()) {
                 cache_.push_back(taken_.back());
                 taken_.pop_back();
@@ -567,62 +642,57 @@ void VmmDevice::map_batch(const std::uint64_t* vas, std::size_t n, std::size_t n
             ++stats_.revived;
             continue;
         }
-        const std::uint64_t h = acquire_handle(lk, from_buffer);
-        const auto tm = Clock::now();
-        cu_check(drv().map(static_cast<CUdeviceptr>(vas[i]), page_bytes_, 0,
-                           static_cast<CUmemGenericAllocationHandle>(h), 0),
-                 "cuMemMap");
-        stats_.map_call_ns_total += ns_since(tm);
-        live_.emplace(vas[i], h);
-        unaccessed_.push_back(vas[i]);
+        if (live_.count(va) || pending_.count(va)) throw std::runtime_error("VmmDevice::map: page already mapped");
+        std::uint64_t earmark = 0;
+        if (from_buffer && !taken_.empty()) {
+            earmark = taken_.back();
+            taken_.pop_back();
+            ++earmarked_;
+        }
+        pending_.emplace(va, earmark);
+        // a page the worker is pre-mapping right now goes live when it lands
+        if (!inflight_.count(va)) {
+            urgent_.push_back(va);
+            queued = true;
+        }
     }
-    if (!defer_access_) flush_now(lk);
+    if (queued) cv_.notify_one();
+    if (!defer_) wait_pending(lk);
     const double per = ns_since(t0) / static_cast<double>(n);
     stats_.map_ns_total += per * static_cast<double>(n);
     for (std::size_t i = 0; i < n; ++i) sample(stats_.map_ns, per);
 }
 
 void VmmDevice::defer_access(bool on) {
-    {
-        Lock lk(mu_);
-        defer_access_ = on;
+    const auto t0 = Clock::now();
+    Lock lk(mu_);
+    defer_ = on;
+    if (!on && !pending_.empty()) {
+        wait_pending(lk);
+        stats_.map_ns_total += ns_since(t0);
     }
-    if (!on) flush_access();
 }
 
 void VmmDevice::flush_access() {
-    // Deferred flush (outside map_batch): its time belongs to the maps.
     const auto t0 = Clock::now();
     Lock lk(mu_);
-    if (unaccessed_.empty()) return;
-    flush_now(lk);
+    if (pending_.empty()) return;
+    wait_pending(lk);
     stats_.map_ns_total += ns_since(t0);
-}
-
-void VmmDevice::flush_now(Lock& lk) {
-    (void)lk;
-    if (unaccessed_.empty()) return;
-    std::sort(unaccessed_.begin(), unaccessed_.end());
-    for (std::size_t i = 0; i < unaccessed_.size();) {
-        std::size_t j = i + 1;
-        while (j < unaccessed_.size() && unaccessed_[j] == unaccessed_[j - 1] + page_bytes_) ++j;
-        const auto ta = Clock::now();
-        cu_check(drv().set_access(static_cast<CUdeviceptr>(unaccessed_[i]), (j - i) * page_bytes_,
-                                  &access_of(access_desc_), 1),
-                 "cuMemSetAccess");
-        stats_.access_ns_total += ns_since(ta);
-        ++stats_.access_calls;
-        i = j;
-    }
-    unaccessed_.clear();
 }
 
 void VmmDevice::unmap(std::uint64_t va) {
     const auto t0 = Clock::now();
     Lock lk(mu_);
+    if (pending_.count(va)) {
+        // mapped and released within one step: let its map land first
+        cv_.notify_one();
+        done_cv_.wait(lk, [&] { return !pending_.count(va) || !failed_.empty(); });
+        check_failed();
+    }
     const auto it = live_.find(va);
     if (it == live_.end()) throw std::runtime_error("VmmDevice::unmap: page not mapped");
-    parked_.emplace(va, Parked{it->second, epoch_, false});
+    park(va, Parked{it->second, epoch_, false});
     live_.erase(it);
     ++stats_.unmaps;
     const double ns = ns_since(t0);
@@ -654,9 +724,12 @@ void VmmDevice::fence_locked() {
 void VmmDevice::reclaim(bool wait) {
     Lock lk(mu_);
     if (wait) {
-        // Everything goes back: stop pre-mapping and wait for the worker.
+        // Everything goes back: stop the look-ahead and drain the worker.
         hints_.clear();
-        done_cv_.wait(lk, [&] { return inflight_.empty(); });
+        cv_.notify_one();
+        done_cv_.wait(lk, [&] {
+            return (pending_.empty() && inflight_.empty() && urgent_.empty() && worker_busy_ == 0) || !failed_.empty();
+        });
         PRISM_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
         fence_locked();
         advance_fences(true);
@@ -668,7 +741,7 @@ void VmmDevice::reclaim(bool wait) {
         if (wait || (!it->second.clean && it->second.epoch < fenced_)) {
             driver_unmap(it->first);
             cache_.push_back(it->second.handle);
-            it = parked_.erase(it);
+            it = unpark(it);
         } else {
             ++it;
         }
@@ -678,7 +751,19 @@ void VmmDevice::reclaim(bool wait) {
 
 void VmmDevice::grow_buffer(std::uint64_t n) {
     Lock lk(mu_);
-    for (std::uint64_t i = 0; i < n; ++i) buffer_.push_back(acquire_handle(lk, false));
+    for (std::uint64_t i = 0; i < n; ++i) {
+        if (!cache_.empty()) {
+            buffer_.push_back(cache_.back());
+            cache_.pop_back();
+            continue;
+        }
+        CUmemGenericAllocationHandle h = 0;
+        const auto tc = Clock::now();
+        cu_check(drv().create(&h, page_bytes_, &prop_of(prop_), 0), "cuMemCreate");
+        ++stats_.creates;
+        stats_.create_ns_total += ns_since(tc);
+        buffer_.push_back(static_cast<std::uint64_t>(h));
+    }
 }
 
 void VmmDevice::take_buffer(std::uint64_t n) {
@@ -698,7 +783,7 @@ void VmmDevice::set_budget(std::uint64_t pages) {
         cache_.pop_back();
     }
     while (total_locked() > budget_ && !parked_.empty()) {
-        drv().release(static_cast<CUmemGenericAllocationHandle>(steal(lk)));
+        drv().release(static_cast<CUmemGenericAllocationHandle>(steal_now(lk)));
     }
 }
 

@@ -5,6 +5,7 @@
 // ledger has a prism::VmmDevice attached, logical maps/unmaps drive real CUDA
 // VMM calls and every slot change is appended to the pool's device op log.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "host/pool_state.hpp"
@@ -190,9 +191,18 @@ using detail::kNone;
 using detail::PoolState;
 
 // Look-ahead window handed to VmmDevice::premap when a pool grows: twice the
-// pages the growing call mapped, within [8, 64] pages (16-128 MiB).
-constexpr std::uint64_t kPremapMin = 8;
+// pages the growing call mapped, within [16, 64] pages (32-128 MiB).
+constexpr std::uint64_t kPremapMin = 16;
 constexpr std::uint64_t kPremapMax = 64;
+
+// PRISM_PREMAP=0 turns the look-ahead off (A/B measurements).
+bool premap_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PRISM_PREMAP");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
 
 inline bool is_candidate(const PoolState& s, std::uint32_t page) {
     return s.occ[page] > 0 && s.occ[page] < s.tpp;
@@ -383,7 +393,7 @@ AllocResult detail::alloc_kv_into(KvPool& pool, PhysicalLedger& ledger, std::uin
         // The pool is growing: its next maps will be the following lowest
         // unmapped pages. Hand them to the device's worker thread to map
         // (and make accessible) ahead of time, so those maps become revives.
-        const std::uint64_t ahead = std::min<std::uint64_t>(kPremapMax, std::max<std::uint64_t>(kPremapMin, 2 * new_pages));
+        const std::uint64_t ahead = !premap_enabled() ? 0 : std::min<std::uint64_t>(kPremapMax, std::max<std::uint64_t>(kPremapMin, 2 * new_pages));
         vas.clear();
         for (std::uint64_t k = 0; k < ahead && p != kNone; ++k) {
             vas.push_back(s.va + static_cast<std::uint64_t>(p) * s.dev->page_bytes());

@@ -99,10 +99,10 @@ def test_worker_premaps_the_next_pages(product, device):
     gpu.ledger.attach_device(device)
     pool = msim.alloc_kvcache(gpu.ledger, "pm", 131072, 400)  # 16 tokens per page
     device.reset_stats()
-    first = msim.alloc_kv(pool, gpu.ledger, 16)  # maps page 0, hints pages 1..8
+    first = msim.alloc_kv(pool, gpu.ledger, 16)  # maps page 0, hints pages 1..16
     device.quiesce()
     st = device.stats()
-    assert st["maps"] == 1 and st["premaps"] == 8, st
+    assert st["maps"] == 1 and st["premaps"] == 16, st
     grow = msim.alloc_kv(pool, gpu.ledger, 8 * 16)  # pages 1..8
     st = device.stats()
     assert st["premapped_hits"] == 8 and st["revived"] == 8, st
