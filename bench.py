@@ -278,11 +278,20 @@ def gpu_arm(args, rank, world):
         dist.barrier()
     torch.cuda.synchronize()
     dev.synchronize()
+    # PRISM_NCU_TIMED=1: bracket the timed region for `ncu --profile-from-start off`
+    ncu_timed = os.environ.get("PRISM_NCU_TIMED") == "1"
     with ClockSampler(torch.cuda.current_device()) as clk:
+        if ncu_timed:
+            torch.cuda.cudart().cudaProfilerStart()
+        t_mark = time.monotonic_ns()
         start.record(stream)
         launches = run_steps(models, steps, q_bufs, out_bufs, scale, events, kv_bufs)
         end.record(stream)
         end.synchronize()
+        if ncu_timed:
+            torch.cuda.cudart().cudaProfilerStop()
+    if os.environ.get("PRISM_VMM_TRACE"):
+        print(f"timed-region {t_mark} {time.monotonic_ns()}", file=sys.stderr)
     torch.cuda.synchronize()
     ms_total = start.elapsed_time(end)
     if world > 1:
@@ -368,6 +377,7 @@ def e2e_arm(models, steps, warm, scale, dev, world):
     torch.cuda.synchronize()
     dev.reset_stats()
     step_ms = []
+    t_mark = time.monotonic_ns()
     t0 = time.perf_counter()
     for _ in range(steps):
         # Serving-loop order: each model's step is enqueued (its copies run on
@@ -382,6 +392,8 @@ def e2e_arm(models, steps, warm, scale, dev, world):
     for m in models:
         m.eng.wait_host()
     sec = time.perf_counter() - t0
+    if os.environ.get("PRISM_VMM_TRACE"):
+        print(f"e2e-region {t_mark} {time.monotonic_ns()}", file=sys.stderr)
     st = dev.stats()
     step_ms.sort()
     tokens = steps * len(models) * B_PER_MODEL
@@ -464,12 +476,14 @@ def page_map_summary(st, steps):
     worker maps on demand. Every per-page driver call runs on the worker;
     background_us_per_page_op is its driver time, beside the engine loop
     (tools/vmm_interference.py: it does not slow kernels or launches). The
-    breakdown is per driver call kind (worker thread)."""
+    breakdown is per driver call kind (worker thread). Physical memory moves
+    in chunks of `chunk_pages` logical pages (one VMM handle each)."""
     maps, unmaps = st["maps"], st["unmaps"]
     total_us = (st["map_ns_total"] + st["unmap_ns_total"]) / 1e3
     ops = max(maps + unmaps, 1)
     return {"logical_maps": maps, "logical_unmaps": unmaps, "revived_in_place": st["revived"],
-            "premapped_hits": st["premapped_hits"], "premaps": st["premaps"], "urgent_maps": st["urgent"],
+            "chunk_pages": st["chunk_pages"], "premapped_hits": st["premapped_hits"],
+            "premapped_chunks": st["premaps"], "urgent_chunks": st["urgent"],
             "driver_creates": st["creates"], "driver_unmaps": st["driver_unmaps"], "steals": st["steals"],
             "map_us_p50": round(st["map_ns_p50"] / 1e3, 2), "map_us_p99": round(st["map_ns_p99"] / 1e3, 2),
             "unmap_us_p50": round(st["unmap_ns_p50"] / 1e3, 2), "unmap_us_p99": round(st["unmap_ns_p99"] / 1e3, 2),

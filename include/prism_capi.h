@@ -314,8 +314,12 @@ int prism_parse_trace_text(const char* text, const char* origin, prism_trace_eve
 
 /* ------------------------------------------------------------------ GPU data path (product only; no reference counterpart) */
 
-/* prism::VmmDevice on CUDA device `ordinal` (2 MiB pages). */
+/* prism::VmmDevice on CUDA device `ordinal` (2 MiB pages). Physical memory
+ * is managed in chunks of `chunk_pages` logical pages (one VMM handle each;
+ * 0 = PRISM_CHUNK_PAGES or 8); prism_device_open uses the default. */
 int prism_device_open(int ordinal, uint64_t page_bytes, prism_device** out);
+int prism_device_open_chunked(int ordinal, uint64_t page_bytes, uint64_t chunk_pages, prism_device** out);
+int prism_device_chunk_pages(const prism_device* d, uint64_t* out);
 void prism_device_close(prism_device* d);
 /* Ledger capacity in pages after leaving reserve_bytes of free HBM. */
 int prism_device_capacity_pages(const prism_device* d, uint64_t reserve_bytes, uint64_t* out);
@@ -329,12 +333,14 @@ typedef struct {
     uint64_t steals; /* parked pages moved to another VA (cross-model memory movement) */
     double steal_ns_total; /* cuMemUnmap time of steals (worker thread) */
     double background_ns_total; /* worker-thread driver time (all per-page driver calls run there) */
-    uint64_t premaps;           /* pages the worker mapped ahead of need */
-    uint64_t premapped_hits;    /* logical maps satisfied by a pre-mapped page */
+    uint64_t premaps;           /* chunks the worker mapped ahead of need */
+    uint64_t premapped_hits;    /* logical maps that revived a chunk mapped ahead */
     uint64_t batched_unmaps;    /* cuMemUnmap calls covering a run of >1 pages */
     uint64_t caller_steals_clean; /* steals that took a pre-mapped page */
     double wait_ns_total;       /* caller time waiting for the worker's queued maps (inside map_ns_total) */
-    uint64_t urgent;            /* pages the worker mapped on demand (not anticipated by the look-ahead) */
+    uint64_t urgent;            /* chunks the worker mapped on demand (not anticipated by the look-ahead) */
+    uint64_t total_chunks;      /* physical chunks held (mapped, cached, in flight) */
+    uint64_t chunk_pages;       /* logical pages per chunk */
 } prism_device_stats;
 int prism_device_stats_get(const prism_device* d, prism_device_stats* out);
 int prism_device_reset_stats(prism_device* d);
@@ -377,9 +383,11 @@ int prism_engine_append_kv_synthetic(prism_gpu* g, int engine_index, int layer_b
 /* K3: q, out device bf16 [n_decodes][n_q_heads][head_dim]; chunk <= 0 picks the split size. */
 int prism_engine_decode_attention(prism_gpu* g, int engine_index, int layer, const void* q, void* out, float scale,
                                   int32_t chunk);
-/* K3 implementation: 0 tensor-core mma.sync, 2-stage cp.async ring, 3 CTAs/SM,
- * split-K (default); 1 CUDA-core SIMT; 2 tensor-core, 3-stage ring, 2 CTAs/SM;
- * 3 tensor-core stream-K persistent (equal tile ranges per CTA). */
+/* K3 implementation: 3 tensor-core stream-K persistent, equal KV-tile ranges
+ * per CTA (default); 0 tensor-core mma.sync, 2-stage cp.async ring, 3 CTAs/SM,
+ * split-K; 1 CUDA-core SIMT; 2 tensor-core, 3-stage ring, 2 CTAs/SM.
+ * A positive `chunk` in prism_engine_decode_attention selects the split-K
+ * kernels (0 when variant 3 is set). */
 int prism_set_attention_variant(int variant);
 int prism_engine_synth_q(prism_gpu* g, int engine_index, int layer, uint64_t seed, float q_scale, void* q);
 /* End-to-end: the same attention with HOST buffers (pinned or pageable);

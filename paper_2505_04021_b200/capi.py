@@ -160,7 +160,7 @@ class DeviceStats(C.Structure):
         ("access_calls", c_uint64), ("steals", c_uint64), ("steal_ns_total", c_double),
         ("background_ns_total", c_double)] + [(n, c_uint64) for n in ("premaps", "premapped_hits", "batched_unmaps",
                                                                  "caller_steals_clean")] + [
-        ("wait_ns_total", c_double), ("urgent", c_uint64)]
+        ("wait_ns_total", c_double), ("urgent", c_uint64), ("total_chunks", c_uint64), ("chunk_pages", c_uint64)]
 
 
 class EngineDeviceOptions(C.Structure):
@@ -241,6 +241,8 @@ _HOST_DECLS = {
 
 _DEVICE_DECLS = {
     "prism_device_open": (c_int, [c_int, c_uint64, P(c_void_p)]),
+    "prism_device_open_chunked": (c_int, [c_int, c_uint64, c_uint64, P(c_void_p)]),
+    "prism_device_chunk_pages": (c_int, [c_void_p, P(c_uint64)]),
     "prism_device_close": (None, [c_void_p]),
     "prism_device_capacity_pages": (c_int, [c_void_p, c_uint64, P(c_uint64)]),
     "prism_device_stats_get": (c_int, [c_void_p, P(DeviceStats)]),

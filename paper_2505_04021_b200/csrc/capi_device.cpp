@@ -75,11 +75,15 @@ extern "C" {
 int prism_has_device_path(void) { return 1; }
 
 int prism_device_open(int ordinal, uint64_t page_bytes, prism_device** out) {
+    return prism_device_open_chunked(ordinal, page_bytes, 0, out);
+}
+
+int prism_device_open_chunked(int ordinal, uint64_t page_bytes, uint64_t chunk_pages, prism_device** out) {
     return dguard([&] {
         need(out, "out");
         auto* d = new prism_device();
         try {
-            d->dev = prism::VmmDevice::open(ordinal, page_bytes);
+            d->dev = prism::VmmDevice::open(ordinal, page_bytes, chunk_pages);
         } catch (...) {
             delete d;
             throw;
@@ -130,6 +134,8 @@ int prism_device_stats_get(const prism_device* d, prism_device_stats* out) {
         out->caller_steals_clean = s.caller_steals_clean;
         out->wait_ns_total = s.wait_ns_total;
         out->urgent = s.urgent;
+        out->total_chunks = d->dev->total_handles();
+        out->chunk_pages = d->dev->chunk_pages();
     });
 }
 
@@ -144,6 +150,14 @@ int prism_device_reclaim(prism_device* d, int wait) {
     return dguard([&] {
         need(d, "device");
         d->dev->reclaim(wait != 0);
+    });
+}
+
+int prism_device_chunk_pages(const prism_device* d, uint64_t* out) {
+    return dguard([&] {
+        need(d, "device");
+        need(out, "out");
+        *out = d->dev->chunk_pages();
     });
 }
 

@@ -347,19 +347,23 @@ void launch_d(int group, const AttnArgs& a, dim3 grid, cudaStream_t stream) {
 
 }  // namespace
 
-// K3 variant: 0 = tensor-core mma.sync kernel, 2-stage ring, 3 CTAs/SM
-// (default; measured 75% / 89% of HBM on C1 / C3); 1 = CUDA-core SIMT
-// kernel; 2 = tensor-core, 3-stage ring, 2 CTAs/SM. PRISM_K3=mma|simt|mma3.
-// 3 = stream-K persistent tensor-core kernel (decode_attn_streamk.cu).
+// K3 variant (PRISM_K3=streamk|mma|simt|mma3, or prism_set_attention_variant):
+//   3 = stream-K persistent tensor-core kernel (decode_attn_streamk.cu) —
+//       default: every CTA gets an equal share of all (request, kv-head) KV
+//       tiles, no wave tail; measured 85.7% / 101% of the measured copy
+//       bandwidth on C1 / C3 (profiles/r01_k3_sweep.jsonl);
+//   0 = tensor-core mma.sync kernel, 2-stage ring, 3 CTAs/SM, wave-aware
+//       split-K (74.8% / 95.0%);
+//   1 = CUDA-core SIMT kernel; 2 = tensor-core, 3-stage ring, 2 CTAs/SM.
 static int g_variant = [] {
     const char* v = std::getenv("PRISM_K3");
+    if (v && std::strcmp(v, "mma") == 0) return 0;
     if (v && std::strcmp(v, "simt") == 0) return 1;
     if (v && std::strcmp(v, "mma3") == 0) return 2;
-    if (v && std::strcmp(v, "streamk") == 0) return 3;
-    return 0;
+    return 3;
 }();
 int attention_variant() { return g_variant; }
-void set_attention_variant(int v) { g_variant = (v >= 0 && v <= 3) ? v : 0; }
+void set_attention_variant(int v) { g_variant = (v >= 0 && v <= 3) ? v : 3; }
 
 // Host launcher shared by the engine API and the C-ABI.
 void launch_decode_attention(EngineDeviceImpl& d, int layer, const void* q, void* out, float scale, int chunk_override) {

@@ -14,7 +14,9 @@
 //     and the last of them to finish merges (ticket per pair).
 // The per-tile math (mma.sync S = K·Qᵀ, movmatrix Pᵀ, Oᵀ += Vᵀ·Pᵀ, warp-shared
 // online softmax) is the same as the split-K kernel.
+#include <algorithm>
 #include <cfloat>
+#include <cstdlib>
 
 #include "cuda/attn_common.cuh"
 #include "cuda/device_impl.cuh"
@@ -410,6 +412,8 @@ void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec) {
         int dev = 0, n = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        // PRISM_SK_SMS: spread the tiles over fewer SMs (experiments)
+        if (const char* e = std::getenv("PRISM_SK_SMS")) n = std::max(1, std::min(n, std::atoi(e)));
         return n;
     }();
     const int n_pairs = n_dec * d.n_kv;
@@ -427,7 +431,11 @@ void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec) {
         d.sk_total = acc;
         d.sk_prefix.upload(static_cast<std::size_t>(n_pairs) + 1, d.stream);
         d.sk_step = d.step_serial;
-        const int per_sm = d.head_dim == 128 ? occupancy_sk_d<128>(d.group) : occupancy_sk_d<64>(d.group);
+        static const int per_sm_cap = [] {
+            const char* e = std::getenv("PRISM_SK_PER_SM");  // experiments
+            return e ? std::max(1, std::atoi(e)) : 1 << 30;
+        }();
+        const int per_sm = std::min(per_sm_cap, d.head_dim == 128 ? occupancy_sk_d<128>(d.group) : occupancy_sk_d<64>(d.group));
         const int slots = sms * per_sm;
         d.sk_per_cta = std::max(1, (d.sk_total + slots - 1) / slots);
         // partial slots per pair: CTAs a pair's tile range can touch

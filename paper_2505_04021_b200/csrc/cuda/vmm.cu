@@ -1,12 +1,13 @@
-// prism::VmmDevice implementation: CUDA VMM (driver API) behind the ledger.
+// prism::VmmDevice implementation: CUDA VMM (driver API) behind the ledger,
+// in chunks of K logical pages (see host/vmm.hpp).
 // Driver entry points are resolved at run time through the runtime's
 // cudaGetDriverEntryPoint, so the library loads on machines without a driver
 // (the CPU build/test container) and only fails when a device is opened.
 //
-// Threading: every public method takes mu_. The caller's thread performs its
-// driver calls while holding mu_ (those are the maps nobody anticipated); the
-// background worker drops mu_ around its driver calls and marks the VAs it
-// is working on in inflight_, which callers wait out on done_cv_.
+// Threading: every public method takes mu_. The worker drops mu_ around its
+// driver calls and marks the chunk it works on `inflight`; callers never
+// wait for an in-flight chunk except at sync points (wait_pending) and in
+// whole-range operations.
 #include <cuda.h>
 
 #include <algorithm>
@@ -76,21 +77,18 @@ void sample(std::vector<float>& ring, double ns) {
     if (ring.size() < kMaxSamples) ring.push_back(static_cast<float>(ns));
 }
 
-// How many in-window parked entries a steal skips over looking for a page
-// outside every look-ahead window (bounds the scan).
+// How many in-window idle chunks a steal skips over looking for one outside
+// every look-ahead window (bounds the scan).
 constexpr int kStealScan = 256;
-// Longest contiguous run the worker maps before one cuMemSetAccess.
-constexpr std::size_t kPremapRun = 8;
-// At most this many pre-mapped (clean parked) pages per device (1 GiB).
-constexpr std::uint64_t kMaxClean = 512;
-
+// At most this many logical pages are mapped ahead by the look-ahead (2 GiB).
+constexpr std::uint64_t kMaxCleanPages = 1024;
 
 CUmemAllocationProp& prop_of(void* p) { return *static_cast<CUmemAllocationProp*>(p); }
 CUmemAccessDesc& access_of(void* p) { return *static_cast<CUmemAccessDesc*>(p); }
 
 }  // namespace
 
-std::shared_ptr<VmmDevice> VmmDevice::open(int ordinal, std::uint64_t page_bytes) {
+std::shared_ptr<VmmDevice> VmmDevice::open(int ordinal, std::uint64_t page_bytes, std::uint64_t chunk_pages) {
     int count = 0;
     PRISM_CUDA(cudaGetDeviceCount(&count));
     if (ordinal < 0 || ordinal >= count) throw std::runtime_error("VmmDevice: no CUDA device " + std::to_string(ordinal));
@@ -101,10 +99,16 @@ std::shared_ptr<VmmDevice> VmmDevice::open(int ordinal, std::uint64_t page_bytes
     cu_check(drv().attribute(&vmm, CU_DEVICE_ATTRIBUTE_VIRTUAL_MEMORY_MANAGEMENT_SUPPORTED, ordinal),
              "cuDeviceGetAttribute");
     if (!vmm) throw std::runtime_error("VmmDevice: device does not support virtual memory management");
+    if (chunk_pages == 0) {
+        const char* e = std::getenv("PRISM_CHUNK_PAGES");
+        chunk_pages = e ? static_cast<std::uint64_t>(std::max(1, std::atoi(e))) : 8;
+    }
 
     std::shared_ptr<VmmDevice> dev(new VmmDevice());
     dev->ordinal_ = ordinal;
     dev->page_bytes_ = page_bytes;
+    dev->chunk_pages_ = chunk_pages;
+    dev->chunk_bytes_ = page_bytes * chunk_pages;
     auto* prop = new CUmemAllocationProp();
     std::memset(prop, 0, sizeof(*prop));
     prop->type = CU_MEM_ALLOCATION_TYPE_PINNED;
@@ -125,8 +129,25 @@ std::shared_ptr<VmmDevice> VmmDevice::open(int ordinal, std::uint64_t page_bytes
     cudaStream_t s = nullptr;
     PRISM_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
     dev->stream_ = s;
+    dev->tracing_ = std::getenv("PRISM_VMM_TRACE") != nullptr;
     dev->worker_ = std::thread([raw = dev.get()] { raw->worker_main(); });
     return dev;
+}
+
+void VmmDevice::trace(char kind, std::uint32_t n, Clock::time_point t0, double ns) {
+    if (!tracing_ || trace_.size() >= (1u << 20)) return;
+    const auto t = std::chrono::duration_cast<std::chrono::nanoseconds>(t0.time_since_epoch()).count();
+    trace_.push_back(TraceRec{static_cast<std::int64_t>(t), kind, n, static_cast<float>(ns / 1e3)});
+}
+
+void VmmDevice::dump_trace() const {
+    if (!tracing_) return;
+    if (FILE* f = std::fopen(std::getenv("PRISM_VMM_TRACE"), "w")) {
+        for (const TraceRec& r : trace_) {
+            std::fprintf(f, "%lld %c %u %.1f\n", static_cast<long long>(r.t_ns), r.kind, r.n, r.us);
+        }
+        std::fclose(f);
+    }
 }
 
 VmmDevice::~VmmDevice() {
@@ -136,19 +157,14 @@ VmmDevice::~VmmDevice() {
     }
     cv_.notify_all();
     if (worker_.joinable()) worker_.join();
+    dump_trace();
     try {
         cudaSetDevice(ordinal_);
         cudaDeviceSynchronize();
-        for (auto& [va, p] : parked_) {
-            drv().unmap(va, page_bytes_);
-            drv().release(p.handle);
+        for (auto& [va, c] : chunks_) {
+            if (c.mapped) drv().unmap(va, chunk_bytes_);
+            if (c.handle) drv().release(c.handle);
         }
-        for (auto& [va, h] : live_) {
-            drv().unmap(va, page_bytes_);
-            drv().release(h);
-        }
-        for (auto h : buffer_) drv().release(h);
-        for (auto h : taken_) drv().release(h);
         for (auto h : cache_) drv().release(h);
         for (void* e : fences_) cudaEventDestroy(static_cast<cudaEvent_t>(e));
         if (stream_) cudaStreamDestroy(static_cast<cudaStream_t>(stream_));
@@ -158,98 +174,137 @@ VmmDevice::~VmmDevice() {
     delete static_cast<CUmemAccessDesc*>(access_desc_);
 }
 
+// ---------------------------------------------------------------- bookkeeping
+
+std::uint64_t VmmDevice::chunk_of(std::uint64_t page_va) const {
+    auto r = ranges_.upper_bound(page_va);
+    if (r == ranges_.begin()) throw std::runtime_error("VmmDevice: address outside every reserved range");
+    --r;
+    return r->first + (page_va - r->first) / chunk_bytes_ * chunk_bytes_;
+}
+
+std::uint64_t VmmDevice::total_locked() const { return mapped_ + cache_.size() + creating_; }
+
+std::uint64_t VmmDevice::budget_chunks() const {
+    return (budget_pages_ + chunk_pages_ - 1) / chunk_pages_ + ranges_.size();
+}
+
+bool VmmDevice::in_window(std::uint64_t chunk_va) const {
+    auto r = ranges_.upper_bound(chunk_va);
+    if (r == ranges_.begin()) return false;
+    --r;
+    const auto w = window_.find(r->first);
+    return w != window_.end() && chunk_va >= w->second.first && chunk_va < w->second.second;
+}
+
+void VmmDevice::set_idle(std::uint64_t va, Chunk& c) {
+    idle_.insert(va);
+    if (c.clean) ++clean_;
+}
+
+void VmmDevice::drop_if_empty(ChunkMap::iterator it) {
+    const Chunk& c = it->second;
+    if (!c.mapped && !c.inflight && !c.queued && c.refs == 0 && c.handle == 0) chunks_.erase(it);
+}
+
+void VmmDevice::check_failed() const {
+    if (!failed_.empty()) throw std::runtime_error("VmmDevice worker: " + failed_);
+}
+
+void VmmDevice::wait_pending(Lock& lk) {
+    if (unready_ == 0) return;
+    const auto tw = Clock::now();
+    cv_.notify_one();
+    done_cv_.wait(lk, [&] { return unready_ == 0 || !failed_.empty(); });
+    const double ns = ns_since(tw);
+    stats_.wait_ns_total += ns;
+    trace('W', 0, tw, ns);
+    check_failed();
+}
+
 // ---------------------------------------------------------------- worker
 
-bool VmmDevice::take_handle(Lock& lk, std::uint64_t va, bool urgent, std::uint64_t& h) {
-    // A handle for `va`; it stays counted in inflight_handles_ until it lands
-    // in live_ / parked_ (or back in cache_). Urgent maps use the buffer
-    // handle the caller earmarked, then the cache, a new handle within the
-    // budget, and finally a released page moved from elsewhere; look-ahead
-    // maps only use free budget.
-    if (urgent) {
-        const auto p = pending_.find(va);
-        if (p != pending_.end() && p->second) {
-            h = p->second;
-            p->second = 0;
-            --earmarked_;
-            ++inflight_handles_;
-            return true;
-        }
-    }
+bool VmmDevice::take_handle(Lock& lk, bool urgent, std::uint64_t& h) {
+    // A handle for the chunk in flight: cached, new within the physical
+    // budget, or (urgent only) moved from an idle chunk; counted in mapped_.
     if (!cache_.empty()) {
         h = cache_.back();
         cache_.pop_back();
-        ++inflight_handles_;
+        ++mapped_;
         return true;
     }
-    if (total_locked() < budget_) {
-        ++inflight_handles_;
+    const auto create = [&]() {
+        ++creating_;
         lk.unlock();
         CUmemGenericAllocationHandle ch = 0;
         const auto tc = Clock::now();
-        const CUresult r = drv().create(&ch, page_bytes_, &prop_of(prop_), 0);
+        const CUresult r = drv().create(&ch, chunk_bytes_, &prop_of(prop_), 0);
         const double ns = ns_since(tc);
         lk.lock();
-        if (r == CUDA_SUCCESS) {
-            h = static_cast<std::uint64_t>(ch);
-            ++stats_.creates;
-            stats_.create_ns_total += ns;
-            return true;
-        }
-        --inflight_handles_;
-        if (!urgent) return false;
-    }
+        --creating_;
+        if (r != CUDA_SUCCESS) return false;
+        h = static_cast<std::uint64_t>(ch);
+        ++mapped_;
+        ++stats_.creates;
+        stats_.create_ns_total += ns;
+        trace('C', 1, tc, ns);
+        return true;
+    };
+    if (total_locked() < budget_chunks() && create()) return true;
     if (!urgent) return false;
     if (steal_for_worker(lk, h)) return true;
-    // Nothing parked to move (the ledger never maps past the budget, so this
-    // means the budget shrank under queued maps): create past it.
-    ++inflight_handles_;
-    CUmemGenericAllocationHandle ch = 0;
-    const CUresult r = drv().create(&ch, page_bytes_, &prop_of(prop_), 0);
-    if (r != CUDA_SUCCESS) {
-        --inflight_handles_;
-        return false;
-    }
-    ++stats_.creates;
-    h = static_cast<std::uint64_t>(ch);
-    return true;
+    // Nothing idle to move (the budget shrank under queued maps): past it.
+    return create();
 }
 
 bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h) {
-    // Move the highest parked page that is safe (pre-mapped and never read,
-    // or released before a fence that passed), preferring pages outside every
-    // pool's look-ahead window: allocation reuses the lowest unmapped page
-    // indices, so high parked pages are the least likely to be revived soon.
+    // Move the highest idle chunk that is safe (look-ahead and never read,
+    // or released before a fence that passed), preferring chunks outside
+    // every pool's look-ahead window: allocation reuses the lowest unmapped
+    // page indices, so high idle chunks are the least likely to be revived.
+    // The handle keeps its mapped_ count (it moves from chunk to chunk).
     while (!stop_) {
         advance_fences(false);
-        auto pick = parked_.end(), fallback = parked_.end();
+        std::uint64_t pick = 0, fallback = 0;
         int scanned = 0;
-        for (auto it = parked_.rbegin(); it != parked_.rend(); ++it) {
-            if (!(it->second.clean || it->second.epoch < fenced_)) continue;
-            if (fallback == parked_.end()) fallback = std::prev(it.base());
-            if (!in_window(it->first)) {
-                pick = std::prev(it.base());
+        for (auto it = idle_.rbegin(); it != idle_.rend(); ++it) {
+            const Chunk& v = chunks_.find(*it)->second;
+            if (!(v.clean || v.epoch < fenced_)) continue;
+            if (!fallback) fallback = *it;
+            if (!in_window(*it)) {
+                pick = *it;
                 break;
             }
             if (++scanned >= kStealScan) break;
         }
-        if (pick == parked_.end()) pick = fallback;
-        if (pick != parked_.end()) {
-            const std::uint64_t victim = pick->first;
-            const Parked saved = pick->second;
-            if (saved.clean) ++stats_.caller_steals_clean;
-            unpark(pick);
-            inflight_.insert(victim);
-            ++inflight_handles_;
+        if (!pick) pick = fallback;
+        if (pick) {
+            const auto vit = chunks_.find(pick);
+            Chunk& v = vit->second;
+            idle_.erase(pick);
+            if (v.clean) {
+                --clean_;
+                ++stats_.caller_steals_clean;
+            }
+            h = v.handle;
+            v.handle = 0;
+            v.mapped = false;
+            v.clean = false;
+            v.inflight = true;
             lk.unlock();
             const auto t0 = Clock::now();
-            const CUresult r = drv().unmap(static_cast<CUdeviceptr>(victim), page_bytes_);
+            const CUresult r = drv().unmap(static_cast<CUdeviceptr>(pick), chunk_bytes_);
             const double ns = ns_since(t0);
             lk.lock();
-            inflight_.erase(victim);
+            v.inflight = false;
             if (r != CUDA_SUCCESS) {
-                --inflight_handles_;
-                park(victim, saved);
+                v.handle = h;
+                v.mapped = true;
+                if (v.refs == 0) {
+                    set_idle(pick, v);
+                } else {
+                    --unready_;  // a caller revived it meanwhile: still mapped
+                }
                 failed_ = "cuMemUnmap failed (" + std::to_string(r) + ")";
                 done_cv_.notify_all();
                 return false;
@@ -257,14 +312,21 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h) {
             ++stats_.driver_unmaps;
             ++stats_.steals;
             stats_.steal_ns_total += ns;
-            // its owner may have mapped the page again meanwhile
-            if (pending_.count(victim)) urgent_.push_back(victim);
-            h = saved.handle;
+            trace('U', 1, t0, ns);
+            if (v.refs > 0) {
+                // its pool mapped a page in it again meanwhile: map it back
+                if (!v.queued) {
+                    urgent_.push_back(pick);
+                    v.queued = true;
+                }
+            } else {
+                drop_if_empty(vit);
+            }
             done_cv_.notify_all();
             return true;
         }
-        if (parked_.empty()) return false;
-        // Every parked page may still be read by queued kernels: fence and
+        if (idle_.empty()) return false;
+        // Every idle chunk may still be read by queued kernels: fence and
         // poll until that fence passes.
         fence_locked();
         lk.unlock();
@@ -274,161 +336,138 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h) {
     return false;
 }
 
-void VmmDevice::map_run(Lock& lk, std::vector<std::uint64_t>& run, std::vector<std::uint64_t>& hs, bool urgent) {
-    // `run`: contiguous VAs already in inflight_, one handle each in hs.
+bool VmmDevice::map_chunk(Lock& lk, std::uint64_t va, std::uint64_t h, bool urgent) {
+    // `va` is marked inflight and owns handle h (counted in mapped_).
+    const auto it = chunks_.find(va);
+    Chunk& c = it->second;
+    c.handle = h;
     lk.unlock();
-    std::size_t mapped = 0;
-    CUresult r = CUDA_SUCCESS;
     const auto tm = Clock::now();
-    for (; mapped < run.size(); ++mapped) {
-        r = drv().map(static_cast<CUdeviceptr>(run[mapped]), page_bytes_, 0,
-                      static_cast<CUmemGenericAllocationHandle>(hs[mapped]), 0);
-        if (r != CUDA_SUCCESS) break;
-    }
+    CUresult r = drv().map(static_cast<CUdeviceptr>(va), chunk_bytes_, 0, static_cast<CUmemGenericAllocationHandle>(h), 0);
     const double map_ns = ns_since(tm);
     double acc_ns = 0.0;
     if (r == CUDA_SUCCESS) {
         const auto ta = Clock::now();
-        r = drv().set_access(static_cast<CUdeviceptr>(run[0]), run.size() * page_bytes_, &access_of(access_desc_), 1);
+        r = drv().set_access(static_cast<CUdeviceptr>(va), chunk_bytes_, &access_of(access_desc_), 1);
         acc_ns = ns_since(ta);
-    }
-    if (r != CUDA_SUCCESS) {
-        for (std::size_t i = 0; i < mapped; ++i) drv().unmap(static_cast<CUdeviceptr>(run[i]), page_bytes_);
+        if (r != CUDA_SUCCESS) drv().unmap(static_cast<CUdeviceptr>(va), chunk_bytes_);
     }
     lk.lock();
-    inflight_handles_ -= run.size();
-    for (std::size_t i = 0; i < run.size(); ++i) {
-        inflight_.erase(run[i]);
-        if (r != CUDA_SUCCESS) {
-            cache_.push_back(hs[i]);
-            continue;
-        }
-        const auto p = pending_.find(run[i]);
-        if (p != pending_.end()) {
-            // logically mapped meanwhile (or urgent): straight to live
-            if (p->second) {
-                cache_.push_back(p->second);
-                --earmarked_;
-            }
-            pending_.erase(p);
-            live_.emplace(run[i], hs[i]);
-        } else {
-            park(run[i], Parked{hs[i], 0, true});
-        }
-    }
+    c.inflight = false;
     stats_.map_call_ns_total += map_ns;
     stats_.access_ns_total += acc_ns;
     if (acc_ns > 0.0) ++stats_.access_calls;
+    trace(urgent ? 'M' : 'P', 1, tm, map_ns + acc_ns);
     if (r != CUDA_SUCCESS) {
+        c.handle = 0;
+        --mapped_;
+        cache_.push_back(h);
         if (urgent) failed_ = "cuMemMap/cuMemSetAccess failed (" + std::to_string(r) + ")";
         hints_.clear();
-    } else if (urgent) {
-        stats_.urgent += run.size();
-    } else {
-        stats_.premaps += run.size();
+        if (c.refs == 0) drop_if_empty(it);
+        return false;
     }
+    c.mapped = true;
+    if (c.refs > 0) {
+        --unready_;
+        c.clean = false;
+    } else {
+        c.clean = !urgent;  // an urgent chunk whose pages all left meanwhile keeps its release epoch
+        set_idle(va, c);
+    }
+    if (urgent) {
+        ++stats_.urgent;
+    } else {
+        ++stats_.premaps;
+    }
+    return true;
 }
 
 void VmmDevice::worker_main() {
     if (cudaSetDevice(ordinal_) != cudaSuccess) return;
-    const auto free_va = [&](std::uint64_t v) {
-        return !live_.count(v) && !parked_.count(v) && !inflight_.count(v) && !pending_.count(v);
+    const auto free_chunk = [&](std::uint64_t v) {
+        const auto it = chunks_.find(v);
+        return it == chunks_.end() ||
+               (!it->second.mapped && !it->second.inflight && !it->second.queued && it->second.refs == 0);
     };
     Lock lk(mu_);
     while (!stop_) {
-        // 1. urgent maps, in runs of contiguous VAs
-        std::vector<std::uint64_t> run, hs;
-        while (!urgent_.empty() && run.size() < kPremapRun) {
-            const std::uint64_t v = urgent_.front();
-            if (!pending_.count(v) || inflight_.count(v)) {  // resolved by a look-ahead map
-                urgent_.pop_front();
+        // 1. urgent chunks
+        if (!urgent_.empty()) {
+            const std::uint64_t va = urgent_.front();
+            urgent_.pop_front();
+            const auto it = chunks_.find(va);
+            Chunk& c = it->second;
+            c.queued = false;
+            if (c.refs == 0 || c.mapped || c.inflight) {  // released, or mapped by the look-ahead
+                drop_if_empty(it);
                 continue;
             }
-            if (!run.empty() && v != run.back() + page_bytes_) break;
-            run.push_back(v);
-            urgent_.pop_front();
-        }
-        if (!run.empty()) {
             ++worker_busy_;
             const auto t0 = Clock::now();
-            for (std::uint64_t v : run) inflight_.insert(v);
-            for (std::uint64_t v : run) {
-                std::uint64_t h = 0;
-                if (!take_handle(lk, v, true, h)) break;
-                hs.push_back(h);
+            c.inflight = true;
+            std::uint64_t h = 0;
+            if (take_handle(lk, true, h)) {
+                map_chunk(lk, va, h, true);
+            } else {
+                c.inflight = false;
+                if (failed_.empty()) failed_ = "out of physical memory for a queued chunk";
             }
-            if (hs.size() < run.size()) {
-                for (std::size_t i = hs.size(); i < run.size(); ++i) inflight_.erase(run[i]);
-                if (failed_.empty()) failed_ = "VmmDevice: out of physical memory for a queued map";
-                run.resize(hs.size());
-            }
-            if (!run.empty()) map_run(lk, run, hs, true);
             stats_.background_ns_total += ns_since(t0);
             --worker_busy_;
             done_cv_.notify_all();
             continue;
         }
-        // 2. look-ahead: a run of up to kPremapRun contiguous hinted VAs
-        if (clean_ >= kMaxClean) hints_.clear();  // enough memory is pre-mapped already
-        const std::size_t max_run =
-            static_cast<std::size_t>(std::min<std::uint64_t>(kPremapRun, kMaxClean - std::min(clean_, kMaxClean)));
-        for (auto it = hints_.begin(); it != hints_.end() && run.empty();) {
+        // 2. look-ahead
+        std::uint64_t va = 0;
+        if (clean_ * chunk_pages_ >= kMaxCleanPages) hints_.clear();  // enough is mapped ahead
+        for (auto it = hints_.begin(); it != hints_.end() && !va;) {
             auto& list = it->second;
-            while (!list.empty() && run.empty()) {
+            while (!list.empty() && !va) {
                 const std::uint64_t v = list.back();
                 list.pop_back();
-                if (free_va(v)) run.push_back(v);
-            }
-            while (!run.empty() && run.size() < max_run && !list.empty() && list.back() == run.back() + page_bytes_ &&
-                   free_va(list.back())) {
-                run.push_back(list.back());
-                list.pop_back();
+                if (free_chunk(v)) va = v;
             }
             it = list.empty() ? hints_.erase(it) : std::next(it);
         }
-        if (!run.empty()) {
+        if (va) {
             ++worker_busy_;
             const auto t0 = Clock::now();
-            for (std::uint64_t v : run) {
-                std::uint64_t h = 0;
-                if (!take_handle(lk, v, false, h)) {
-                    hints_.clear();  // no free budget: look-ahead waits for the next hint
-                    break;
+            const auto it = chunks_.emplace(va, Chunk{}).first;
+            it->second.inflight = true;
+            std::uint64_t h = 0;
+            if (take_handle(lk, false, h)) {
+                map_chunk(lk, va, h, false);
+            } else {
+                it->second.inflight = false;
+                if (it->second.refs > 0 && !it->second.queued) {  // wanted meanwhile
+                    urgent_.push_back(va);
+                    it->second.queued = true;
                 }
-                hs.push_back(h);
+                drop_if_empty(it);
+                hints_.clear();  // no free budget: wait for the next hint
             }
-            // creating handles may have dropped the lock: keep the prefix
-            // that is still free (a caller may have queued one urgently)
-            std::size_t keep = 0;
-            while (keep < hs.size() && free_va(run[keep])) ++keep;
-            for (std::size_t i = keep; i < hs.size(); ++i) {
-                cache_.push_back(hs[i]);
-                --inflight_handles_;
-            }
-            run.resize(keep);
-            hs.resize(keep);
-            for (std::uint64_t v : run) inflight_.insert(v);
-            if (!run.empty()) map_run(lk, run, hs, false);
             stats_.background_ns_total += ns_since(t0);
             --worker_busy_;
             done_cv_.notify_all();
             continue;
         }
         // 3. ready handles
-        if (cache_.size() < cache_target_ && total_locked() < budget_) {
+        if (cache_.size() < cache_target_ && total_locked() < budget_chunks()) {
             ++worker_busy_;
-            const auto t0 = Clock::now();
-            ++inflight_handles_;
+            ++creating_;
             lk.unlock();
             CUmemGenericAllocationHandle h = 0;
-            const CUresult r = drv().create(&h, page_bytes_, &prop_of(prop_), 0);
+            const auto t0 = Clock::now();
+            const CUresult r = drv().create(&h, chunk_bytes_, &prop_of(prop_), 0);
             const double ns = ns_since(t0);
             lk.lock();
-            --inflight_handles_;
+            --creating_;
             if (r == CUDA_SUCCESS) {
                 cache_.push_back(static_cast<std::uint64_t>(h));
                 ++stats_.creates;
                 stats_.create_ns_total += ns;
+                trace('C', 1, t0, ns);
             } else {
                 cache_target_ = 0;  // out of memory: stop until asked again
             }
@@ -445,11 +484,18 @@ void VmmDevice::worker_main() {
 void VmmDevice::premap(std::uint64_t owner, const std::uint64_t* vas, std::size_t n) {
     {
         Lock lk(mu_);
-        if (n) window_[owner] = {vas[0], vas[n - 1] + page_bytes_};
-        auto& list = hints_[owner];
+        std::vector<std::uint64_t> chunks;
+        for (std::size_t i = 0; i < n; ++i) {
+            const std::uint64_t c = chunk_of(vas[i]);
+            if (chunks.empty() || chunks.back() != c) chunks.push_back(c);
+        }
+        if (chunks.empty()) {
+            hints_.erase(owner);
+            return;
+        }
+        window_[owner] = {chunks.front(), chunks.back() + chunk_bytes_};
         // stored reversed: the worker pops from the back, lowest VA first
-        list.assign(std::make_reverse_iterator(vas + n), std::make_reverse_iterator(vas));
-        if (list.empty()) hints_.erase(owner);
+        hints_[owner].assign(chunks.rbegin(), chunks.rend());
     }
     cv_.notify_one();
 }
@@ -460,10 +506,10 @@ void VmmDevice::forget(std::uint64_t owner) {
     window_.erase(owner);
 }
 
-void VmmDevice::prefill_cache(std::uint64_t n) {
+void VmmDevice::prefill_cache(std::uint64_t pages) {
     {
         Lock lk(mu_);
-        cache_target_ = n;
+        cache_target_ = (pages + chunk_pages_ - 1) / chunk_pages_;
     }
     cv_.notify_one();
 }
@@ -473,41 +519,13 @@ void VmmDevice::quiesce() {
     cv_.notify_one();
     done_cv_.wait(lk, [&] {
         return !failed_.empty() ||
-               (worker_busy_ == 0 && hints_.empty() && urgent_.empty() && pending_.empty() &&
-                !(cache_.size() < cache_target_ && total_locked() < budget_));
+               (worker_busy_ == 0 && urgent_.empty() && hints_.empty() &&
+                !(cache_.size() < cache_target_ && total_locked() < budget_chunks()));
     });
     check_failed();
 }
 
 // ---------------------------------------------------------------- caller side
-
-void VmmDevice::check_failed() const {
-    if (!failed_.empty()) throw std::runtime_error("VmmDevice worker: " + failed_);
-}
-
-void VmmDevice::wait_pending(Lock& lk) {
-    if (pending_.empty()) return;
-    const auto tw = Clock::now();
-    cv_.notify_one();
-    done_cv_.wait(lk, [&] { return pending_.empty() || !failed_.empty(); });
-    stats_.wait_ns_total += ns_since(tw);
-    check_failed();
-}
-
-bool VmmDevice::busy_in(std::uint64_t lo, std::uint64_t hi) const {
-    for (const auto& kv : pending_) {
-        if (kv.first >= lo && kv.first < hi) return true;
-    }
-    for (std::uint64_t v : inflight_) {
-        if (v >= lo && v < hi) return true;
-    }
-    return false;
-}
-
-std::uint64_t VmmDevice::total_locked() const {
-    return live_.size() + parked_.size() + buffer_.size() + taken_.size() + cache_.size() + inflight_handles_ +
-           earmarked_;
-}
 
 std::uint64_t VmmDevice::total_handles() const {
     Lock lk(mu_);
@@ -515,7 +533,7 @@ std::uint64_t VmmDevice::total_handles() const {
 }
 std::uint64_t VmmDevice::buffered_handles() const {
     Lock lk(mu_);
-    return buffer_.size() + taken_.size();
+    return buffer_pages_;
 }
 std::uint64_t VmmDevice::cached_handles() const {
     Lock lk(mu_);
@@ -523,56 +541,65 @@ std::uint64_t VmmDevice::cached_handles() const {
 }
 std::uint64_t VmmDevice::pending_unmaps() const {
     Lock lk(mu_);
-    return parked_.size();
-}
-
-bool VmmDevice::in_window(std::uint64_t va) const {
-    auto r = ranges_.upper_bound(va);
-    if (r == ranges_.begin()) return false;
-    --r;
-    if (va >= r->second) return false;
-    const auto w = window_.find(r->first);
-    return w != window_.end() && va >= w->second.first && va < w->second.second;
+    return idle_.size();
 }
 
 std::uint64_t VmmDevice::reserve(std::uint64_t pages) {
+    const std::uint64_t chunks = (pages + chunk_pages_ - 1) / chunk_pages_;
     CUdeviceptr va = 0;
-    cu_check(drv().reserve(&va, pages * page_bytes_, page_bytes_, 0, 0), "cuMemAddressReserve");
+    cu_check(drv().reserve(&va, chunks * chunk_bytes_, page_bytes_, 0, 0), "cuMemAddressReserve");
     Lock lk(mu_);
-    ranges_[static_cast<std::uint64_t>(va)] = static_cast<std::uint64_t>(va) + pages * page_bytes_;
+    ranges_[static_cast<std::uint64_t>(va)] = static_cast<std::uint64_t>(va) + chunks * chunk_bytes_;
     return static_cast<std::uint64_t>(va);
+}
+
+void VmmDevice::unmap_chunk_caller(ChunkMap::iterator it) {
+    Chunk& c = it->second;
+    const auto t0 = Clock::now();
+    cu_check(drv().unmap(static_cast<CUdeviceptr>(it->first), chunk_bytes_), "cuMemUnmap");
+    ++stats_.driver_unmaps;
+    sample(stats_.unmap_ns, ns_since(t0));
+    if (idle_.erase(it->first) && c.clean) --clean_;
+    c.mapped = false;
+    c.clean = false;
+    cache_.push_back(c.handle);
+    c.handle = 0;
+    --mapped_;
 }
 
 void VmmDevice::release(std::uint64_t va, std::uint64_t pages) {
     Lock lk(mu_);
-    const std::uint64_t end = va + pages * page_bytes_;
+    (void)pages;
+    const auto r = ranges_.find(va);
+    if (r == ranges_.end()) throw std::runtime_error("VmmDevice::release: unknown range");
+    const std::uint64_t end = r->second;
     hints_.erase(va);
     window_.erase(va);
-    // the worker may be mapping into (or moving a page out of) this range
-    done_cv_.wait(lk, [&] { return !busy_in(va, end) || !failed_.empty(); });
-    ranges_.erase(va);
-    bool synced = false;
-    const auto sync = [&] {
-        if (!synced) PRISM_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
-        synced = true;
-    };
-    for (auto it = parked_.lower_bound(va); it != parked_.end() && it->first < end;) {
-        if (!it->second.clean) sync();
-        driver_unmap(it->first);
-        cache_.push_back(it->second.handle);
-        it = unpark(it);
-    }
-    for (auto it = live_.begin(); it != live_.end();) {
-        if (it->first >= va && it->first < end) {
-            sync();
-            driver_unmap(it->first);
-            cache_.push_back(it->second);
-            it = live_.erase(it);
-        } else {
-            ++it;
+    // the worker may be mapping into (or moving a chunk out of) this range
+    cv_.notify_one();
+    done_cv_.wait(lk, [&] {
+        if (!failed_.empty()) return true;
+        for (auto it = chunks_.lower_bound(va); it != chunks_.end() && it->first < end; ++it) {
+            if (it->second.inflight || it->second.queued) return false;
         }
+        return true;
+    });
+    bool synced = false;
+    for (auto it = chunks_.lower_bound(va); it != chunks_.end() && it->first < end;) {
+        Chunk& c = it->second;
+        if (c.mapped) {
+            if (!c.clean && !synced) {
+                PRISM_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
+                synced = true;
+            }
+            unmap_chunk_caller(it);
+        } else if (c.refs > 0) {
+            --unready_;  // never mapped (worker failed): nothing to undo
+        }
+        it = chunks_.erase(it);
     }
-    cu_check(drv().addr_free(static_cast<CUdeviceptr>(va), pages * page_bytes_), "cuMemAddressFree");
+    ranges_.erase(r);
+    cu_check(drv().addr_free(static_cast<CUdeviceptr>(va), end - va), "cuMemAddressFree");
 }
 
 void VmmDevice::advance_fences(bool wait) {
@@ -589,36 +616,13 @@ void VmmDevice::advance_fences(bool wait) {
     fenced_ += done;
 }
 
-std::uint64_t VmmDevice::steal_now(Lock& lk) {
-    // Caller-side move (budget shrink): the highest safe parked page, after
-    // draining the stream if none is safe yet.
-    (void)lk;
-    advance_fences(false);
-    auto pick = parked_.end();
-    for (auto it = parked_.rbegin(); it != parked_.rend(); ++it) {
-        if (it->second.clean || it->second.epoch < fenced_) {
-            pick = std::prev(it.base());
-            break;
-        }
-    }
-    if (pick == parked_.end()) {
-        fence_locked();
-        advance_fences(true);
-        pick = std::prev(parked_.end());
-    }
-    driver_unmap(pick->first);
-    const std::uint64_t h = pick->second.handle;
-    unpark(pick);
-    ++stats_.steals;
-    return h;
-}
-
 void VmmDevice::map(std::uint64_t va, bool from_buffer) {
     const std::uint64_t one[1] = {va};
     map_batch(one, 1, from_buffer ? 1 : 0);
 }
 
 void VmmDevice::map_batch(const std::uint64_t* vas, std::size_t n, std::size_t n_from_buffer) {
+    (void)n_from_buffer;  // buffer pages are cached chunks (take_buffer)
     if (n == 0) return;
     const auto t0 = Clock::now();
     Lock lk(mu_);
@@ -626,35 +630,28 @@ void VmmDevice::map_batch(const std::uint64_t* vas, std::size_t n, std::size_t n
     stats_.maps += n;
     bool queued = false;
     for (std::size_t i = 0; i < n; ++i) {
-        const std::uint64_t va = vas[i];
-        const bool from_buffer = i < n_from_buffer;
-        const auto p = parked_.find(va);
-        if (p != parked_.end()) {
-            // Revive in place; a buffer handle earmarked for this map returns
-            // to the cache (it stays counted as physical memory).
-            if (p->second.clean) ++stats_.premapped_hits;
-            live_.emplace(va, p->second.handle);
-            unpark(p);
-            if (from_buffer && !taken_.empty()) {
-                cache_.push_back(taken_.back());
-                taken_.pop_back();
+        const std::uint64_t cv = chunk_of(vas[i]);
+        Chunk& c = chunks_[cv];
+        if (c.mapped) {
+            // no driver call: the chunk is mapped (live, or idle: revive)
+            if (c.refs == 0) {
+                idle_.erase(cv);
+                if (c.clean) {
+                    --clean_;
+                    ++stats_.premapped_hits;
+                    c.clean = false;
+                }
             }
             ++stats_.revived;
-            continue;
+        } else if (c.refs == 0) {
+            ++unready_;
+            if (!c.inflight && !c.queued) {
+                urgent_.push_back(cv);
+                c.queued = true;
+                queued = true;
+            }
         }
-        if (live_.count(va) || pending_.count(va)) throw std::runtime_error("VmmDevice::map: page already mapped");
-        std::uint64_t earmark = 0;
-        if (from_buffer && !taken_.empty()) {
-            earmark = taken_.back();
-            taken_.pop_back();
-            ++earmarked_;
-        }
-        pending_.emplace(va, earmark);
-        // a page the worker is pre-mapping right now goes live when it lands
-        if (!inflight_.count(va)) {
-            urgent_.push_back(va);
-            queued = true;
-        }
+        ++c.refs;
     }
     if (queued) cv_.notify_one();
     if (!defer_) wait_pending(lk);
@@ -667,7 +664,7 @@ void VmmDevice::defer_access(bool on) {
     const auto t0 = Clock::now();
     Lock lk(mu_);
     defer_ = on;
-    if (!on && !pending_.empty()) {
+    if (!on && unready_ > 0) {
         wait_pending(lk);
         stats_.map_ns_total += ns_since(t0);
     }
@@ -676,7 +673,7 @@ void VmmDevice::defer_access(bool on) {
 void VmmDevice::flush_access() {
     const auto t0 = Clock::now();
     Lock lk(mu_);
-    if (pending_.empty()) return;
+    if (unready_ == 0) return;
     wait_pending(lk);
     stats_.map_ns_total += ns_since(t0);
 }
@@ -684,27 +681,22 @@ void VmmDevice::flush_access() {
 void VmmDevice::unmap(std::uint64_t va) {
     const auto t0 = Clock::now();
     Lock lk(mu_);
-    if (pending_.count(va)) {
-        // mapped and released within one step: let its map land first
-        cv_.notify_one();
-        done_cv_.wait(lk, [&] { return !pending_.count(va) || !failed_.empty(); });
-        check_failed();
+    const auto it = chunks_.find(chunk_of(va));
+    if (it == chunks_.end() || it->second.refs == 0) throw std::runtime_error("VmmDevice::unmap: page not mapped");
+    Chunk& c = it->second;
+    if (--c.refs == 0) {
+        c.epoch = epoch_;  // kernels issued before the next fence may read it
+        c.clean = false;
+        if (c.mapped) {
+            set_idle(it->first, c);
+        } else {
+            --unready_;  // queued / in flight: lands idle (or is skipped)
+        }
     }
-    const auto it = live_.find(va);
-    if (it == live_.end()) throw std::runtime_error("VmmDevice::unmap: page not mapped");
-    park(va, Parked{it->second, epoch_, false});
-    live_.erase(it);
     ++stats_.unmaps;
     const double ns = ns_since(t0);
     stats_.unmap_ns_total += ns;
     sample(stats_.unmap_ns, ns);
-}
-
-void VmmDevice::driver_unmap(std::uint64_t va) {
-    const auto t0 = Clock::now();
-    cu_check(drv().unmap(static_cast<CUdeviceptr>(va), page_bytes_), "cuMemUnmap");
-    ++stats_.driver_unmaps;
-    sample(stats_.unmap_ns, ns_since(t0));
 }
 
 void VmmDevice::fence() {
@@ -727,9 +719,7 @@ void VmmDevice::reclaim(bool wait) {
         // Everything goes back: stop the look-ahead and drain the worker.
         hints_.clear();
         cv_.notify_one();
-        done_cv_.wait(lk, [&] {
-            return (pending_.empty() && inflight_.empty() && urgent_.empty() && worker_busy_ == 0) || !failed_.empty();
-        });
+        done_cv_.wait(lk, [&] { return (urgent_.empty() && worker_busy_ == 0) || !failed_.empty(); });
         PRISM_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream_)));
         fence_locked();
         advance_fences(true);
@@ -737,58 +727,73 @@ void VmmDevice::reclaim(bool wait) {
         advance_fences(false);
     }
     const auto t0 = Clock::now();
-    for (auto it = parked_.begin(); it != parked_.end();) {
-        if (wait || (!it->second.clean && it->second.epoch < fenced_)) {
-            driver_unmap(it->first);
-            cache_.push_back(it->second.handle);
-            it = unpark(it);
-        } else {
-            ++it;
+    for (auto v = idle_.begin(); v != idle_.end();) {
+        const auto it = chunks_.find(*v);
+        ++v;  // unmap_chunk_caller erases the current entry
+        const Chunk& c = it->second;
+        if (wait || (!c.clean && c.epoch < fenced_)) {
+            unmap_chunk_caller(it);
+            drop_if_empty(it);
         }
     }
     stats_.unmap_ns_total += ns_since(t0);
 }
 
-void VmmDevice::grow_buffer(std::uint64_t n) {
+void VmmDevice::grow_buffer(std::uint64_t pages) {
     Lock lk(mu_);
-    for (std::uint64_t i = 0; i < n; ++i) {
-        if (!cache_.empty()) {
-            buffer_.push_back(cache_.back());
-            cache_.pop_back();
-            continue;
-        }
+    buffer_pages_ += pages;
+    const std::uint64_t need = (buffer_pages_ + chunk_pages_ - 1) / chunk_pages_;
+    while (cache_.size() < need) {
         CUmemGenericAllocationHandle h = 0;
         const auto tc = Clock::now();
-        cu_check(drv().create(&h, page_bytes_, &prop_of(prop_), 0), "cuMemCreate");
+        cu_check(drv().create(&h, chunk_bytes_, &prop_of(prop_), 0), "cuMemCreate");
         ++stats_.creates;
         stats_.create_ns_total += ns_since(tc);
-        buffer_.push_back(static_cast<std::uint64_t>(h));
+        cache_.push_back(static_cast<std::uint64_t>(h));
     }
 }
 
-void VmmDevice::take_buffer(std::uint64_t n) {
+void VmmDevice::take_buffer(std::uint64_t pages) {
     Lock lk(mu_);
-    for (std::uint64_t i = 0; i < n && !buffer_.empty(); ++i) {
-        taken_.push_back(buffer_.back());
-        buffer_.pop_back();
-    }
+    buffer_pages_ -= std::min(pages, buffer_pages_);
 }
 
 void VmmDevice::set_budget(std::uint64_t pages) {
     Lock lk(mu_);
-    budget_ = pages;
-    // Shrink: free cached handles first, then physically release parked pages.
-    while (total_locked() > budget_ && !cache_.empty()) {
+    budget_pages_ = pages;
+    // Shrink: free cached handles first, then physically release idle chunks.
+    const auto over = [&] { return total_locked() > budget_chunks(); };
+    while (over() && !cache_.empty()) {
         drv().release(static_cast<CUmemGenericAllocationHandle>(cache_.back()));
         cache_.pop_back();
     }
-    while (total_locked() > budget_ && !parked_.empty()) {
-        drv().release(static_cast<CUmemGenericAllocationHandle>(steal_now(lk)));
+    while (over() && !idle_.empty()) {
+        advance_fences(false);
+        auto pick = idle_.end();
+        for (auto v = idle_.rbegin(); v != idle_.rend(); ++v) {
+            const Chunk& c = chunks_.find(*v)->second;
+            if (c.clean || c.epoch < fenced_) {
+                pick = std::prev(v.base());
+                break;
+            }
+        }
+        if (pick == idle_.end()) {
+            fence_locked();
+            advance_fences(true);
+            pick = std::prev(idle_.end());
+        }
+        const auto it = chunks_.find(*pick);
+        unmap_chunk_caller(it);
+        drop_if_empty(it);
+        drv().release(static_cast<CUmemGenericAllocationHandle>(cache_.back()));
+        cache_.pop_back();
+        ++stats_.steals;
     }
 }
 
 VmmStats VmmDevice::stats() const {
     Lock lk(mu_);
+    dump_trace();  // PRISM_VMM_TRACE only
     return stats_;
 }
 

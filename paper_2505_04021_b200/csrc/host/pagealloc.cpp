@@ -191,9 +191,12 @@ using detail::kNone;
 using detail::PoolState;
 
 // Look-ahead window handed to VmmDevice::premap when a pool grows: twice the
-// pages the growing call mapped, within [16, 64] pages (32-128 MiB).
-constexpr std::uint64_t kPremapMin = 16;
-constexpr std::uint64_t kPremapMax = 64;
+// pages the growing call mapped, within [128, 256] pages (16-32 physical
+// chunks of 8). 128 pages are ~32 decode steps of runway for a C1 pool, so
+// the worker rides out the multi-10-ms periods in which VMM calls stall
+// (tools/vmm_trace_summary.py); look-ahead only ever uses free budget.
+constexpr std::uint64_t kPremapMin = 128;
+constexpr std::uint64_t kPremapMax = 256;
 
 // PRISM_PREMAP=0 turns the look-ahead off (A/B measurements).
 bool premap_enabled() {

@@ -511,12 +511,18 @@ def throughput_of(kv_budget_bytes: int, spec: ModelSpec, prompt_tokens: int = 20
 class Device:
     """prism::VmmDevice — CUDA VMM backend of one GPU (product only)."""
 
-    def __init__(self, ordinal: int = 0, page_bytes: int = PAGE_BYTES, lib=None):
+    def __init__(self, ordinal: int = 0, page_bytes: int = PAGE_BYTES, lib=None, chunk_pages: int = 0):
+        """chunk_pages: logical pages per physical VMM handle (0: default 8)."""
         self.lib = _lib(lib)
         if not self.lib.has_device:
             raise capi.CudaError(5, f"{self.lib.path} has no GPU data path")
         self.h = C.c_void_p()
-        self.lib.call("prism_device_open", ordinal, page_bytes, C.byref(self.h))
+        self.lib.call("prism_device_open_chunked", ordinal, page_bytes, chunk_pages, C.byref(self.h))
+
+    def chunk_pages(self) -> int:
+        v = C.c_uint64()
+        self.lib.call("prism_device_chunk_pages", self.h, C.byref(v))
+        return v.value
 
     def close(self):
         if getattr(self, "h", None) and self.h.value:

@@ -77,7 +77,7 @@ def _attend_and_check(eng, spec, layers, q_scale=4.0):
 def variant(request, product):
     product.call("prism_set_attention_variant", request.param)
     yield request.param
-    product.call("prism_set_attention_variant", 0)
+    product.call("prism_set_attention_variant", 3)
 
 
 @pytest.mark.parametrize("shape", list(S.SHAPES))

@@ -93,19 +93,22 @@ def test_weights_shrink_the_physical_budget(product, device):
 
 def test_worker_premaps_the_next_pages(product, device):
     """A growing pool hands its next lowest unmapped pages to the device's
-    worker thread, which maps them ahead of need: the pool's next maps are
-    revives of those pre-mapped pages (no driver call on the caller)."""
+    worker thread, which maps their physical chunks ahead of need: the
+    pool's next maps need no driver call."""
+    K = device.chunk_pages()
     gpu = msim.GpuState(0, 200, lib=product)
     gpu.ledger.attach_device(device)
     pool = msim.alloc_kvcache(gpu.ledger, "pm", 131072, 400)  # 16 tokens per page
     device.reset_stats()
-    first = msim.alloc_kv(pool, gpu.ledger, 16)  # maps page 0, hints pages 1..16
+    first = msim.alloc_kv(pool, gpu.ledger, 16)  # maps page 0 (urgent chunk), hints the next pages
     device.quiesce()
     st = device.stats()
-    assert st["maps"] == 1 and st["premaps"] == 16, st
+    ahead = {p // K for p in range(1, 129)} - {0}
+    assert st["maps"] == 1 and st["urgent"] == 1 and st["premaps"] == len(ahead), st
     grow = msim.alloc_kv(pool, gpu.ledger, 8 * 16)  # pages 1..8
     st = device.stats()
-    assert st["premapped_hits"] == 8 and st["revived"] == 8, st
+    assert st["revived"] == 8 and st["urgent"] == 1, st  # no page needed a driver call
+    assert st["premapped_hits"] == len({p // K for p in range(1, 9)} - {0}), st
     assert sorted({h.page for h in grow.handles}) == list(range(1, 9))
     msim.free_kv(pool, gpu.ledger, first.handles + grow.handles)
     device.quiesce()
@@ -116,19 +119,21 @@ def test_worker_premaps_the_next_pages(product, device):
 
 def test_worker_stays_within_the_physical_budget(product, device):
     cap = 12
+    K = device.chunk_pages()
     gpu = msim.GpuState(0, cap, lib=product)
     gpu.ledger.attach_device(device)
     device.reclaim(True)
     pool = msim.alloc_kvcache(gpu.ledger, "tight", 131072, 400)
     device.reset_stats()
-    held = msim.alloc_kv(pool, gpu.ledger, 10 * 16).handles  # 10 pages; hint asks for 20 more
+    held = msim.alloc_kv(pool, gpu.ledger, 10 * 16).handles  # 10 pages; the hint asks for more
     device.quiesce()
-    st = device.stats()
-    assert st["premaps"] <= cap - 10, st
-    # the rest of the ledger still maps (revives / steals of pre-mapped pages)
-    more = msim.alloc_kv(pool, gpu.ledger, 2 * 16)
+    # physical budget: ceil(cap / K) chunks + one partial chunk per pool
+    budget_chunks = -(-cap // K) + 1
+    assert device.stats()["total_chunks"] <= budget_chunks
+    more = msim.alloc_kv(pool, gpu.ledger, 2 * 16)  # the rest of the ledger still maps
     assert more.shortfall_pages == 0
     assert msim.alloc_kv(pool, gpu.ledger, 1).shortfall_pages == 1
+    assert device.stats()["total_chunks"] <= budget_chunks
     msim.free_kv(pool, gpu.ledger, held + more.handles)
     device.quiesce()
     device.reclaim(True)

@@ -71,7 +71,7 @@ def main():
                 print(json.dumps({"config": name, "variant": VARIANTS[v], "chunk": chunk, "ms_per_launch": round(ms, 4),
                                   "GBps": round(gbs, 1), "frac_of_6457.7": round(gbs / 6457.7, 4)}), flush=True)
         del eng, gpu
-    lib.call("prism_set_attention_variant", 0)
+    lib.call("prism_set_attention_variant", 3)
 
 
 if __name__ == "__main__":
