@@ -86,46 +86,59 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
         return lo;
     };
 
-    // ---------------- prefetch cursor: slot ids (and kv head) of the next
-    // tile to issue are loaded one tile ahead of its cp.async, crossing pair
-    // boundaries as the CTA's range does.
-    constexpr std::uint32_t kNoSlot = 0xFFFFFFFFu;
+    // ---------------- prefetch cursor: the row offsets of the next tile to
+    // issue are decoded one tile ahead of its cp.async, crossing pair
+    // boundaries as the CTA's range does. Thread t copies 16-byte column
+    // (t % kCpr) of rows t / kCpr + i * kRowsPerPass (i < kLoads), so a warp
+    // touches kRpw rows per pass, 16 in all; lane L decodes one of them
+    // (once per tile, lanes 16-31 mirror 0-15) and each copy pass takes its
+    // row offset by shuffle: no per-thread slot-id arithmetic on the copy path.
+    constexpr int kRpw = 32 / S::kCpr;  // rows per warp per pass
+    static_assert(kRpw * S::kLoads == 16, "a warp copies 16 rows per tile");
+    constexpr std::uint64_t kNoRow = ~0ull;
     int pf = pair_of(g_begin);
     int pf_first = __ldg(T + pf), pf_end = __ldg(T + pf + 1);
     DecodeDesc pf_desc = a.desc[pf / n_kv];
-    auto load_sids = [&](int g, std::uint32_t (&dst)[S::kLoads], int& dst_h) {
+    const int sub = lane / S::kCpr;  // this thread's row within a pass
+    const int my_row = warp * kRpw + (lane & 15) % kRpw + ((lane & 15) / kRpw) * S::kRowsPerPass;
+    const std::uint64_t page_bytes = a.g.page_bytes;
+    const std::uint32_t tpp = a.g.tpp;
+    const std::uint64_t magic = a.g.magic;
+    auto load_rows = [&](int g) -> std::uint64_t {
         while (g >= pf_end) {
             ++pf;
             pf_first = pf_end;
             pf_end = __ldg(T + pf + 1);
             pf_desc = a.desc[pf / n_kv];
         }
-        dst_h = pf % n_kv;
-        const int t0 = (g - pf_first) * S::kT;
-        const std::int32_t* row = a.table + pf_desc.row;
-#pragma unroll
-        for (int i = 0; i < S::kLoads; ++i) {
-            const int t = t0 + tid / S::kCpr + i * S::kRowsPerPass;
-            dst[i] = t < pf_desc.ctx ? static_cast<std::uint32_t>(__ldg(row + t)) : kNoSlot;
-        }
+        const int h = pf % n_kv;
+        const int t = (g - pf_first) * S::kT + my_row;
+        if (t >= pf_desc.ctx) return kNoRow;
+        const std::uint32_t sid = static_cast<std::uint32_t>(__ldg(a.table + pf_desc.row + t));
+        const std::uint32_t page = slot_page(sid, magic);
+        const std::uint32_t slot = sid - page * tpp;
+        const std::uint32_t block = static_cast<std::uint32_t>(a.layer * 2 * n_kv + h);
+        return page * page_bytes + (static_cast<std::uint64_t>(block) * tpp + slot) * (D * 2);
     };
-    auto issue = [&](int g, const std::uint32_t (&sids)[S::kLoads], int h) {
+    const int col = tid % S::kCpr;
+    const int dst0 = swz_sk<D>(warp * kRpw + sub, col);  // + i * kRowsPerPass rows (row & 7 fixed)
+    auto issue = [&](int g, std::uint64_t rows) {
         unsigned char* skb = smem + (g % S::kStages) * S::kStageB;
         unsigned char* svb = skb + S::kTileB;
-        const int col = tid % S::kCpr;
 #pragma unroll
         for (int i = 0; i < S::kLoads; ++i) {
-            const int r = tid / S::kCpr + i * S::kRowsPerPass;
+            const std::uint64_t off = __shfl_sync(0xffffffffu, rows, i * kRpw + sub);
             const char* src_k = reinterpret_cast<const char*>(a.table);
             const char* src_v = src_k;
             int bytes = 0;
-            if (sids[i] != kNoSlot) {
-                src_k = base + row_offset(a.g, sids[i], a.layer, 0, h) + col * 16;
+            if (off != kNoRow) {
+                src_k = base + off + col * 16;
                 src_v = src_k + v_delta;
                 bytes = 16;
             }
-            cp_async16(skb + swz_sk<D>(r, col), src_k, bytes);
-            cp_async16(svb + swz_sk<D>(r, col), src_v, bytes);
+            const int dst = dst0 + i * S::kRowsPerPass * S::kRowB;
+            cp_async16(skb + dst, src_k, bytes);
+            cp_async16(svb + dst, src_v, bytes);
         }
     };
 
@@ -244,24 +257,23 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
     };
 
     // ---------------- pipeline over the CTA's tile range
-    std::uint32_t sids[S::kLoads];
-    int sid_h = 0;
+    std::uint64_t rows = kNoRow;
 #pragma unroll
     for (int st = 0; st < S::kStages - 1; ++st) {
         if (g_begin + st < g_end) {
-            load_sids(g_begin + st, sids, sid_h);
-            issue(g_begin + st, sids, sid_h);
+            rows = load_rows(g_begin + st);
+            issue(g_begin + st, rows);
         }
         cp_async_commit();
     }
-    if (g_begin + S::kStages - 1 < g_end) load_sids(g_begin + S::kStages - 1, sids, sid_h);
+    if (g_begin + S::kStages - 1 < g_end) rows = load_rows(g_begin + S::kStages - 1);
     const int wrow = warp * 16;
     for (int g = g_begin; g < g_end; ++g) {
         cp_async_wait<S::kStages - 2>();
         __syncthreads();
         if (g + S::kStages - 1 < g_end) {
-            issue(g + S::kStages - 1, sids, sid_h);
-            if (g + S::kStages < g_end) load_sids(g + S::kStages, sids, sid_h);
+            issue(g + S::kStages - 1, rows);
+            if (g + S::kStages < g_end) rows = load_rows(g + S::kStages);
         }
         cp_async_commit();
 
