@@ -17,8 +17,10 @@ e2e     = the same through the C-ABI with HOST buffers: per step the new K/V
           rows and q for all layers are copied from pinned host memory and the
           attention output copied back (prism_engine_decode_host)
 roofline: K3, algorithmic bytes (K+V rows of every context token + q + out)
-          per launch / mean CUDA-event duration of the K3 launches in the
-          timed region, against MEASURED_PEAKS.json hbm_gbs
+          per launch / mean K3 launch duration: CUDA events bracket each
+          model step's 32 back-to-back K3 launches in the timed region
+          (time / 32, so inter-launch gaps count against the kernel);
+          against MEASURED_PEAKS.json hbm_gbs
 cpu_baseline: reference engine::step (oracle/_ref, the reference compiled
           from its sources) for the allocation half + this repo's CPU port of
           paged attention (oracle/restate) on a bounded sample, N=1 rank 0 only
@@ -212,15 +214,19 @@ def run_steps(models, n, q_bufs, out_bufs, scale, k3_events=None, kv_bufs=None):
                 m.eng.append_kv_synthetic(0, L, SEED)  # K2 (generated content)
             launches += 2
             q, o = q_bufs[mi], out_bufs[mi]
+            # one event pair per model step brackets its L back-to-back K3
+            # launches (per-launch events would sit between the launches and
+            # serialise the programmatic-dependent overlap of one K3's tail
+            # with the next one's prologue)
+            if k3_events is not None:
+                s, e = k3_events.pop()
+                s.record(k3_events.stream)
             for layer in range(L):
-                if k3_events is not None:
-                    s, e = k3_events.pop()
-                    s.record(k3_events.stream)
                 m.eng.decode_attention(layer, q[layer].data_ptr(), o[layer].data_ptr(), scale)  # K3
-                if k3_events is not None:
-                    e.record(k3_events.stream)
-                    k3_events.used.append((s, e))
                 launches += 1
+            if k3_events is not None:
+                e.record(k3_events.stream)
+                k3_events.used.append((s, e))
     return launches
 
 
@@ -273,7 +279,7 @@ def gpu_arm(args, rank, world):
 
     # ---- value: device-timed K steps, inputs resident in HBM
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    events = EventPool(steps * len(models) * L, stream)
+    events = EventPool(steps * len(models), stream)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -297,7 +303,7 @@ def gpu_arm(args, rank, world):
     if world > 1:
         dist.barrier()
     bytes_per_launch = k3_bytes(models)
-    k3_ms = [s.elapsed_time(e) for s, e in events.used]
+    k3_ms = [s.elapsed_time(e) / L for s, e in events.used]  # mean per launch within each model step
     vstats = dev.stats()
 
     ms_max = ms_total
@@ -347,7 +353,7 @@ def gpu_arm(args, rank, world):
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind,
                      "kernel": "k3_decode (paged GQA decode attention)",
                      "k3_mean_ms": round(avg_ms, 5), "k3_bytes_per_launch": int(avg_bytes),
-                     "k3_share_of_step": round(sum(k3_ms) / ms_total, 4)},
+                     "k3_share_of_step": round(sum(k3_ms) * L / ms_total, 4)},
         "page_map": page_map_summary(vstats, steps),
         "clocks": clk.summary(),
     }

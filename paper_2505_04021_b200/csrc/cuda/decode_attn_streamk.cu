@@ -164,7 +164,6 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
         m0 = m1 = -INFINITY;
         l0 = l1 = 0.f;
     };
-    start_pair();
 
     float* red_o = reinterpret_cast<float*>(smem + S::kRingB);  // [warps][G][D]
     float* red_m = red_o + S::kWarps * G * D;                  // [warps][8]
@@ -267,6 +266,14 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
         cp_async_commit();
     }
     if (g_begin + S::kStages - 1 < g_end) rows = load_rows(g_begin + S::kStages - 1);
+    // Programmatic dependent launch: everything above reads only state that
+    // predates the previous kernel on the stream (block table, decode
+    // descriptors, tile prefix, K/V pages — see EngineDeviceImpl::k3_chain),
+    // so it overlaps that kernel's tail. q, out and the split-K workspace
+    // (shared with the previous K3) are touched only after it completed.
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    start_pair();
     const int wrow = warp * 16;
     for (int g = g_begin; g < g_end; ++g) {
         cp_async_wait<S::kStages - 2>();
@@ -354,7 +361,7 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
 }
 
 template <int D, int G>
-void launch_sk(const SkArgs& s, cudaStream_t stream, int sms) {
+void launch_sk(const SkArgs& s, cudaStream_t stream, int sms, bool chained) {
     using S = SkShape<D, G>;
     static int per_sm = 0;
     if (per_sm == 0) {
@@ -366,8 +373,17 @@ void launch_sk(const SkArgs& s, cudaStream_t stream, int sms) {
     }
     (void)sms;
     const int grid = (s.total_tiles + s.per_cta - 1) / s.per_cta;
-    k3_decode_streamk<D, G><<<grid, S::kThreads, S::kSmem, stream>>>(s);
-    PRISM_CUDA(cudaGetLastError());
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(S::kThreads);
+    cfg.dynamicSmemBytes = S::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = chained ? 1 : 0;
+    PRISM_CUDA(cudaLaunchKernelEx(&cfg, k3_decode_streamk<D, G>, s));
 }
 
 template <int D, int G>
@@ -400,16 +416,16 @@ int occupancy_sk_d(int group) {
 }
 
 template <int D>
-void launch_sk_d(int group, const SkArgs& s, cudaStream_t stream, int sms) {
+void launch_sk_d(int group, const SkArgs& s, cudaStream_t stream, int sms, bool chained) {
     switch (group) {
-        case 1: launch_sk<D, 1>(s, stream, sms); break;
-        case 2: launch_sk<D, 2>(s, stream, sms); break;
-        case 3: launch_sk<D, 3>(s, stream, sms); break;
-        case 4: launch_sk<D, 4>(s, stream, sms); break;
-        case 5: launch_sk<D, 5>(s, stream, sms); break;
-        case 6: launch_sk<D, 6>(s, stream, sms); break;
-        case 7: launch_sk<D, 7>(s, stream, sms); break;
-        case 8: launch_sk<D, 8>(s, stream, sms); break;
+        case 1: launch_sk<D, 1>(s, stream, sms, chained); break;
+        case 2: launch_sk<D, 2>(s, stream, sms, chained); break;
+        case 3: launch_sk<D, 3>(s, stream, sms, chained); break;
+        case 4: launch_sk<D, 4>(s, stream, sms, chained); break;
+        case 5: launch_sk<D, 5>(s, stream, sms, chained); break;
+        case 6: launch_sk<D, 6>(s, stream, sms, chained); break;
+        case 7: launch_sk<D, 7>(s, stream, sms, chained); break;
+        case 8: launch_sk<D, 8>(s, stream, sms, chained); break;
         default: throw std::runtime_error("decode_attention: unsupported GQA group");
     }
 }
@@ -429,7 +445,14 @@ void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec) {
         return n;
     }();
     const int n_pairs = n_dec * d.n_kv;
+    // PDL only behind our own K3 of this step (PRISM_K3_PDL=0 disables)
+    static const bool pdl = [] {
+        const char* e = std::getenv("PRISM_K3_PDL");
+        return !(e && e[0] == '0');
+    }();
+    bool chained = pdl && d.k3_chain;
     if (d.sk_step != d.step_serial) {
+        chained = false;  // the prefix upload below precedes this launch
         d.sk_prefix.ensure(static_cast<std::size_t>(n_pairs) + 1);
         std::int32_t acc = 0;
         for (int b = 0; b < n_dec; ++b) {
@@ -467,11 +490,13 @@ void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec) {
     s.a.part_o = ws;
     s.a.part_ml = ws + per * d.head_dim;
     s.a.tickets = d.attn_counters(static_cast<std::size_t>(n_pairs));
+    chained = chained && d.k3_chain;  // a workspace reallocation breaks the chain
     if (d.head_dim == 128) {
-        launch_sk_d<128>(d.group, s, d.stream, sms);
+        launch_sk_d<128>(d.group, s, d.stream, sms, chained);
     } else {
-        launch_sk_d<64>(d.group, s, d.stream, sms);
+        launch_sk_d<64>(d.group, s, d.stream, sms, chained);
     }
+    d.k3_chain = true;
 }
 
 }  // namespace prism

@@ -147,10 +147,17 @@ public:
     std::uint64_t sk_step = ~0ull;
     Staging<std::int32_t> sk_prefix;
     int sk_total = 0, sk_per_cta = 1, sk_max_parts = 1;
+    // true while the last operation this engine put on `stream` is a
+    // stream-K K3 launch (no K1 / K2 / upload / other kernel since): the next
+    // K3 may then be launched as a programmatic dependent (PDL) of it.
+    bool k3_chain = false;
 
     // host-buffer (end-to-end) path
     cudaStream_t copy_stream = nullptr;
-    void* host_stage = nullptr;       // device staging for K/V/q/out
+    void* host_stage = nullptr;       // device staging for K/V/q/out: two sets
+    int stage_parity = 0;             // set the next call uses
+    bool stage_used[2] = {false, false};
+    cudaEvent_t stage_free[2] = {nullptr, nullptr};  // recorded after a set's last reader
     std::size_t host_stage_bytes = 0;
     std::vector<cudaEvent_t> host_events;
     cudaEvent_t host_done = nullptr;

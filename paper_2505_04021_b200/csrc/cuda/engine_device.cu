@@ -67,6 +67,9 @@ EngineDeviceImpl::~EngineDeviceImpl() {
     }
     for (cudaEvent_t ev : host_events) cudaEventDestroy(ev);
     if (host_done) cudaEventDestroy(host_done);
+    for (cudaEvent_t e : stage_free) {
+        if (e) cudaEventDestroy(e);
+    }
     if (host_stage) cudaFree(host_stage);
     if (table) cudaFree(table);
     if (step_slots) cudaFree(step_slots);
@@ -133,6 +136,7 @@ void EngineDeviceImpl::grow_table(std::int64_t need) {
 }
 
 void EngineDeviceImpl::begin_step(me::Engine&) {
+    k3_chain = false;
     // Pages unmapped during earlier steps become reclaimable once the fence
     // recorded here (after every kernel the caller issued for those steps)
     // has passed; see VmmDevice.
@@ -145,6 +149,7 @@ void EngineDeviceImpl::end_step(me::Engine&, const me::IterationOutcome& out, co
                                 std::int32_t prefill_tokens) {
     vmm->defer_access(false);  // pages must be accessible before K2/K3 run
     ++step_serial;
+    k3_chain = false;
     // K1: replay this step's allocations / frees on the device slot state.
     const std::int64_t n = pool->mirror->replay(*pool, table, step_slots, opts.max_step_tokens, stream);
     step_tokens = static_cast<int>(n);
@@ -181,6 +186,7 @@ void EngineDeviceImpl::end_step(me::Engine&, const me::IterationOutcome& out, co
 
 float* EngineDeviceImpl::attn_workspace(std::size_t floats) {
     if (floats > workspace_floats) {
+        k3_chain = false;
         if (workspace) {
             PRISM_CUDA(cudaStreamSynchronize(stream));
             PRISM_CUDA(cudaFree(workspace));
@@ -193,6 +199,7 @@ float* EngineDeviceImpl::attn_workspace(std::size_t floats) {
 
 int* EngineDeviceImpl::attn_counters(std::size_t n) {
     if (n > counters_n) {
+        k3_chain = false;
         if (counters) {
             PRISM_CUDA(cudaStreamSynchronize(stream));
             PRISM_CUDA(cudaFree(counters));
@@ -224,46 +231,60 @@ void decode_host(me::Engine& eng, const void* new_k, const void* new_v, const vo
         PRISM_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         d.host_events.push_back(ev);
     }
-    if (need > d.host_stage_bytes) {
+    // Two staging sets, alternating per call: the copies of this call only
+    // wait for the compute work of the call before the previous one (the last
+    // reader of this set), so the next step's inputs stream in while the
+    // current step's kernels run.
+    const std::size_t set_bytes = (need + 255) / 256 * 256;
+    if (2 * set_bytes > d.host_stage_bytes) {
         PRISM_CUDA(cudaStreamSynchronize(d.copy_stream));
         PRISM_CUDA(cudaStreamSynchronize(d.stream));
         if (d.host_stage) PRISM_CUDA(cudaFree(d.host_stage));
-        PRISM_CUDA(cudaMalloc(&d.host_stage, need));
-        d.host_stage_bytes = need;
+        PRISM_CUDA(cudaMalloc(&d.host_stage, 2 * set_bytes));
+        d.host_stage_bytes = 2 * set_bytes;
+        d.stage_used[0] = d.stage_used[1] = false;
     }
-    char* dk = static_cast<char*>(d.host_stage);
+    for (cudaEvent_t& e : d.stage_free) {
+        if (!e) PRISM_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    const int set = d.stage_parity;
+    d.stage_parity ^= 1;
+    char* dk = static_cast<char*>(d.host_stage) + set * (d.host_stage_bytes / 2);
     char* dv = dk + kv_bytes;
     char* dq = dv + kv_bytes;
     char* dout = dq + q_layer * L;
     cudaStream_t cs = d.copy_stream;
     std::vector<cudaEvent_t>& ev = d.host_events;
-    // Copies of this call start after the compute stream's earlier work on
-    // the staging buffers; q of layer l gates only K3(l); out of layer l goes
-    // back while K3(l+1) runs.
-    PRISM_CUDA(cudaEventRecord(ev[0], d.stream));
-    PRISM_CUDA(cudaStreamWaitEvent(cs, ev[0], 0));
-    if (new_k && new_v && n_tok) {
+    if (d.stage_used[set]) PRISM_CUDA(cudaStreamWaitEvent(cs, d.stage_free[set], 0));
+    // All inputs (new K/V rows, q of every layer) go in one burst and gate
+    // the compute stream once; outputs go back in groups of kOutGroup layers
+    // while the following layers' K3 run. Few cross-stream edges keep the K3
+    // launches back to back (programmatic-dependent chain).
+    constexpr int kOutGroup = 8;
+    const bool with_kv = new_k && new_v && n_tok;
+    if (with_kv) {
         PRISM_CUDA(cudaMemcpyAsync(dk, new_k, kv_bytes, cudaMemcpyHostToDevice, cs));
         PRISM_CUDA(cudaMemcpyAsync(dv, new_v, kv_bytes, cudaMemcpyHostToDevice, cs));
-        PRISM_CUDA(cudaEventRecord(ev[0], cs));
-        PRISM_CUDA(cudaStreamWaitEvent(d.stream, ev[0], 0));
-        append_step_kv(eng, 0, L, dk, dv);
     }
+    if (n_dec) PRISM_CUDA(cudaMemcpyAsync(dq, q, q_layer * L, cudaMemcpyHostToDevice, cs));
+    PRISM_CUDA(cudaEventRecord(ev[1], cs));
+    PRISM_CUDA(cudaStreamWaitEvent(d.stream, ev[1], 0));
+    if (with_kv) append_step_kv(eng, 0, L, dk, dv);
     if (n_dec) {
         for (int l = 0; l < L; ++l) {
-            PRISM_CUDA(cudaMemcpyAsync(dq + q_layer * l, static_cast<const char*>(q) + q_layer * l, q_layer,
-                                       cudaMemcpyHostToDevice, cs));
-            PRISM_CUDA(cudaEventRecord(ev[1 + l], cs));
-        }
-        for (int l = 0; l < L; ++l) {
-            PRISM_CUDA(cudaStreamWaitEvent(d.stream, ev[1 + l], 0));
             launch_decode_attention(d, l, dq + q_layer * l, dout + q_layer * l, scale, 0);
-            PRISM_CUDA(cudaEventRecord(ev[1 + L + l], d.stream));
-            PRISM_CUDA(cudaStreamWaitEvent(cs, ev[1 + L + l], 0));
-            PRISM_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + q_layer * l, dout + q_layer * l, q_layer,
-                                       cudaMemcpyDeviceToHost, cs));
+            if ((l + 1) % kOutGroup == 0 || l + 1 == L) {
+                const int first = l / kOutGroup * kOutGroup;
+                cudaEvent_t e = ev[2 + l / kOutGroup];
+                PRISM_CUDA(cudaEventRecord(e, d.stream));
+                PRISM_CUDA(cudaStreamWaitEvent(cs, e, 0));
+                PRISM_CUDA(cudaMemcpyAsync(static_cast<char*>(out) + q_layer * first, dout + q_layer * first,
+                                           q_layer * (l + 1 - first), cudaMemcpyDeviceToHost, cs));
+            }
         }
     }
+    PRISM_CUDA(cudaEventRecord(d.stage_free[set], d.stream));
+    d.stage_used[set] = true;
     PRISM_CUDA(cudaEventRecord(d.host_done, cs));
     if (wait) wait_host(eng);
 }

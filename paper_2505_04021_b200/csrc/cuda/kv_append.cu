@@ -91,6 +91,7 @@ void launch_append(EngineDeviceImpl& d, int layer_begin, int layer_end, const vo
         throw std::runtime_error("append_step_kv: bad layer range");
     }
     if (d.step_tokens == 0) return;
+    d.k3_chain = false;
     AppendArgs a{d.geom,  d.step_slots, d.token_meta.dev, static_cast<const uint4*>(k), static_cast<const uint4*>(v),
                  layer_begin, layer_end - layer_begin, d.step_tokens, seed};
     const std::uint64_t work =
@@ -119,6 +120,7 @@ void append_step_kv_synthetic(msim::engine::Engine& eng, int layer_begin, int la
 void synth_decode_q(msim::engine::Engine& eng, int layer, std::uint64_t seed, float q_scale, void* q) {
     EngineDeviceImpl& d = impl_of(eng);
     if (d.step_decodes == 0) return;
+    d.k3_chain = false;
     const std::uint64_t work = static_cast<std::uint64_t>(d.step_decodes) * d.n_q * d.head_dim;
     k_synth_q<<<grid_for(work, 256), 256, 0, d.stream>>>(d.decode_desc.dev, d.step_decodes, d.n_q, d.head_dim, layer,
                                                           seed, q_scale, static_cast<__nv_bfloat16*>(q));

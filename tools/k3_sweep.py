@@ -13,7 +13,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2505_04021_b200 import msim  # noqa: E402
 
 L, NQ, NKV, D = 32, 32, 8, 128
-VARIANTS = {0: "mma-2stage", 1: "simt", 2: "mma-3stage", 3: "streamk"}
+PEAK = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "MEASURED_PEAKS.json")))["hbm_gbs"]
+VARIANTS = {0: "mma-2stage", 1: "simt", 2: "mma-3stage", 3: "streamk", 4: "bulk"}
 
 
 def build(dev, B, ctx):
@@ -64,12 +65,12 @@ def main():
     for name, B, ctx, chunks, reps in (("C1", 64, 2048, (0, 256, 512, 1024, 2048), 10),
                                        ("C3", 16, 32768, (0, 512, 1024, 2048, 4096), 3)):
         gpu, eng = build(dev, B, ctx)
-        for v in (3, 0, 2, 1):
+        for v in [int(x) for x in os.environ.get("K3_VARIANTS", "3,0,2,1").split(",")]:
             lib.call("prism_set_attention_variant", v)
-            for chunk in (chunks if v != 3 else (0,)):
+            for chunk in (chunks if v < 3 else (0,)):
                 ms, gbs = time_k3(dev, eng, B, chunk, reps)
                 print(json.dumps({"config": name, "variant": VARIANTS[v], "chunk": chunk, "ms_per_launch": round(ms, 4),
-                                  "GBps": round(gbs, 1), "frac_of_6457.7": round(gbs / 6457.7, 4)}), flush=True)
+                                  "GBps": round(gbs, 1), "frac_of_peak": round(gbs / PEAK, 4)}), flush=True)
         del eng, gpu
     lib.call("prism_set_attention_variant", 3)
 
