@@ -96,29 +96,56 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
     constexpr int kRpw = 32 / S::kCpr;  // rows per warp per pass
     static_assert(kRpw * S::kLoads == 16, "a warp copies 16 rows per tile");
     constexpr std::uint64_t kNoRow = ~0ull;
+    // The cursor is software-pipelined two deep so no load latency is exposed
+    // on the copy path: the raw slot id of a tile is loaded one iteration
+    // before it is decoded into a row offset (load_sid / decode_row), and the
+    // end tile + descriptor of the pair after the cursor's are loaded when the
+    // cursor enters a pair (crossing a boundary then needs no load).
     int pf = pair_of(g_begin);
     int pf_first = __ldg(T + pf), pf_end = __ldg(T + pf + 1);
-    DecodeDesc pf_desc = a.desc[pf / n_kv];
+    int pf_ctx = a.desc[pf / n_kv].ctx;
+    std::int64_t pf_row = a.desc[pf / n_kv].row;
+    int nx_end = 0, nx_ctx = 0;
+    std::int64_t nx_row = 0;
+    auto prefetch_next_pair = [&]() {
+        if (pf + 1 < sk.n_pairs) {
+            nx_end = __ldg(T + pf + 2);
+            nx_ctx = a.desc[(pf + 1) / n_kv].ctx;
+            nx_row = a.desc[(pf + 1) / n_kv].row;
+        }
+    };
+    prefetch_next_pair();
     const int sub = lane / S::kCpr;  // this thread's row within a pass
     const int my_row = warp * kRpw + (lane & 15) % kRpw + ((lane & 15) / kRpw) * S::kRowsPerPass;
     const std::uint64_t page_bytes = a.g.page_bytes;
     const std::uint32_t tpp = a.g.tpp;
     const std::uint64_t magic = a.g.magic;
-    auto load_rows = [&](int g) -> std::uint64_t {
-        while (g >= pf_end) {
+    // raw slot id of this lane's row of tile g (-1: past the context) and
+    // its (layer, K, kv head) block
+    auto load_sid = [&](int g, std::uint32_t& block) -> std::int32_t {
+        if (g >= pf_end) {  // every pair has >= 1 tile: at most one crossing per tile
             ++pf;
             pf_first = pf_end;
-            pf_end = __ldg(T + pf + 1);
-            pf_desc = a.desc[pf / n_kv];
+            pf_end = nx_end;
+            pf_ctx = nx_ctx;
+            pf_row = nx_row;
+            prefetch_next_pair();
         }
-        const int h = pf % n_kv;
+        block = static_cast<std::uint32_t>(a.layer * 2 * n_kv + pf % n_kv);
         const int t = (g - pf_first) * S::kT + my_row;
-        if (t >= pf_desc.ctx) return kNoRow;
-        const std::uint32_t sid = static_cast<std::uint32_t>(__ldg(a.table + pf_desc.row + t));
+        return t < pf_ctx ? __ldg(a.table + pf_row + t) : -1;
+    };
+    auto decode_row = [&](std::int32_t sid_raw, std::uint32_t block) -> std::uint64_t {
+        if (sid_raw < 0) return kNoRow;
+        const std::uint32_t sid = static_cast<std::uint32_t>(sid_raw);
         const std::uint32_t page = slot_page(sid, magic);
         const std::uint32_t slot = sid - page * tpp;
-        const std::uint32_t block = static_cast<std::uint32_t>(a.layer * 2 * n_kv + h);
         return page * page_bytes + (static_cast<std::uint64_t>(block) * tpp + slot) * (D * 2);
+    };
+    auto load_rows = [&](int g) -> std::uint64_t {
+        std::uint32_t block;
+        const std::int32_t sid = load_sid(g, block);
+        return decode_row(sid, block);
     };
     const int col = tid % S::kCpr;
     const int dst0 = swz_sk<D>(warp * kRpw + sub, col);  // + i * kRowsPerPass rows (row & 7 fixed)
@@ -149,9 +176,23 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
     std::uint32_t qb[S::kKSteps][2];
     float o[S::kMTiles][4];
     float m0, m1, l0, l1;
+    // the pair after cp: its end tile and context are loaded, and its q
+    // block pulled into L1, when cp starts (only after the PDL wait: q may be
+    // produced by the previous kernel)
+    int cn_end = 0, cn_ctx = 0;
     auto start_pair = [&]() {
         const int b = cp / n_kv, h = cp % n_kv;
-        ctx = a.desc[b].ctx;
+        if (cp + 1 < sk.n_pairs && cp_end < g_end) {
+            cn_end = __ldg(T + cp + 2);
+            cn_ctx = a.desc[(cp + 1) / n_kv].ctx;
+            constexpr int kLines = G * D * 2 / 128;
+            if (tid < kLines) {
+                const int nb = (cp + 1) / n_kv, nh = (cp + 1) % n_kv;
+                const char* nq = reinterpret_cast<const char*>(
+                    a.q + (static_cast<std::size_t>(nb) * n_q + static_cast<std::size_t>(nh) * G) * D);
+                asm volatile("prefetch.global.L1 [%0];\n" ::"l"(nq + tid * 128));
+            }
+        }
         const __nv_bfloat16* qrow =
             a.q + (static_cast<std::size_t>(b) * n_q + static_cast<std::size_t>(h) * G + qr) * D;
 #pragma unroll
@@ -266,6 +307,8 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
         cp_async_commit();
     }
     if (g_begin + S::kStages - 1 < g_end) rows = load_rows(g_begin + S::kStages - 1);
+    std::uint32_t blk_p = 0;  // raw slot id / block of tile g + kStages (decoded one iteration later)
+    std::int32_t sid_p = g_begin + S::kStages < g_end ? load_sid(g_begin + S::kStages, blk_p) : -1;
     // Programmatic dependent launch: everything above reads only state that
     // predates the previous kernel on the stream (block table, decode
     // descriptors, tile prefix, K/V pages — see EngineDeviceImpl::k3_chain),
@@ -273,6 +316,7 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
     // (shared with the previous K3) are touched only after it completed.
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    ctx = a.desc[cp / n_kv].ctx;
     start_pair();
     const int wrow = warp * 16;
     for (int g = g_begin; g < g_end; ++g) {
@@ -280,7 +324,10 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
         __syncthreads();
         if (g + S::kStages - 1 < g_end) {
             issue(g + S::kStages - 1, rows);
-            if (g + S::kStages < g_end) rows = load_rows(g + S::kStages);
+            if (g + S::kStages < g_end) {
+                rows = decode_row(sid_p, blk_p);
+                if (g + S::kStages + 1 < g_end) sid_p = load_sid(g + S::kStages + 1, blk_p);
+            }
         }
         cp_async_commit();
 
@@ -352,7 +399,8 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
             if (g + 1 < g_end) {
                 ++cp;
                 cp_first = cp_end;
-                cp_end = __ldg(T + cp + 1);
+                cp_end = cn_end;
+                ctx = cn_ctx;
                 start_pair();
             }
         }
