@@ -266,6 +266,7 @@ def gpu_arm(args, rank, world):
     gen = torch.Generator(device="cuda").manual_seed(SEED)
     kv_bufs = [tuple((torch.rand((L, B_PER_MODEL, NKV, D), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
                      for _ in range(2)) for _ in models]
+    torch.cuda.synchronize()  # K/V producers (torch stream) before the engine stream reads them
     scale = 1.0 / math.sqrt(D)
     # q content: synthetic at each request's current position (per layer)
     for mi, m in enumerate(models):

@@ -12,7 +12,11 @@
 //   decode_attention       K3: paged GQA decode attention (bf16 in, fp32
 //                          accumulation, split-K) for the requests that
 //                          decoded in the last step, one layer per call.
-// All device work is asynchronous on the GPU's stream (VmmDevice::stream()).
+// All device work is asynchronous on the GPU's stream (VmmDevice::stream(),
+// engine_stream()); device buffers passed in (K/V, q) must be complete in that
+// stream's order and outputs are ready in it — a caller producing them on
+// another stream orders the two (event / stream wait), as with any library
+// stream.
 // Every function throws std::runtime_error when CUDA is unavailable — there
 // is no CPU fallback.
 #pragma once
@@ -55,6 +59,18 @@ void append_step_kv_synthetic(msim::engine::Engine& eng, int layer_begin, int la
 // K3. q, out: device bf16 [last_step_decodes][n_q_heads][head_dim]; scale is
 // applied to q·k (pass 1/sqrt(head_dim) for standard attention).
 void decode_attention(msim::engine::Engine& eng, int layer, const void* q, void* out, float scale);
+
+// K4 (chunked-prefill attention, tcgen05/TMEM): causal attention of the last
+// step's prefill chunk over its request's pages. q, out: device bf16
+// [last_step_prefill_tokens][n_q_heads][head_dim]; query i sits at position
+// last_step_prefill_first + i and attends keys 0..that position (the chunk's
+// own K/V must have been appended, K2). head_dim 64 or 128.
+void prefill_attention(msim::engine::Engine& eng, int layer, const void* q, void* out, float scale);
+// Query tokens of the last step's prefill chunk (0: none, or it was preempted
+// in the same step), the position of its first token and its request id.
+int last_step_prefill_tokens(const msim::engine::Engine& eng);
+int last_step_prefill_first(const msim::engine::Engine& eng);
+std::uint64_t last_step_prefill_request(const msim::engine::Engine& eng);
 
 // End-to-end decode with HOST buffers for the last step: H2D of the new K/V
 // rows ([n_layers][last_step_tokens][n_kv][head_dim], may be null) and q

@@ -389,6 +389,16 @@ int prism_engine_decode_attention(prism_gpu* g, int engine_index, int layer, con
  * A positive `chunk` in prism_engine_decode_attention selects the split-K
  * kernels (0 when variant 3 is set). */
 int prism_set_attention_variant(int variant);
+/* K4, chunked-prefill attention of the last step's prefill chunk (no reference
+ * counterpart: the reference allocates the chunk, engine.cpp:182-210, but
+ * computes no attention). q, out: device bf16
+ * [n_tokens][n_q_heads][head_dim]; query i at position first + i attends keys
+ * 0..first+i of its request (causal), K/V from the pages (append them first). */
+int prism_engine_prefill_info(const prism_gpu* g, int engine_index, int32_t* n_tokens, int32_t* first,
+                              uint64_t* request);
+int prism_engine_prefill_attention(prism_gpu* g, int engine_index, int layer, const void* q, void* out, float scale);
+/* Diagnostics: progress words of the last K4 launch (PRISM_K4_DEBUG=1), readable while it runs. */
+int prism_debug_k4_progress(uint32_t* out, int32_t n, int32_t* got);
 int prism_engine_synth_q(prism_gpu* g, int engine_index, int layer, uint64_t seed, float q_scale, void* q);
 /* End-to-end: the same attention with HOST buffers (pinned or pageable);
  * copies q in, runs K2 for new_k/new_v (host, may be null) over all layers

@@ -294,6 +294,7 @@ int prism_engine_append_kv_synthetic(prism_gpu* g, int engine_index, int layer_b
 
 namespace prism {
 void launch_decode_attention(class EngineDeviceImpl& d, int layer, const void* q, void* out, float scale, int chunk);
+int k4_debug_read(unsigned* out, int n);
 EngineDeviceImpl& impl_of(const msim::engine::Engine& eng);
 void set_attention_variant(int v);
 }  // namespace prism
@@ -306,6 +307,32 @@ int prism_engine_decode_attention(prism_gpu* g, int engine_index, int layer, con
         need(q, "q");
         need(out, "out");
         prism::launch_decode_attention(prism::impl_of(engine_at(g, engine_index)), layer, q, out, scale, chunk);
+    });
+}
+
+int prism_engine_prefill_info(const prism_gpu* g, int engine_index, int32_t* n_tokens, int32_t* first,
+                              uint64_t* request) {
+    return dguard([&] {
+        const me::Engine& e = engine_at(g, engine_index);
+        if (n_tokens) *n_tokens = prism::last_step_prefill_tokens(e);
+        if (first) *first = prism::last_step_prefill_first(e);
+        if (request) *request = prism::last_step_prefill_request(e);
+    });
+}
+
+int prism_engine_prefill_attention(prism_gpu* g, int engine_index, int layer, const void* q, void* out, float scale) {
+    return dguard([&] {
+        need(q, "q");
+        need(out, "out");
+        prism::prefill_attention(engine_at(g, engine_index), layer, q, out, scale);
+    });
+}
+
+int prism_debug_k4_progress(uint32_t* out, int32_t n, int32_t* got) {
+    return dguard([&] {
+        need(out, "out");
+        const int m = prism::k4_debug_read(out, n);
+        if (got) *got = m;
     });
 }
 

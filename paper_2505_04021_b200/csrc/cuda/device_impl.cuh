@@ -134,6 +134,11 @@ public:
     int step_tokens = 0;
     int step_decodes = 0;
     std::vector<std::uint64_t> decode_ids;
+    // the last step's prefill chunk (K4): block-table row, first position,
+    // query tokens (0: no live chunk), request id
+    std::int64_t prefill_row = -1;
+    std::int32_t prefill_first = 0, prefill_chunk = 0;
+    std::uint64_t prefill_request = 0;
     Staging<TokenMeta> token_meta;
     Staging<DecodeDesc> decode_desc;
 

@@ -161,6 +161,14 @@ void EngineDeviceImpl::end_step(me::Engine&, const me::IterationOutcome& out, co
     };
     token_meta.ensure(static_cast<std::size_t>(std::max<std::int64_t>(n, 1)));
     std::int64_t k = 0;
+    this->prefill_row = -1;
+    this->prefill_chunk = 0;
+    if (prefill_row >= 0 && !dead(prefill_id)) {
+        this->prefill_row = prefill_row;
+        this->prefill_first = prefill_first;
+        this->prefill_chunk = out.chunk_tokens;
+        this->prefill_request = prefill_id;
+    }
     if (prefill_row >= 0) {
         const bool is_dead = dead(prefill_id);
         for (std::int32_t t = 0; t < prefill_tokens; ++t, ++k) {

@@ -479,6 +479,17 @@ class Engine:
         self.lib.call("prism_engine_decode_attention", self.gpu.h, self.index, layer, C.c_void_p(q_ptr),
                       C.c_void_p(out_ptr), scale, chunk)
 
+    def prefill_info(self):
+        """(query tokens, first position, request id) of the last step's
+        prefill chunk; tokens == 0 when there is none."""
+        n, first, rid = C.c_int32(), C.c_int32(), C.c_uint64()
+        self.lib.call("prism_engine_prefill_info", self.gpu.h, self.index, C.byref(n), C.byref(first), C.byref(rid))
+        return n.value, first.value, rid.value
+
+    def prefill_attention(self, layer: int, q_ptr: int, out_ptr: int, scale: float) -> None:
+        self.lib.call("prism_engine_prefill_attention", self.gpu.h, self.index, layer, C.c_void_p(q_ptr),
+                      C.c_void_p(out_ptr), scale)
+
     def synth_q(self, layer: int, seed: int, q_scale: float, q_ptr: int) -> None:
         self.lib.call("prism_engine_synth_q", self.gpu.h, self.index, layer, seed, q_scale, C.c_void_p(q_ptr))
 

@@ -46,5 +46,11 @@ def device(product):
     from paper_2505_04021_b200 import msim
 
     dev = msim.Device(0, lib=product)
+    # Device pointers handed to the engine must be ready on its stream (the
+    # engine's kernels do not wait for other streams): run the tests' torch
+    # work (K/V / q producers, output reads) on that same stream.
+    prev = torch.cuda.current_stream()
+    torch.cuda.set_stream(torch.cuda.ExternalStream(dev.stream()))
     yield dev
+    torch.cuda.set_stream(prev)
     dev.close()
