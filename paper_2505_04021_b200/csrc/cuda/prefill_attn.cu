@@ -29,7 +29,9 @@
 //              into the TMEM O accumulator; completion reaches the other
 //              roles through tcgen05.commit on mbarriers.
 // S(t+1) is issued before P(t)·V(t), so the tensor core computes the next
-// scores while the softmax warps work on the current ones.
+// scores while the softmax warps work on the current ones; P is double
+// buffered, so the softmax of tile t+1 overlaps P(t)·V(t) (only a rare O
+// rescale waits for it).
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -78,8 +80,8 @@ struct PfShape {
     static constexpr int kOffQ = 0;
     static constexpr int kOffKV = kOffQ + kQB;
     static constexpr int kOffP = kOffKV + 2 * kStageB;
-    static constexpr int kOffRows = kOffP + kPB;   // [2][kN] K row byte offsets (loaders)
-    static constexpr int kOffBar = kOffRows + 2 * kN * 8;
+    static constexpr int kOffRows = kOffP + 2 * kPB;  // P double buffer; then [2][kN] K row offsets / 128 B
+    static constexpr int kOffBar = kOffRows + 2 * kN * 4;
     static constexpr int kBars = 12;
     static constexpr int kSmem = kOffBar + kBars * 8 + 16 + 1024;  // + TMEM address slot + alignment slack
     static constexpr int kThreads = 256;
@@ -230,6 +232,7 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
         }
         mb_init(b_pfull, 128);
         mb_init(b_pvdone, 1);
+        mb_init(b_pvdone + 8, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     if (warp == 7) {
@@ -268,18 +271,21 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
         const char* base = reinterpret_cast<const char*>(a.g.base);
         const std::uint64_t kblock = static_cast<std::uint64_t>(a.layer * 2 * n_kv + h) * a.g.tpp;
         const std::uint64_t v_delta = static_cast<std::uint64_t>(n_kv) * a.g.tpp * (D * 2);
-        std::uint64_t* offs = reinterpret_cast<std::uint64_t*>(smem + S::kOffRows);  // [2][kN]
-        constexpr std::uint64_t kNone = ~0ull;
+        // row start offsets in 128-byte units (rows are 128 / 256 B aligned;
+        // < 2^32 units for a 180 GB pool), kNone past the keys
+        std::uint32_t* offs = reinterpret_cast<std::uint32_t*>(smem + S::kOffRows);  // [2][kN]
+        constexpr std::uint32_t kNone = ~0u;
         auto load_sid = [&](int t, int r) -> std::int32_t {
             const int key = t * S::kN + r;
             return (r < S::kN && key < kv_len) ? __ldg(a.row + key) : -1;
         };
-        auto decode = [&](std::int32_t sid_raw) -> std::uint64_t {
+        auto decode = [&](std::int32_t sid_raw) -> std::uint32_t {
             if (sid_raw < 0) return kNone;
             const std::uint32_t sid = static_cast<std::uint32_t>(sid_raw);
             const std::uint32_t page = slot_page(sid, a.g.magic);
             const std::uint32_t slot = sid - page * a.g.tpp;
-            return static_cast<std::uint64_t>(page) * a.g.page_bytes + (kblock + slot) * (D * 2);
+            return static_cast<std::uint32_t>(
+                (static_cast<std::uint64_t>(page) * a.g.page_bytes + (kblock + slot) * (D * 2)) >> 7);
         };
         auto store_offs = [&](int t, std::int32_t s0, std::int32_t s1) {
             offs[(t & 1) * S::kN + lt] = decode(s0);
@@ -297,13 +303,13 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
             if (t >= 2) mb_wait(b_kvempty + 8 * s, ((t >> 1) - 1) & 1);
             unsigned char* kt = smem + S::kOffKV + s * S::kStageB;
             unsigned char* vt = kt + S::kKB;
-            const std::uint64_t* to = offs + s * S::kN;
+            const std::uint32_t* to = offs + s * S::kN;
             for (int r = r0; r < S::kN; r += kRowsPerPass) {
-                const std::uint64_t off = to[r];
+                const std::uint32_t off = to[r];
                 const char* srck = base;
                 int bytes = 0;
                 if (off != kNone) {
-                    srck = base + off + c * 16;
+                    srck = base + (static_cast<std::uint64_t>(off) << 7) + c * 16;
                     bytes = 16;
                 }
                 cp_async16(kt + sw_off<S::kN>(r, c), srck, bytes);
@@ -348,10 +354,10 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
 #pragma unroll
                 for (int k = 0; k < S::kN / 16; ++k) {
                     const std::uint32_t poff = (k >> 2) * (128 * 128) + (k & 3) * 32;
-                    tc_mma(tmem + S::kColO, sw128_desc(sP + poff, 16), sw128_desc(vt + k * 2048, S::kN * 128),
+                    tc_mma(tmem + S::kColO, sw128_desc(sP + (t & 1) * S::kPB + poff, 16), sw128_desc(vt + k * 2048, S::kN * 128),
                            idesc_o, (t > 0 || k > 0) ? 1u : 0u);
                 }
-                tc_commit(b_pvdone);
+                tc_commit(b_pvdone + 8 * (t & 1));
                 tc_commit(b_kvempty + 8 * (t & 1));
                 k4_mark(a.dbg, 4, 100 + t);
             }
@@ -365,6 +371,13 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
         const bool row_ok = tok < tq && r < kTQ * G;
         const int pos = row_ok ? a.first + i0 + tok : -1;  // last key this row may attend
         float m_run = -INFINITY, l_run = 0.f;
+        // PV(j) completes phase j >> 1 of pv_done[j & 1] (one barrier per P
+        // buffer): PV(j + 2) needs this warpgroup's P(j + 2), so a barrier is
+        // never two phases ahead of a wait here and parity waits are exact
+        auto ensure_pv = [&](int j) {
+            mb_wait(b_pvdone + 8 * (j & 1), (j >> 1) & 1);
+            tc_fence_after();
+        };
         for (int t = 0; t < n_tiles; ++t) {
             const int s = t & 1;
             mb_wait(b_sfull + 8 * s, (t >> 1) & 1);
@@ -373,16 +386,28 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
             const std::uint32_t ts = tmem + lane_base + s * 128;
             const int k0 = t * S::kN;
             // pass 1: row max of this tile (scaled, log2 domain)
-            float mt = -INFINITY;
+            // (8 independent partial maxima / sums: one warp per scheduler, so
+            // the reductions must not be one serial dependency chain; tiles
+            // entirely below the diagonal skip the causal mask)
+            const bool full = k0 + S::kN - 1 <= pos;
+            const int lim = pos - k0;  // last visible column of this tile
+            float mx[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
                 float v[32];
                 tc_ld32(ts + cc * 32, v);
+                if (full) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    if (k0 + cc * 32 + j <= pos) mt = fmaxf(mt, v[j] * a.scale_log2);
+                    for (int j = 0; j < 32; ++j) mx[j & 7] = fmaxf(mx[j & 7], v[j]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) mx[j & 7] = fmaxf(mx[j & 7], cc * 32 + j <= lim ? v[j] : -INFINITY);
                 }
             }
+            float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+            mt *= a.scale_log2;  // scale > 0: max commutes with the scaling
             // lazy rescale (threshold 2^8): only when the max grows a lot
             bool rescale = false;
             float alpha = 1.f;
@@ -395,12 +420,12 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
                 l_run *= alpha;
             }
             const float m_use = m_run == -INFINITY ? 0.f : m_run;
-            // P(t) reuses the single P buffer and O is touched below: PV(t-1) must be done
-            if (t >= 1) {
-                mb_wait(b_pvdone, (t - 1) & 1);
-                tc_fence_after();
-            }
+            // P(t) goes to P buffer t & 1, last read by PV(t-2)
+            if (t >= 2) ensure_pv(t - 2);
             // pass 2: p = exp2(s - m), row sum, bf16 P into the swizzled K-major P tile
+            float ls[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ls[j] = 0.f;
 #pragma unroll
             for (int cc = 0; cc < 4; ++cc) {
                 float v[32];
@@ -408,22 +433,29 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
                 std::uint32_t pk[16];
 #pragma unroll
                 for (int j = 0; j < 32; j += 2) {
-                    const float p0 = k0 + cc * 32 + j <= pos ? fast_exp2(v[j] * a.scale_log2 - m_use) : 0.f;
-                    const float p1 = k0 + cc * 32 + j + 1 <= pos ? fast_exp2(v[j + 1] * a.scale_log2 - m_use) : 0.f;
-                    l_run += p0 + p1;
+                    float p0 = fast_exp2(fmaf(v[j], a.scale_log2, -m_use));
+                    float p1 = fast_exp2(fmaf(v[j + 1], a.scale_log2, -m_use));
+                    if (!full) {
+                        p0 = cc * 32 + j <= lim ? p0 : 0.f;
+                        p1 = cc * 32 + j + 1 <= lim ? p1 : 0.f;
+                    }
+                    ls[(j >> 1) & 7] += p0 + p1;
                     pk[j >> 1] = pack_bf16(p0, p1);
                 }
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
                     const int chunk = cc * 4 + q4;  // 16-byte chunk of the 256-byte P row
-                    unsigned char* dst = smem + S::kOffP + sw_off<S::kM>(r, chunk);
+                    unsigned char* dst = smem + S::kOffP + (t & 1) * S::kPB + sw_off<S::kM>(r, chunk);
                     *reinterpret_cast<uint4*>(dst) = make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
                 }
             }
+            l_run += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
             tc_fence_before();
             mb_arrive(b_sfree + 8 * s);
-            // O *= alpha for the rows whose max moved (warp-collective TMEM access)
+            // O *= alpha for the rows whose max moved (warp-collective TMEM
+            // access; rare with the 2^8 threshold): O must be settled, PV(t-1) done
             if (__any_sync(0xffffffffu, rescale)) {
+                ensure_pv(t - 1);
 #pragma unroll
                 for (int cc = 0; cc < D / 32; ++cc) {
                     float v[32];
@@ -440,8 +472,7 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
             if (r == 0) k4_mark(a.dbg, 6, 100 + t);
         }
         // epilogue: O / l -> bf16 -> out[token][h*G + g][:]
-        mb_wait(b_pvdone, (n_tiles - 1) & 1);
-        tc_fence_after();
+        ensure_pv(n_tiles - 1);
         if (r == 0) k4_mark(a.dbg, 7, 1);
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
         __nv_bfloat16* dst =
