@@ -18,14 +18,15 @@
 //              domain with lazy rescaling (O in TMEM is rescaled only when a
 //              row max grows by more than 2^8), writes P (bf16) to shared
 //              memory, final O / l to global;
-//   warps 4-6  loaders: gather the Q tile and each 128-key K/V tile from the
+//   warps 4-6  loaders: gather the Q tile and each 64-key K/V tile from the
 //              pages with cp.async (16 B per thread-op) into 128B-swizzled
-//              K-major tiles (the UMMA canonical layout), 2-stage ring;
+//              K-major tiles (the UMMA canonical layout), 5-stage ring
+//              (64-key tiles: a deep ring hides the gather latency);
 //              cp.async.mbarrier.arrive signals a stage without blocking the
 //              loader (the MMA thread fences the generic->async proxy);
 //   warp 7     TMEM allocation, and one lane issues every tcgen05.mma:
-//              S = Q·Kᵀ (M=128, N=128, K=head_dim) into one of two TMEM S
-//              buffers, O += P·V (M=128, N=head_dim, K=128; V used MN-major)
+//              S = Q·Kᵀ (M=128, N=64, K=head_dim) into one of two TMEM S
+//              buffers, O += P·V (M=128, N=head_dim, K=64; V used MN-major)
 //              into the TMEM O accumulator; completion reaches the other
 //              roles through tcgen05.commit on mbarriers.
 // S(t+1) is issued before P(t)·V(t), so the tensor core computes the next
@@ -71,7 +72,8 @@ __device__ __forceinline__ void k4_mark(unsigned* dbg, int slot, unsigned v) {
 template <int D>
 struct PfShape {
     static constexpr int kM = 128;            // MMA rows (packed token x head)
-    static constexpr int kN = 128;            // keys per K/V tile
+    static constexpr int kN = 64;             // keys per K/V tile
+    static constexpr int kStages = 5;         // K/V ring depth
     static constexpr int kSub = D / 64;       // 64-element (128 B) swizzle atoms along head_dim
     static constexpr int kQB = kM * D * 2;    // Q tile bytes
     static constexpr int kKB = kN * D * 2;    // K (or V) tile bytes
@@ -79,10 +81,10 @@ struct PfShape {
     static constexpr int kPB = kM * kN * 2;   // P tile bytes
     static constexpr int kOffQ = 0;
     static constexpr int kOffKV = kOffQ + kQB;
-    static constexpr int kOffP = kOffKV + 2 * kStageB;
+    static constexpr int kOffP = kOffKV + kStages * kStageB;
     static constexpr int kOffRows = kOffP + 2 * kPB;  // P double buffer; then [2][kN] K row offsets / 128 B
     static constexpr int kOffBar = kOffRows + 2 * kN * 4;
-    static constexpr int kBars = 12;
+    static constexpr int kBars = 2 * kStages + 8;
     static constexpr int kSmem = kOffBar + kBars * 8 + 16 + 1024;  // + TMEM address slot + alignment slack
     static constexpr int kThreads = 256;
     static constexpr int kLoaders = 96;   // warps 4-6
@@ -218,15 +220,19 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
     const std::uint32_t sKV = saddr(smem + S::kOffKV);
     const std::uint32_t sP = saddr(smem + S::kOffP);
     const std::uint32_t bar = saddr(smem + S::kOffBar);
-    const std::uint32_t b_q = bar, b_kvfull = bar + 8, b_kvempty = bar + 24, b_sfull = bar + 40,
-                        b_sfree = bar + 56, b_pfull = bar + 72, b_pvdone = bar + 80;
+    // mbarriers: q | kv_full[kStages] | kv_empty[kStages] | s_full[2] | s_free[2] | p_full | pv_done[2]
+    const std::uint32_t b_q = bar, b_kvfull = bar + 8, b_kvempty = b_kvfull + 8 * S::kStages,
+                        b_sfull = b_kvempty + 8 * S::kStages, b_sfree = b_sfull + 16, b_pfull = b_sfree + 16,
+                        b_pvdone = b_pfull + 8;
     std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(smem + S::kOffBar + S::kBars * 8);
 
     if (tid == 0) {
         mb_init(b_q, S::kLoaders);
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < S::kStages; ++s) {
             mb_init(b_kvfull + 8 * s, S::kLoaders);
             mb_init(b_kvempty + 8 * s, 1);
+        }
+        for (int s = 0; s < 2; ++s) {
             mb_init(b_sfull + 8 * s, 1);
             mb_init(b_sfree + 8 * s, 128);
         }
@@ -294,16 +300,16 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
         store_offs(0, load_sid(0, lt), load_sid(0, lt + S::kLoaders));
         asm volatile("bar.sync 2, %0;\n" ::"n"(S::kLoaders) : "memory");
         for (int t = 0; t < n_tiles; ++t) {
-            const int s = t & 1;
+            const int s = t % S::kStages;
             std::int32_t n0 = -1, n1 = -1;
             if (t + 1 < n_tiles) {
                 n0 = load_sid(t + 1, lt);
                 n1 = load_sid(t + 1, lt + S::kLoaders);
             }
-            if (t >= 2) mb_wait(b_kvempty + 8 * s, ((t >> 1) - 1) & 1);
+            if (t >= S::kStages) mb_wait(b_kvempty + 8 * s, ((t / S::kStages) - 1) & 1);
             unsigned char* kt = smem + S::kOffKV + s * S::kStageB;
             unsigned char* vt = kt + S::kKB;
-            const std::uint32_t* to = offs + s * S::kN;
+            const std::uint32_t* to = offs + (t & 1) * S::kN;
             for (int r = r0; r < S::kN; r += kRowsPerPass) {
                 const std::uint32_t off = to[r];
                 const char* srck = base;
@@ -331,16 +337,17 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
             fence_proxy_async();  // cp.async (generic proxy) data -> tcgen05.mma (async proxy)
             k4_mark(a.dbg, 2, 1);
             auto issue_s = [&](int t) {
-                const int s = t & 1;
-                mb_wait(b_kvfull + 8 * s, (t >> 1) & 1);
+                const int s = t & 1, ks = t % S::kStages;  // S buffer, K/V stage
+                mb_wait(b_kvfull + 8 * ks, (t / S::kStages) & 1);
                 if (t >= 2) mb_wait(b_sfree + 8 * s, ((t >> 1) - 1) & 1);
                 fence_proxy_async();
                 tc_fence_after();
-                const std::uint32_t kt = sKV + s * S::kStageB;
+                const std::uint32_t kt = sKV + ks * S::kStageB;
 #pragma unroll
                 for (int k = 0; k < D / 16; ++k) {
-                    const std::uint32_t off = (k >> 2) * (128 * 128) + (k & 3) * 32;
-                    tc_mma(tmem + s * 128, sw128_desc(sQ + off, 16), sw128_desc(kt + off, 16), idesc_s, k > 0);
+                    const std::uint32_t offq = (k >> 2) * (S::kM * 128) + (k & 3) * 32;
+                    const std::uint32_t offk = (k >> 2) * (S::kN * 128) + (k & 3) * 32;
+                    tc_mma(tmem + s * S::kN, sw128_desc(sQ + offq, 16), sw128_desc(kt + offk, 16), idesc_s, k > 0);
                 }
                 tc_commit(b_sfull + 8 * s);
                 k4_mark(a.dbg, 3, 100 + t);
@@ -350,15 +357,15 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
                 if (t + 1 < n_tiles) issue_s(t + 1);
                 mb_wait(b_pfull, t & 1);
                 tc_fence_after();
-                const std::uint32_t vt = sKV + (t & 1) * S::kStageB + S::kKB;
+                const std::uint32_t vt = sKV + (t % S::kStages) * S::kStageB + S::kKB;
 #pragma unroll
                 for (int k = 0; k < S::kN / 16; ++k) {
-                    const std::uint32_t poff = (k >> 2) * (128 * 128) + (k & 3) * 32;
+                    const std::uint32_t poff = (k >> 2) * (S::kM * 128) + (k & 3) * 32;
                     tc_mma(tmem + S::kColO, sw128_desc(sP + (t & 1) * S::kPB + poff, 16), sw128_desc(vt + k * 2048, S::kN * 128),
                            idesc_o, (t > 0 || k > 0) ? 1u : 0u);
                 }
                 tc_commit(b_pvdone + 8 * (t & 1));
-                tc_commit(b_kvempty + 8 * (t & 1));
+                tc_commit(b_kvempty + 8 * (t % S::kStages));
                 k4_mark(a.dbg, 4, 100 + t);
             }
         }
@@ -383,7 +390,7 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
             mb_wait(b_sfull + 8 * s, (t >> 1) & 1);
             tc_fence_after();
             if (r == 0) k4_mark(a.dbg, 5, 100 + t);
-            const std::uint32_t ts = tmem + lane_base + s * 128;
+            const std::uint32_t ts = tmem + lane_base + s * S::kN;
             const int k0 = t * S::kN;
             // pass 1: row max of this tile (scaled, log2 domain)
             // (8 independent partial maxima / sums: one warp per scheduler, so
@@ -395,7 +402,7 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
+            for (int cc = 0; cc < S::kN / 32; ++cc) {
                 float v[32];
                 tc_ld32(ts + cc * 32, v);
                 if (full) {
@@ -427,7 +434,7 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
 #pragma unroll
             for (int j = 0; j < 8; ++j) ls[j] = 0.f;
 #pragma unroll
-            for (int cc = 0; cc < 4; ++cc) {
+            for (int cc = 0; cc < S::kN / 32; ++cc) {
                 float v[32];
                 tc_ld32(ts + cc * 32, v);
                 std::uint32_t pk[16];
