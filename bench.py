@@ -509,6 +509,72 @@ def page_map_summary(st, steps):
 # ---------------------------------------------------------------- CPU arm
 
 
+def prefill_c3(chunk=512, ctx=32768, every=8, reps=2, layers=8):
+    """K4 (chunked-prefill attention, tcgen05/TMEM) on BASELINE config 3's
+    shape: one llama3.1-8b request grown to 32K tokens by 512-token prefill
+    chunks (K1 + synthetic K2 each step). Every `every`-th chunk, K4 is timed
+    with CUDA events on the engine stream over reps x layers launches; FLOPs
+    are the causal ones, 4 * n_q * d * sum_i (first + i + 1). Tensor-bound:
+    reported against MEASURED_PEAKS.json bf16_tflops (burst figure, the
+    kernel is timed alone)."""
+    import torch
+
+    from paper_2505_04021_b200 import msim
+
+    dev = msim.Device(0)
+    spec = msim.ModelSpec.llm("c3-prefill", L, NQ, NKV, D, chunk_size=chunk)
+    gpu = msim.GpuState(0, ctx // 16 + 64)
+    gpu.ledger.attach_device(dev)
+    act = gpu.activate(spec)
+    gpu.finish_activation(act.engine_index)
+    eng = gpu.engine(act.engine_index)
+    eng.attach_device(max_step_tokens=chunk + 8)
+    eng.push(1, ctx, 2)
+    stream = torch.cuda.ExternalStream(dev.stream())
+    gen = torch.Generator(device="cuda").manual_seed(SEED)
+    q = (torch.randn((chunk, NQ, D), generator=gen, device="cuda")).to(torch.bfloat16)
+    o = torch.empty_like(q)
+    torch.cuda.synchronize()
+    scale = 1.0 / math.sqrt(D)
+    flops = ms = 0.0
+    launches = chunks = 0
+    while True:
+        eng.step()
+        eng.append_kv_synthetic(0, L, SEED)
+        n, first, _ = eng.prefill_info()
+        if n == 0:
+            break
+        if chunks % every == every - 1 or first + n >= ctx:
+            eng.prefill_attention(0, q.data_ptr(), o.data_ptr(), scale)  # warm
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record(stream)
+            for _ in range(reps):
+                for layer in range(layers):
+                    eng.prefill_attention(layer, q.data_ptr(), o.data_ptr(), scale)
+            e.record(stream)
+            e.synchronize()
+            ms += s.elapsed_time(e)
+            flops += reps * layers * 4.0 * NQ * D * sum(first + i + 1 for i in range(n))
+            launches += reps * layers
+        chunks += 1
+        if first + n >= ctx:
+            break
+    torch.cuda.synchronize()
+    achieved = flops / (ms / 1e3) / 1e12
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peak, src = float(json.load(f)["bf16_tflops"]), "measured (burst)"
+    except Exception:
+        peak, src = 2250.0, "nominal dense bf16"
+    return {"kernel": "k4_prefill (chunked-prefill paged attention, tcgen05.mma + TMEM)",
+            "workload": f"C3 shape: llama3.1-8b request prefilled in {chunk}-token chunks to {ctx} tokens; "
+                        f"K4 timed on every {every}th chunk x {layers} layers x {reps}",
+            "bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
+            "frac": round(achieved / peak, 4), "peak_source": src, "launches_timed": launches,
+            "mean_ms_per_launch": round(ms / max(launches, 1), 4),
+            "flops": "causal: 4 * n_q * head_dim * sum over queries of visible keys"}
+
+
 def cpu_arm(args, sample_seqs=8, sample_layers=4, ref_steps=4):
     """CPU path of the same step: reference engine::step (allocation half, the
     reference itself) + CPU paged attention port (all host threads) on a
@@ -595,6 +661,7 @@ def main():
     ap.add_argument("--impl", default="prism", choices=["prism", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-churn", action="store_true", help="skip the C2 page map/unmap measurement")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the C3 chunked-prefill (K4) measurement")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -628,6 +695,11 @@ def main():
                 res["cpu_baseline"] = cpu_arm(args)
             except Exception as e:  # reported, never substituted for the GPU number
                 res["cpu_baseline"] = {"error": str(e)}
+        if world == 1 and not args.no_prefill:
+            try:
+                res["prefill_c3"] = prefill_c3()
+            except Exception as e:
+                res["prefill_c3"] = {"error": str(e)}
         if world == 1 and not args.no_churn:
             try:
                 res["page_map_c2"] = page_churn_c2()
