@@ -20,7 +20,7 @@ NVFLAGS   := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -DPRISM_PRODUCT -
              --expt-relaxed-constexpr -Xptxas -v
 LDFLAGS   := -shared -Xlinker -Bsymbolic-functions -Xlinker --no-undefined -lcudart_static -lrt -ldl -lpthread
 
-HOST_SRCS := $(wildcard $(SRC)/host/*.cpp) $(SRC)/capi_host.cpp $(SRC)/capi_device.cpp
+HOST_SRCS := $(wildcard $(SRC)/host/*.cpp) $(SRC)/capi_host.cpp $(SRC)/capi_device.cpp $(SRC)/simcore.cpp
 CU_SRCS   := $(wildcard $(SRC)/cuda/*.cu)
 HOST_OBJS := $(patsubst $(SRC)/%.cpp,$(BUILD)/%.o,$(HOST_SRCS))
 CU_OBJS   := $(patsubst $(SRC)/%.cu,$(BUILD)/%.o,$(CU_SRCS))

@@ -575,6 +575,33 @@ def prefill_c3(chunk=512, ctx=32768, every=8, reps=2, layers=8):
             "flops": "causal: 4 * n_q * head_dim * sum over queries of visible keys"}
 
 
+def slo_c5(copies=6, horizon=240.0):
+    """BASELINE config 5 through simcore (include/msim/simcore.hpp, the
+    native discrete-event driver of SPEC.md:514-579): the 8 SURVEY §8d shapes
+    x 6 (48 models, real weight sizes), per-minute rate segments alternating
+    r and 5r, on 1 / 2 / 4 / 8 B200-sized ledgers (85,830 pages each) under
+    the reference's cost model. Reports SLO attainment (TTFT and TPOT both met)
+    at SLO scales 1 / 2 / 4 and the driver's own speed (simulated engine
+    iterations per wall second, host C++)."""
+    from paper_2505_04021_b200 import msim
+    from paper_2505_04021_b200.configs import c5_case
+
+    models, prof = c5_case(copies=copies, horizon=horizon)
+    trace = msim.synth_trace(prof, TRACE_SEED)
+    out = {"workload": f"C5: {len(models)} models (SURVEY 8d shapes x {copies}), {horizon:.0f} s trace, "
+                       f"rate r / 5r alternating per minute, {len(trace)} requests; simcore, reference cost model",
+           "gpus": {}}
+    for n in (1, 2, 4, 8):
+        t0 = time.perf_counter()
+        r = msim.simulate(msim.SimConfig(n_gpus=n, capacity_pages=85_830), models, trace)
+        wall = time.perf_counter() - t0
+        out["gpus"][str(n)] = {"attainment": {str(k): round(r.attainment(k)["both"], 4) for k in (1, 2, 4)},
+                               "activations": r.summary["activations"], "evictions": r.summary["evictions"],
+                               "preemptions": r.summary["preemptions"],
+                               "sim_iterations_per_s": round(r.summary["iterations"] / wall, 1)}
+    return out
+
+
 def cpu_arm(args, sample_seqs=8, sample_layers=4, ref_steps=4):
     """CPU path of the same step: reference engine::step (allocation half, the
     reference itself) + CPU paged attention port (all host threads) on a
@@ -662,6 +689,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-churn", action="store_true", help="skip the C2 page map/unmap measurement")
     ap.add_argument("--no-prefill", action="store_true", help="skip the C3 chunked-prefill (K4) measurement")
+    ap.add_argument("--no-slo", action="store_true", help="skip the C5 SLO-attainment sweep (simcore)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -700,6 +728,11 @@ def main():
                 res["prefill_c3"] = prefill_c3()
             except Exception as e:
                 res["prefill_c3"] = {"error": str(e)}
+        if world == 1 and not args.no_slo:
+            try:
+                res["slo_c5"] = slo_c5()
+            except Exception as e:
+                res["slo_c5"] = {"error": str(e)}
         if world == 1 and not args.no_churn:
             try:
                 res["page_map_c2"] = page_churn_c2()

@@ -312,6 +312,50 @@ int prism_scale_trace(const prism_trace_event* in, size_t n_in, int factor, uint
 /* parse_trace_lines (workload.hpp:24) */
 int prism_parse_trace_text(const char* text, const char* origin, prism_trace_event* out, size_t cap, size_t* n);
 
+/* ------------------------------------------------------------------ simcore (msim/simcore.hpp)
+ * The deterministic discrete-event driver the reference specifies
+ * (SimMetrics / run / attainment) but does not implement:
+ * place_models at t=0, arrivals -> engine queues (activate_on_arrival for
+ * models without an engine), one engine::step at a time per GPU, eviction_tick
+ * every tick_s. Host-only; built into both the product and the reference
+ * oracle library (identical results are a parity test). */
+typedef struct prism_sim prism_sim;
+
+typedef struct {
+    int32_t n_gpus;
+    uint64_t capacity_pages, page_bytes; /* per GPU */
+    prism_engine_params params;
+    int32_t method; /* 0 naive, 1 parallel activation */
+    double tau_per_gb, tick_s, idle_evict_s, pressure_free_frac;
+    uint64_t buffer_target_pages;
+    int32_t initial_placement;
+    uint64_t max_events;
+} prism_sim_config;
+
+typedef struct {
+    int64_t end_us;
+    uint64_t events, iterations, activations, evictions, preemptions, output_tokens, n_requests, completed;
+    int32_t truncated;
+} prism_sim_summary;
+
+typedef struct {
+    uint64_t id; /* 1-based trace index */
+    int64_t arrival_us, first_token_us, completion_us; /* -1: never */
+    int32_t prompt_tokens, output_tokens, preemptions, gpu;
+} prism_sim_request;
+
+void prism_default_sim_config(prism_sim_config* out);
+/* rates[i]: demand of model i for the initial placement (may be NULL = 0). */
+int prism_sim_run(const prism_sim_config* cfg, const prism_model_spec* specs, const double* rates, size_t n_models,
+                  const prism_trace_event* trace, size_t n_trace, prism_sim** out);
+int prism_sim_summary_get(const prism_sim* s, prism_sim_summary* out);
+int prism_sim_requests(const prism_sim* s, prism_sim_request* out, size_t cap, size_t* n);
+int prism_sim_gpu_busy(const prism_sim* s, int64_t* out, size_t cap, size_t* n);
+/* TTFT / TPOT / both attainment at slo_scale for model_id (NULL or "" = all). */
+int prism_sim_attainment(const prism_sim* s, const char* model_id, double slo_scale, double* ttft, double* tpot,
+                         double* both, uint64_t* n);
+void prism_sim_free(prism_sim* s);
+
 /* ------------------------------------------------------------------ GPU data path (product only; no reference counterpart) */
 
 /* prism::VmmDevice on CUDA device `ordinal` (2 MiB pages). Physical memory

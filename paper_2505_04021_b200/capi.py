@@ -142,6 +142,25 @@ class TraceEvent(C.Structure):
                 ("output_tokens", c_int32)]
 
 
+class SimConfig(C.Structure):
+    _fields_ = [("n_gpus", c_int32), ("capacity_pages", c_uint64), ("page_bytes", c_uint64),
+                ("params", EngineParams), ("method", c_int32), ("tau_per_gb", c_double), ("tick_s", c_double),
+                ("idle_evict_s", c_double), ("pressure_free_frac", c_double), ("buffer_target_pages", c_uint64),
+                ("initial_placement", c_int32), ("max_events", c_uint64)]
+
+
+class SimSummary(C.Structure):
+    _fields_ = [("end_us", c_int64)] + [(n, c_uint64) for n in (
+        "events", "iterations", "activations", "evictions", "preemptions", "output_tokens", "n_requests",
+        "completed")] + [("truncated", c_int32)]
+
+
+class SimRequest(C.Structure):
+    _fields_ = [("id", c_uint64), ("arrival_us", c_int64), ("first_token_us", c_int64),
+                ("completion_us", c_int64), ("prompt_tokens", c_int32), ("output_tokens", c_int32),
+                ("preemptions", c_int32), ("gpu", c_int32)]
+
+
 class RateSegment(C.Structure):
     _fields_ = [("start_s", c_double), ("end_s", c_double), ("rate_per_s", c_double)]
 
@@ -237,6 +256,15 @@ _HOST_DECLS = {
     "prism_scale_trace": (c_int, [P(TraceEvent), c_size_t, c_int, c_uint64, c_double, P(TraceEvent), c_size_t,
                                   P(c_size_t)]),
     "prism_parse_trace_text": (c_int, [c_char_p, c_char_p, P(TraceEvent), c_size_t, P(c_size_t)]),
+    "prism_default_sim_config": (None, [P(SimConfig)]),
+    "prism_sim_run": (c_int, [P(SimConfig), P(ModelSpec), P(c_double), c_size_t, P(TraceEvent), c_size_t,
+                              P(c_void_p)]),
+    "prism_sim_summary_get": (c_int, [c_void_p, P(SimSummary)]),
+    "prism_sim_requests": (c_int, [c_void_p, P(SimRequest), c_size_t, P(c_size_t)]),
+    "prism_sim_gpu_busy": (c_int, [c_void_p, P(c_int64), c_size_t, P(c_size_t)]),
+    "prism_sim_attainment": (c_int, [c_void_p, c_char_p, c_double, P(c_double), P(c_double), P(c_double),
+                                     P(c_uint64)]),
+    "prism_sim_free": (None, [c_void_p]),
 }
 
 _DEVICE_DECLS = {

@@ -19,6 +19,7 @@
 #include "msim/errors.hpp"
 #include "msim/pagealloc.hpp"
 #include "msim/placement.hpp"
+#include "msim/simcore.hpp"
 #include "msim/workload.hpp"
 #include "prism_capi.h"
 #include "capi_handles.hpp"
@@ -28,6 +29,13 @@ namespace me = msim::engine;
 namespace pl = msim::placement;
 namespace ad = msim::admission;
 namespace wl = msim::workload;
+namespace sc = msim::simcore;
+
+// prism_sim: a finished simcore run (metrics + the models it ran, for SLOs)
+struct prism_sim {
+    sc::SimMetrics metrics;
+    std::vector<sc::ModelEntry> models;
+};
 
 namespace prism_capi_detail {
 
@@ -842,5 +850,123 @@ int prism_parse_trace_text(const char* text, const char* origin, prism_trace_eve
         emit_trace(wl::parse_trace_lines(text, origin ? origin : "<mem>"), out, cap, n);
     });
 }
+
+/* ------------------------------------------------------------------ simcore */
+
+void prism_default_sim_config(prism_sim_config* out) {
+    if (!out) return;
+    const sc::SimConfig d;
+    *out = prism_sim_config{};
+    out->n_gpus = d.n_gpus;
+    out->capacity_pages = d.capacity_pages;
+    out->page_bytes = d.page_bytes;
+    prism_default_engine_params(&out->params);
+    out->method = d.method == me::ActivationMethod::parallel ? 1 : 0;
+    out->tau_per_gb = d.tau_per_gb;
+    out->tick_s = d.tick_s;
+    out->idle_evict_s = d.idle_evict_s;
+    out->pressure_free_frac = d.pressure_free_frac;
+    out->buffer_target_pages = d.buffer_target_pages;
+    out->initial_placement = d.initial_placement ? 1 : 0;
+    out->max_events = d.max_events;
+}
+
+int prism_sim_run(const prism_sim_config* cfg, const prism_model_spec* specs, const double* rates, size_t n_models,
+                  const prism_trace_event* trace, size_t n_trace, prism_sim** out) {
+    return guard([&] {
+        need(cfg, "cfg");
+        need(out, "out");
+        if (n_models) need(specs, "specs");
+        if (n_trace) need(trace, "trace");
+        sc::SimConfig c;
+        c.n_gpus = cfg->n_gpus;
+        c.capacity_pages = cfg->capacity_pages;
+        c.page_bytes = cfg->page_bytes;
+        c.params = to_params(&cfg->params);
+        c.method = cfg->method ? me::ActivationMethod::parallel : me::ActivationMethod::naive;
+        c.tau_per_gb = cfg->tau_per_gb;
+        c.tick_s = cfg->tick_s;
+        c.idle_evict_s = cfg->idle_evict_s;
+        c.pressure_free_frac = cfg->pressure_free_frac;
+        c.buffer_target_pages = cfg->buffer_target_pages;
+        c.initial_placement = cfg->initial_placement != 0;
+        c.max_events = cfg->max_events;
+        auto sim = std::make_unique<prism_sim>();
+        for (std::size_t i = 0; i < n_models; ++i) {
+            sc::ModelEntry m;
+            m.spec = to_spec(specs[i]);
+            m.rate = rates ? rates[i] : 0.0;
+            sim->models.push_back(std::move(m));
+        }
+        std::vector<wl::TraceEvent> t;
+        t.reserve(n_trace);
+        for (std::size_t i = 0; i < n_trace; ++i) {
+            t.push_back(wl::TraceEvent{trace[i].arrival_s, trace[i].model_id, trace[i].prompt_tokens,
+                                       trace[i].output_tokens});
+        }
+        sim->metrics = sc::run(c, sim->models, t);
+        *out = sim.release();
+    });
+}
+
+int prism_sim_summary_get(const prism_sim* s, prism_sim_summary* out) {
+    return guard([&] {
+        need(s, "sim");
+        need(out, "out");
+        const sc::SimMetrics& m = s->metrics;
+        *out = prism_sim_summary{};
+        out->end_us = m.end_us;
+        out->events = m.events;
+        out->iterations = m.iterations;
+        out->activations = m.activations;
+        out->evictions = m.evictions;
+        out->preemptions = m.preemptions;
+        out->output_tokens = m.output_tokens;
+        out->n_requests = m.requests.size();
+        for (const auto& r : m.requests) out->completed += r.completion_us >= 0;
+        out->truncated = m.truncated ? 1 : 0;
+    });
+}
+
+int prism_sim_requests(const prism_sim* s, prism_sim_request* out, size_t cap, size_t* n) {
+    return guard([&] {
+        need(s, "sim");
+        const auto& rs = s->metrics.requests;
+        if (n) *n = rs.size();
+        if (!out) return;
+        room(rs.size(), cap, "requests");
+        for (std::size_t i = 0; i < rs.size(); ++i) {
+            out[i] = prism_sim_request{rs[i].id, rs[i].arrival_us, rs[i].first_token_us, rs[i].completion_us,
+                                       rs[i].prompt_tokens, rs[i].output_tokens, rs[i].preemptions, rs[i].gpu};
+        }
+    });
+}
+
+int prism_sim_gpu_busy(const prism_sim* s, int64_t* out, size_t cap, size_t* n) {
+    return guard([&] {
+        need(s, "sim");
+        const auto& b = s->metrics.gpu_busy_us;
+        if (n) *n = b.size();
+        if (!out) return;
+        room(b.size(), cap, "gpu_busy");
+        for (std::size_t i = 0; i < b.size(); ++i) out[i] = b[i];
+    });
+}
+
+int prism_sim_attainment(const prism_sim* s, const char* model_id, double slo_scale, double* ttft, double* tpot,
+                         double* both, uint64_t* n) {
+    return guard([&] {
+        need(s, "sim");
+        const auto a = sc::attainment(s->metrics, s->models, slo_scale);
+        const auto it = a.find(model_id ? model_id : "");
+        if (it == a.end()) throw std::invalid_argument("prism_sim_attainment: no requests for that model");
+        if (ttft) *ttft = it->second.ttft;
+        if (tpot) *tpot = it->second.tpot;
+        if (both) *both = it->second.both;
+        if (n) *n = it->second.n;
+    });
+}
+
+void prism_sim_free(prism_sim* s) { delete s; }
 
 }  // extern "C"

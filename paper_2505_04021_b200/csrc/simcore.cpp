@@ -1,0 +1,347 @@
+// prism-b200 — simcore (include/msim/simcore.hpp): the deterministic
+// discrete-event composition of engine::step, placement and the allocator
+// that the reference specifies but does not implement.
+// Only the public msim:: API is used, so this file also compiles against the
+// reference's headers and sources (oracle/Makefile): both builds must yield
+// identical metrics.
+#include "msim/simcore.hpp"
+
+#include <algorithm>
+#include <array>
+#include <deque>
+#include <map>
+#include <queue>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "msim/defaults.hpp"
+#include "msim/errors.hpp"
+#include "msim/placement.hpp"
+
+namespace msim::simcore {
+
+namespace {
+
+namespace me = msim::engine;
+namespace pl = msim::placement;
+
+enum Kind : int { kArrival = 0, kIterationDone = 1, kActivationDone = 2, kSchedulerTick = 3 };
+
+struct Event {
+    SimTime t;
+    int kind;
+    std::uint64_t seq;
+    std::int64_t a;  // arrival: trace index; iteration_done: gpu; activation_done: model index
+    bool operator>(const Event& o) const { return std::tie(t, kind, seq) > std::tie(o.t, o.kind, o.seq); }
+};
+
+struct ModelState {
+    int gpu = -1;       // GPU holding its engine (serving or loading), -1: none
+    int engine = -1;
+    bool loading = false;
+    std::deque<std::size_t> waiting;  // trace indices not yet in the engine queue
+    std::uint64_t outstanding = 0;    // arrived, not completed
+    SimTime idle_since = 0;           // last time outstanding dropped to 0
+};
+
+struct Gpu {
+    me::GpuState gs;
+    bool busy = false;
+    std::size_t rr = 0;  // next engine index the round robin looks at
+    Gpu(int id, std::uint64_t cap, std::uint64_t page) : gs(id, cap, page) {}
+};
+
+class Sim {
+public:
+    Sim(const SimConfig& cfg, const std::vector<ModelEntry>& models, const std::vector<workload::TraceEvent>& trace)
+        : cfg_(cfg), models_(models), trace_(trace) {
+        if (cfg.n_gpus < 1) throw UsageError("simcore: n_gpus must be >= 1");
+        if (cfg.capacity_pages == 0 || cfg.page_bytes == 0) throw UsageError("simcore: empty GPU");
+        for (std::size_t i = 0; i < models.size(); ++i) {
+            const auto& s = models[i].spec;
+            if (s.tp_degree != 1) throw UsageError("simcore: tp_degree != 1 is not supported: " + s.model_id);
+            const std::uint64_t wp = (s.weight_bytes + cfg.page_bytes - 1) / cfg.page_bytes;
+            if (wp >= cfg.capacity_pages) throw UsageError("simcore: model fits no GPU: " + s.model_id);
+            if (!index_.emplace(s.model_id, i).second) throw UsageError("simcore: duplicate model " + s.model_id);
+        }
+        for (const auto& ev : trace) {
+            if (!index_.count(ev.model_id)) throw UsageError("simcore: trace names an unknown model: " + ev.model_id);
+        }
+        for (int g = 0; g < cfg.n_gpus; ++g) gpus_.emplace_back(g, cfg.capacity_pages, cfg.page_bytes);
+        state_.resize(models.size());
+        m_.requests.resize(trace.size());
+        m_.gpu_busy_us.assign(static_cast<std::size_t>(cfg.n_gpus), 0);
+        for (std::size_t i = 0; i < trace.size(); ++i) {
+            RequestRecord& r = m_.requests[i];
+            r.id = i + 1;
+            r.model_id = trace[i].model_id;
+            r.arrival_us = seconds_to_us(trace[i].arrival_s);
+            r.prompt_tokens = trace[i].prompt_tokens;
+            r.output_tokens = trace[i].output_tokens;
+            push(r.arrival_us, kArrival, static_cast<std::int64_t>(i));
+        }
+    }
+
+    SimMetrics run() {
+        if (cfg_.initial_placement && !models_.empty()) place_all();
+        if (!trace_.empty()) push(seconds_to_us(cfg_.tick_s), kSchedulerTick, 0);
+        while (!q_.empty()) {
+            if (m_.events >= cfg_.max_events) {
+                m_.truncated = true;
+                break;
+            }
+            const Event ev = q_.top();
+            q_.pop();
+            ++m_.events;
+            now_ = ev.t;
+            m_.end_us = now_;
+            switch (ev.kind) {
+                case kArrival: on_arrival(static_cast<std::size_t>(ev.a)); break;
+                case kIterationDone: on_iteration_done(static_cast<int>(ev.a)); break;
+                case kActivationDone: on_activation_done(static_cast<std::size_t>(ev.a)); break;
+                case kSchedulerTick: on_tick(); break;
+            }
+        }
+        return std::move(m_);
+    }
+
+private:
+    void push(SimTime t, int kind, std::int64_t a) { q_.push(Event{t, kind, seq_++, a}); }
+
+    // ------------------------------------------------------------ views
+    std::vector<pl::GpuView> views() const {
+        std::vector<pl::GpuView> out;
+        for (const Gpu& g : gpus_) {
+            pl::GpuView v;
+            v.gpu_id = g.gs.gpu_id;
+            v.capacity_pages = g.gs.ledger.capacity_pages();
+            v.capacity_bytes = v.capacity_pages * cfg_.page_bytes;
+            v.free_pages = g.gs.ledger.free_pages();
+            v.page_bytes = cfg_.page_bytes;
+            for (std::size_t i = 0; i < models_.size(); ++i) {
+                const ModelState& s = state_[i];
+                if (s.gpu != v.gpu_id) continue;
+                const auto& spec = models_[i].spec;
+                pl::ResidentModel r;
+                r.idle_s = (s.outstanding == 0 && !s.loading) ? us_to_seconds(now_ - s.idle_since) : 0.0;
+                r.ttft_slo_s = spec.ttft_slo_s;
+                r.weight_bytes = spec.weight_bytes;
+                r.weight_pages = (spec.weight_bytes + cfg_.page_bytes - 1) / cfg_.page_bytes;
+                v.weight_bytes += spec.weight_bytes;
+                v.w_req_rate += models_[i].rate / spec.ttft_slo_s;
+                v.residents.emplace(spec.model_id, r);
+            }
+            out.push_back(std::move(v));
+        }
+        return out;
+    }
+
+    // ------------------------------------------------------------ activation
+    bool start_activation(std::size_t mi, int gpu) {
+        Gpu& g = gpus_[static_cast<std::size_t>(gpu)];
+        const auto act = me::activate(g.gs, models_[mi].spec, cfg_.method, cfg_.activation, cfg_.params);
+        if (!act) return false;
+        ModelState& s = state_[mi];
+        s.gpu = gpu;
+        s.engine = act->engine_index;
+        s.loading = true;
+        ++m_.activations;
+        push(now_ + act->total_us(), kActivationDone, static_cast<std::int64_t>(mi));
+        return true;
+    }
+
+    void place_all() {
+        std::vector<pl::ModelDemand> demand;
+        for (const ModelEntry& m : models_) {
+            pl::ModelDemand d;
+            d.spec = m.spec;
+            d.rate = m.rate;
+            demand.push_back(d);
+        }
+        pl::PlacementPlan plan;
+        try {
+            plan = pl::place_models(demand, views(), cfg_.tau_per_gb);
+        } catch (const pl::PlacementError&) {
+            return;  // not everything fits at once: models activate on arrival instead
+        }
+        for (std::size_t i = 0; i < models_.size(); ++i) {
+            const auto it = plan.assignment.find(models_[i].spec.model_id);
+            if (it == plan.assignment.end() || it->second.empty()) continue;
+            start_activation(i, it->second.front());
+        }
+    }
+
+    bool try_activate(std::size_t mi) {
+        const auto gpu = pl::activate_on_arrival(models_[mi].spec, views());
+        return gpu && start_activation(mi, *gpu);
+    }
+
+    void on_activation_done(std::size_t mi) {
+        ModelState& s = state_[mi];
+        Gpu& g = gpus_[static_cast<std::size_t>(s.gpu)];
+        me::finish_activation(g.gs, s.engine);
+        s.loading = false;
+        me::Engine& e = g.gs.engines[static_cast<std::size_t>(s.engine)];
+        while (!s.waiting.empty()) {
+            enqueue(e, s.waiting.front(), s.gpu);
+            s.waiting.pop_front();
+        }
+        wake(s.gpu);
+    }
+
+    // ------------------------------------------------------------ requests
+    void enqueue(me::Engine& e, std::size_t ti, int gpu) {
+        me::EngineRequest r;
+        r.id = ti + 1;
+        r.prompt_tokens = trace_[ti].prompt_tokens;
+        r.output_tokens = trace_[ti].output_tokens;
+        e.local_queue.push_back(std::move(r));
+        m_.requests[ti].gpu = gpu;
+    }
+
+    void on_arrival(std::size_t ti) {
+        const std::size_t mi = index_.at(trace_[ti].model_id);
+        ModelState& s = state_[mi];
+        ++s.outstanding;
+        if (s.gpu >= 0 && !s.loading) {
+            enqueue(gpus_[static_cast<std::size_t>(s.gpu)].gs.engines[static_cast<std::size_t>(s.engine)], ti, s.gpu);
+            wake(s.gpu);
+            return;
+        }
+        s.waiting.push_back(ti);
+        if (s.gpu < 0) try_activate(mi);
+    }
+
+    // ------------------------------------------------------------ iterations
+    void wake(int gpu) {
+        if (!gpus_[static_cast<std::size_t>(gpu)].busy) step_next(gpu);
+    }
+
+    void step_next(int gpu) {
+        Gpu& g = gpus_[static_cast<std::size_t>(gpu)];
+        const std::vector<pagealloc::PhysicalLedger*> ledgers{&g.gs.ledger};
+        const std::size_t n = g.gs.engines.size();
+        for (std::size_t k = 0; k < n; ++k) {
+            const std::size_t ei = (g.rr + k) % n;
+            me::Engine& e = g.gs.engines[ei];
+            if (!e.serving() || !e.has_runnable_work(ledgers)) continue;
+            const me::IterationOutcome o = me::step(e, ledgers, cfg_.params, now_);
+            const SimTime dur = std::max<SimTime>(o.duration_us, 1);
+            const SimTime end = now_ + dur;
+            for (std::uint64_t id : o.first_tokens) m_.requests[id - 1].first_token_us = end;
+            for (std::uint64_t id : o.preemptions) {
+                RequestRecord& r = m_.requests[id - 1];
+                r.first_token_us = -1;  // restarts from scratch
+                ++r.preemptions;
+                ++m_.preemptions;
+            }
+            for (std::uint64_t id : o.completions) {
+                RequestRecord& r = m_.requests[id - 1];
+                r.completion_us = end;
+                m_.output_tokens += static_cast<std::uint64_t>(r.output_tokens);
+                ModelState& s = state_[index_.at(r.model_id)];
+                if (--s.outstanding == 0) s.idle_since = end;
+            }
+            pagealloc::refill_buffer(g.gs.ledger, cfg_.buffer_target_pages);
+            ++m_.iterations;
+            m_.gpu_busy_us[static_cast<std::size_t>(gpu)] += dur;
+            g.rr = (ei + 1) % n;
+            g.busy = true;
+            push(end, kIterationDone, gpu);
+            return;
+        }
+        g.busy = false;
+    }
+
+    void on_iteration_done(int gpu) {
+        gpus_[static_cast<std::size_t>(gpu)].busy = false;
+        step_next(gpu);
+    }
+
+    // ------------------------------------------------------------ global tick
+    bool any_waiting() const {
+        for (const ModelState& s : state_) {
+            if (s.gpu < 0 && !s.waiting.empty()) return true;
+        }
+        return false;
+    }
+
+    void on_tick() {
+        const bool demand = any_waiting();
+        const double frac = cfg_.pressure_free_frac;
+        const auto pressured = [demand, frac](const pl::GpuView& v) {
+            return demand || static_cast<double>(v.free_pages) < frac * static_cast<double>(v.capacity_pages);
+        };
+        for (const pl::Eviction& ev : pl::eviction_tick(views(), cfg_.idle_evict_s, pressured)) {
+            const std::size_t mi = index_.at(ev.model_id);
+            ModelState& s = state_[mi];
+            Gpu& g = gpus_[static_cast<std::size_t>(s.gpu)];
+            me::Engine& e = g.gs.engines[static_cast<std::size_t>(s.engine)];
+            if (s.loading || !e.drained()) continue;
+            me::deactivate(g.gs, s.engine);
+            s.gpu = -1;
+            s.engine = -1;
+            ++m_.evictions;
+        }
+        for (std::size_t mi = 0; mi < models_.size(); ++mi) {
+            if (state_[mi].gpu < 0 && !state_[mi].waiting.empty()) try_activate(mi);
+        }
+        // keep ticking while requests are outstanding
+        bool open = false;
+        for (const ModelState& s : state_) open = open || s.outstanding > 0;
+        if (open || q_.size() > 0) push(now_ + seconds_to_us(cfg_.tick_s), kSchedulerTick, 0);
+    }
+
+    const SimConfig& cfg_;
+    const std::vector<ModelEntry>& models_;
+    const std::vector<workload::TraceEvent>& trace_;
+    std::map<std::string, std::size_t> index_;
+    std::vector<Gpu> gpus_;
+    std::vector<ModelState> state_;
+    std::priority_queue<Event, std::vector<Event>, std::greater<Event>> q_;
+    std::uint64_t seq_ = 0;
+    SimTime now_ = 0;
+    SimMetrics m_;
+};
+
+}  // namespace
+
+SimMetrics run(const SimConfig& cfg, const std::vector<ModelEntry>& models,
+               const std::vector<workload::TraceEvent>& trace) {
+    Sim sim(cfg, models, trace);
+    return sim.run();
+}
+
+std::map<std::string, Attainment> attainment(const SimMetrics& m, const std::vector<ModelEntry>& models,
+                                             double slo_scale) {
+    std::map<std::string, const engine::ModelSpec*> spec;
+    for (const ModelEntry& e : models) spec[e.spec.model_id] = &e.spec;
+    std::map<std::string, std::array<std::uint64_t, 4>> acc;  // n, ttft ok, tpot ok, both ok
+    for (const RequestRecord& r : m.requests) {
+        const engine::ModelSpec* s = spec.at(r.model_id);
+        bool ttft_ok = false, tpot_ok = false;
+        if (r.first_token_us >= 0 && r.completion_us >= 0) {
+            ttft_ok = us_to_seconds(r.first_token_us - r.arrival_us) <= slo_scale * s->ttft_slo_s;
+            const double tpot = r.output_tokens > 1
+                                    ? us_to_seconds(r.completion_us - r.first_token_us) / (r.output_tokens - 1)
+                                    : 0.0;
+            tpot_ok = tpot <= slo_scale * s->tpot_slo_s;
+        }
+        for (const std::string& key : {r.model_id, std::string()}) {
+            auto& a = acc[key];
+            a[0] += 1;
+            a[1] += ttft_ok;
+            a[2] += tpot_ok;
+            a[3] += ttft_ok && tpot_ok;
+        }
+    }
+    std::map<std::string, Attainment> out;
+    for (const auto& [k, a] : acc) {
+        const double n = static_cast<double>(a[0]);
+        out[k] = Attainment{a[0], a[1] / n, a[2] / n, a[3] / n};
+    }
+    return out;
+}
+
+}  // namespace msim::simcore

@@ -822,3 +822,78 @@ def parse_trace_lines(text: str, origin: str = "mem", lib=None) -> list:
     buf = (capi.TraceEvent * max(n.value, 1))()
     lib.call("prism_parse_trace_text", text.encode(), origin.encode(), buf, n.value, C.byref(n))
     return _events(buf, n.value)
+
+
+# ---------------------------------------------------------------- simcore
+
+
+@dataclass
+class SimConfig:
+    """msim::simcore::SimConfig (include/msim/simcore.hpp); defaults = the
+    reference's defaults.hpp (tick 10 s, idle eviction 10 s, pressure 10%,
+    tau 0.05, buffer 8 pages)."""
+
+    n_gpus: int = 1
+    capacity_pages: int = 0
+    page_bytes: int = 2 << 20
+    params: EngineParams = field(default_factory=EngineParams)
+    parallel_activation: bool = True
+    tau_per_gb: float = 0.05
+    tick_s: float = 10.0
+    idle_evict_s: float = 10.0
+    pressure_free_frac: float = 0.10
+    buffer_target_pages: int = 8
+    initial_placement: bool = True
+    max_events: int = 200_000_000
+
+
+class SimResult:
+    """A finished simcore run: summary, per-request records, attainment."""
+
+    def __init__(self, lib, h):
+        self.lib, self.h = lib, h
+        s = capi.SimSummary()
+        lib.call("prism_sim_summary_get", h, C.byref(s))
+        self.summary = {f: getattr(s, f) for f, _ in capi.SimSummary._fields_}
+        n = C.c_size_t()
+        lib.call("prism_sim_requests", h, None, 0, C.byref(n))
+        buf = (capi.SimRequest * max(n.value, 1))()
+        lib.call("prism_sim_requests", h, buf, n.value, C.byref(n))
+        self.requests = [{f: getattr(r, f) for f, _ in capi.SimRequest._fields_} for r in buf[:n.value]]
+        lib.call("prism_sim_gpu_busy", h, None, 0, C.byref(n))
+        busy = (C.c_int64 * max(n.value, 1))()
+        lib.call("prism_sim_gpu_busy", h, busy, n.value, C.byref(n))
+        self.gpu_busy_us = list(busy[:n.value])
+
+    def attainment(self, slo_scale: float = 1.0, model_id: str = "") -> dict:
+        t, p, b, n = C.c_double(), C.c_double(), C.c_double(), C.c_uint64()
+        self.lib.call("prism_sim_attainment", self.h, model_id.encode(), slo_scale, C.byref(t), C.byref(p),
+                      C.byref(b), C.byref(n))
+        return {"ttft": t.value, "tpot": p.value, "both": b.value, "n": n.value}
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.lib.dll.prism_sim_free(self.h)
+            self.h = None
+
+
+def simulate(cfg: SimConfig, models: Sequence, trace: Sequence[TraceEvent], lib=None) -> SimResult:
+    """msim::simcore::run. models: (ModelSpec, rate) pairs; rate = demand
+    for the initial placement."""
+    lib = _lib(lib)
+    c = capi.SimConfig()
+    lib.dll.prism_default_sim_config(C.byref(c))
+    c.n_gpus, c.capacity_pages, c.page_bytes = cfg.n_gpus, cfg.capacity_pages, cfg.page_bytes
+    c.params = cfg.params.to_c()
+    c.method = 1 if cfg.parallel_activation else 0
+    c.tau_per_gb, c.tick_s, c.idle_evict_s = cfg.tau_per_gb, cfg.tick_s, cfg.idle_evict_s
+    c.pressure_free_frac, c.buffer_target_pages = cfg.pressure_free_frac, cfg.buffer_target_pages
+    c.initial_placement, c.max_events = int(cfg.initial_placement), cfg.max_events
+    specs = (capi.ModelSpec * max(len(models), 1))(*[m[0].to_c() for m in models])
+    rates = (C.c_double * max(len(models), 1))(*[m[1] for m in models])
+    arr = (capi.TraceEvent * max(len(trace), 1))()
+    for i, e in enumerate(trace):
+        arr[i] = capi.TraceEvent(e.arrival_s, e.model_id.encode(), e.prompt_tokens, e.output_tokens)
+    h = C.c_void_p()
+    lib.call("prism_sim_run", C.byref(c), specs, rates, len(models), arr, len(trace), C.byref(h))
+    return SimResult(lib, h)

@@ -161,22 +161,7 @@ def allocator_known_answers(lib):
 
 # ---------------------------------------------------------------- engine
 
-SHAPES = {  # (L, n_q, n_kv, d, weight GB)
-    "qwen2.5-0.5b": (24, 14, 2, 64, 0.99),
-    "llama3.2-1b": (16, 32, 8, 64, 2.47),
-    "qwen2.5-1.5b": (28, 12, 2, 128, 3.09),
-    "qwen2.5-3b": (36, 16, 2, 128, 6.17),
-    "llama3.2-3b": (28, 24, 8, 128, 6.43),
-    "qwen2.5-7b": (28, 28, 4, 128, 15.23),
-    "mistral-7b": (32, 32, 8, 128, 14.5),
-    "llama3.1-8b": (32, 32, 8, 128, 16.06),
-}
-
-
-def shape_spec(name, model_id=None, chunk=512, weight_scale=1.0, ttft=1.0) -> msim.ModelSpec:
-    L, nq, nkv, d, wgb = SHAPES[name]
-    return msim.ModelSpec.llm(model_id or name, L, nq, nkv, d, weight_bytes=int(wgb * 1e9 * weight_scale),
-                              chunk_size=chunk, ttft_slo_s=ttft)
+from paper_2505_04021_b200.configs import SHAPES, shape_spec  # noqa: E402,F401 (shared with bench.py)
 
 
 ENGINE_CASES = [

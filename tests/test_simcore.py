@@ -1,0 +1,133 @@
+"""simcore (include/msim/simcore.hpp): the deterministic discrete-event driver
+the reference specifies but does not implement.
+
+Parity: simcore.cpp uses only the public msim:: API and is compiled into both
+the product library and the oracle library built from the reference's own
+sources (oracle/Makefile); the same configuration must give identical
+per-request records and counters on both. Properties from SPEC's simcore
+module: determinism, conservation (every request completes), causality
+(arrival <= first token <= completion, TTFT >= one prefill chunk), attainment
+in [0, 1], non-decreasing in the SLO scale and 1.0 as it grows without bound,
+and (on the config-5 shape) non-decreasing in the GPU count.
+"""
+import pytest
+
+from paper_2505_04021_b200 import msim
+from tests import scenarios as S
+
+from paper_2505_04021_b200.configs import B200_LEDGER_PAGES as LEDGER_PAGES, c5_case, slo_models as _models
+from paper_2505_04021_b200.configs import slo_of as _slo
+
+
+def _run(lib, n_gpus, models, trace, capacity=LEDGER_PAGES, **kw):
+    cfg = msim.SimConfig(n_gpus=n_gpus, capacity_pages=capacity, **kw)
+    return msim.simulate(cfg, models, trace, lib=lib)
+
+
+def _c1(lib):
+    specs = _models(1, ["llama3.1-8b"])
+    a, b = specs[0], S.shape_spec("llama3.1-8b", "llama3.1-8b#1", chunk=512, ttft=_slo("llama3.1-8b")[0])
+    b.tpot_slo_s = a.tpot_slo_s
+    prof = [msim.ModelProfile(s.model_id, [(0.0, 30.0, 6.0)], 1024.0, 0.3, 128.0, 0.4) for s in (a, b)]
+    return [(a, 6.0), (b, 6.0)], msim.synth_trace(prof, 42, lib=lib)
+
+
+def _c2(lib):
+    specs = _models(1)
+    prof = []
+    for i, s in enumerate(specs):
+        segs = [(t, t + 10.0, 3.0) for t in range(10 * (i % 2), 80, 20)]
+        prof.append(msim.ModelProfile(s.model_id, segs, 256.0, 0.6, 64.0, 0.6))
+    return [(s, 1.5) for s in specs], msim.synth_trace(prof, 42, lib=lib)
+
+
+def _c5(lib, copies=2, horizon=180.0):
+    models, prof = c5_case(copies=copies, horizon=horizon)
+    return models, msim.synth_trace(prof, 42, lib=lib)
+
+
+def _check_invariants(res, trace):
+    s = res.summary
+    assert not s["truncated"]
+    assert s["n_requests"] == len(trace) == s["completed"]
+    for r in res.requests:
+        assert r["arrival_us"] <= r["first_token_us"] <= r["completion_us"]
+        assert r["gpu"] >= 0
+    prev = None
+    for scale in (0.1, 0.5, 1.0, 2.0, 10.0, 1e9):
+        a = res.attainment(scale)
+        assert 0.0 <= a["both"] <= min(a["ttft"], a["tpot"]) <= 1.0
+        if prev:
+            assert a["ttft"] >= prev["ttft"] and a["tpot"] >= prev["tpot"] and a["both"] >= prev["both"]
+        prev = a
+    assert prev["both"] == 1.0
+
+
+@pytest.mark.parametrize("case", ["c1", "c2", "c5x2"])
+def test_product_matches_reference_build(product, reference, case):
+    """Same simcore source over the reference's engine / placement /
+    allocator vs over the product's: identical records and counters."""
+    if case == "c1":
+        models, trace = _c1(product)
+        runs = [_run(lib, 1, models, trace, capacity=18_000) for lib in (product, reference)]
+    elif case == "c2":
+        models, trace = _c2(product)
+        runs = [_run(lib, 1, models, trace, capacity=37_000) for lib in (product, reference)]
+    else:
+        models, trace = _c5(product, copies=2, horizon=120.0)
+        runs = [_run(lib, 2, models, trace, capacity=24_000) for lib in (product, reference)]
+    a, b = runs
+    assert a.summary == b.summary
+    assert a.requests == b.requests
+    assert a.gpu_busy_us == b.gpu_busy_us
+    for scale in (0.5, 1.0, 4.0):
+        assert a.attainment(scale) == b.attainment(scale)
+    _check_invariants(a, trace)
+
+
+def test_deterministic_and_conserving(product):
+    models, trace = _c2(product)
+    a = _run(product, 1, models, trace, capacity=37_000)
+    b = _run(product, 1, models, trace, capacity=37_000)
+    assert a.summary == b.summary and a.requests == b.requests
+    _check_invariants(a, trace)
+    # TTFT is at least one prefill chunk's modelled time (SPEC: TTFT >= p / c)
+    p = msim.EngineParams()
+    for r in a.requests:
+        first_chunk = min(r["prompt_tokens"], 512)
+        assert r["first_token_us"] - r["arrival_us"] >= int(p.alpha_ms * 1e3 + p.beta_ms_per_token * 1e3 * first_chunk) - 1
+
+
+def test_pressure_forces_eviction_and_reactivation(product):
+    """Config 5 on one GPU: the 16 models' weights exceed the ledger, so idle
+    models are evicted and re-activated on arrival; all requests still
+    complete."""
+    models, trace = _c5(product, copies=2, horizon=180.0)
+    weight_pages = sum((m.weight_bytes + (2 << 20) - 1) // (2 << 20) for m, _ in models)
+    cap = weight_pages // 2
+    res = _run(product, 1, models, trace, capacity=cap, idle_evict_s=5.0, tick_s=2.0)
+    _check_invariants(res, trace)
+    assert res.summary["evictions"] > 0
+    assert res.summary["activations"] > len({m.model_id for m, _ in models}) // 2
+
+
+def test_attainment_non_decreasing_in_gpu_count(product):
+    """SPEC sweep(gpu_count): prism's attainment is non-decreasing in the GPU
+    count (config-5 shape, 1 / 2 / 4 / 8 GPUs at the B200 ledger size)."""
+    models, trace = _c5(product, copies=6, horizon=120.0)
+    att = []
+    for n in (1, 2, 4, 8):
+        res = _run(product, n, models, trace)
+        _check_invariants(res, trace)
+        att.append(res.attainment(1.0)["both"])
+    assert all(b >= a - 1e-12 for a, b in zip(att, att[1:])), att
+
+
+def test_infeasible_config_raises(product):
+    big = S.shape_spec("llama3.1-8b", "huge", chunk=512)
+    big.weight_bytes = 400 << 30
+    with pytest.raises(msim.capi.UsageError):
+        _run(product, 1, [(big, 1.0)], [msim.TraceEvent(0.0, "huge", 10, 2)])
+    spec = S.shape_spec("llama3.1-8b", "m", chunk=512)
+    with pytest.raises(msim.capi.UsageError):
+        _run(product, 1, [(spec, 1.0)], [msim.TraceEvent(0.0, "unknown", 10, 2)])
