@@ -723,6 +723,11 @@ def main():
                 res["cpu_baseline"] = cpu_arm(args)
             except Exception as e:  # reported, never substituted for the GPU number
                 res["cpu_baseline"] = {"error": str(e)}
+        if world == 1 and not args.no_churn:
+            try:
+                res["page_map_c2"] = page_churn_c2()
+            except Exception as e:
+                res["page_map_c2"] = {"error": str(e)}
         if world == 1 and not args.no_prefill:
             try:
                 res["prefill_c3"] = prefill_c3()
@@ -733,11 +738,6 @@ def main():
                 res["slo_c5"] = slo_c5()
             except Exception as e:
                 res["slo_c5"] = {"error": str(e)}
-        if world == 1 and not args.no_churn:
-            try:
-                res["page_map_c2"] = page_churn_c2()
-            except Exception as e:
-                res["page_map_c2"] = {"error": str(e)}
         print(json.dumps(res))
     if world > 1:
         import torch.distributed as dist
