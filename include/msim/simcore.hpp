@@ -48,7 +48,19 @@ struct ModelEntry {
     double rate = 0.0;       // demand used by the initial placement (requests / s)
 };
 
+// Sharing policy ([MODULE] policies), same harness:
+//   prism            Algorithm 1 placement, arrival activation, idle eviction,
+//                    on-demand cross-model KV sharing through the ledger;
+//   mux_flexible     MuxServe stand-in: place_models once at t = 0 (all
+//                    models must fit), then frozen: no eviction, no arrival
+//                    activation; colocated models share KV on demand;
+//   static_partition the same frozen colocation, but each pool is hard-capped
+//                    (KvPool::set_mapped_page_cap) at an equal share of its
+//                    GPU's KV pages: no cross-model borrowing.
+enum class Policy { prism = 0, mux_flexible = 1, static_partition = 2 };
+
 struct SimConfig {
+    Policy policy = Policy::prism;
     int n_gpus = 1;
     std::uint64_t capacity_pages = 0;  // per GPU
     std::uint64_t page_bytes = 2ull << 20;

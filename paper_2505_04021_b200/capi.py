@@ -143,7 +143,7 @@ class TraceEvent(C.Structure):
 
 
 class SimConfig(C.Structure):
-    _fields_ = [("n_gpus", c_int32), ("capacity_pages", c_uint64), ("page_bytes", c_uint64),
+    _fields_ = [("policy", c_int32), ("n_gpus", c_int32), ("capacity_pages", c_uint64), ("page_bytes", c_uint64),
                 ("params", EngineParams), ("method", c_int32), ("tau_per_gb", c_double), ("tick_s", c_double),
                 ("idle_evict_s", c_double), ("pressure_free_frac", c_double), ("buffer_target_pages", c_uint64),
                 ("initial_placement", c_int32), ("max_events", c_uint64)]

@@ -857,6 +857,7 @@ void prism_default_sim_config(prism_sim_config* out) {
     if (!out) return;
     const sc::SimConfig d;
     *out = prism_sim_config{};
+    out->policy = static_cast<int32_t>(d.policy);
     out->n_gpus = d.n_gpus;
     out->capacity_pages = d.capacity_pages;
     out->page_bytes = d.page_bytes;
@@ -879,6 +880,8 @@ int prism_sim_run(const prism_sim_config* cfg, const prism_model_spec* specs, co
         if (n_models) need(specs, "specs");
         if (n_trace) need(trace, "trace");
         sc::SimConfig c;
+        if (cfg->policy < 0 || cfg->policy > 2) throw std::invalid_argument("prism_sim_run: unknown policy");
+        c.policy = static_cast<sc::Policy>(cfg->policy);
         c.n_gpus = cfg->n_gpus;
         c.capacity_pages = cfg->capacity_pages;
         c.page_bytes = cfg->page_bytes;

@@ -70,6 +70,7 @@ public:
         }
         for (int g = 0; g < cfg.n_gpus; ++g) gpus_.emplace_back(g, cfg.capacity_pages, cfg.page_bytes);
         state_.resize(models.size());
+        cap_pages_.assign(models.size(), 0);
         m_.requests.resize(trace.size());
         m_.gpu_busy_us.assign(static_cast<std::size_t>(cfg.n_gpus), 0);
         for (std::size_t i = 0; i < trace.size(); ++i) {
@@ -162,17 +163,43 @@ private:
         pl::PlacementPlan plan;
         try {
             plan = pl::place_models(demand, views(), cfg_.tau_per_gb);
-        } catch (const pl::PlacementError&) {
-            return;  // not everything fits at once: models activate on arrival instead
+        } catch (const pl::PlacementError& e) {
+            // prism: not everything fits at once, models activate on arrival;
+            // the frozen-colocation baselines need every model placed
+            if (frozen()) throw UsageError(std::string("simcore: policy needs all models placed: ") + e.what());
+            return;
         }
         for (std::size_t i = 0; i < models_.size(); ++i) {
             const auto it = plan.assignment.find(models_[i].spec.model_id);
             if (it == plan.assignment.end() || it->second.empty()) continue;
-            start_activation(i, it->second.front());
+            if (!start_activation(i, it->second.front()) && frozen()) {
+                throw UsageError("simcore: policy could not activate " + models_[i].spec.model_id);
+            }
+        }
+        if (cfg_.policy == Policy::static_partition) {
+            // equal share of each GPU's KV pages (capacity - weights - buffer)
+            for (Gpu& g : gpus_) {
+                std::uint64_t weights = 0, n = 0;
+                for (std::size_t i = 0; i < models_.size(); ++i) {
+                    if (state_[i].gpu != g.gs.gpu_id) continue;
+                    weights += (models_[i].spec.weight_bytes + cfg_.page_bytes - 1) / cfg_.page_bytes;
+                    ++n;
+                }
+                const std::uint64_t cap = g.gs.ledger.capacity_pages();
+                const std::uint64_t kv = cap > weights + cfg_.buffer_target_pages
+                                             ? cap - weights - cfg_.buffer_target_pages
+                                             : 0;
+                for (std::size_t i = 0; i < models_.size(); ++i) {
+                    if (state_[i].gpu == g.gs.gpu_id) cap_pages_[i] = n ? kv / n : 0;
+                }
+            }
         }
     }
 
+    bool frozen() const { return cfg_.policy != Policy::prism; }
+
     bool try_activate(std::size_t mi) {
+        if (frozen()) return false;  // frozen colocation: no arrival-triggered activation
         const auto gpu = pl::activate_on_arrival(models_[mi].spec, views());
         return gpu && start_activation(mi, *gpu);
     }
@@ -183,6 +210,7 @@ private:
         me::finish_activation(g.gs, s.engine);
         s.loading = false;
         me::Engine& e = g.gs.engines[static_cast<std::size_t>(s.engine)];
+        if (cfg_.policy == Policy::static_partition) e.pools.front().set_mapped_page_cap(cap_pages_[mi]);
         while (!s.waiting.empty()) {
             enqueue(e, s.waiting.front(), s.gpu);
             s.waiting.pop_front();
@@ -268,6 +296,12 @@ private:
     }
 
     void on_tick() {
+        if (frozen()) {  // no eviction, no activation: only keep ticking while work is open
+            bool open = false;
+            for (const ModelState& s : state_) open = open || s.outstanding > 0;
+            if (open) push(now_ + seconds_to_us(cfg_.tick_s), kSchedulerTick, 0);
+            return;
+        }
         const bool demand = any_waiting();
         const double frac = cfg_.pressure_free_frac;
         const auto pressured = [demand, frac](const pl::GpuView& v) {
@@ -299,6 +333,7 @@ private:
     std::map<std::string, std::size_t> index_;
     std::vector<Gpu> gpus_;
     std::vector<ModelState> state_;
+    std::vector<std::uint64_t> cap_pages_;  // static_partition: per-model mapped-page cap
     std::priority_queue<Event, std::vector<Event>, std::greater<Event>> q_;
     std::uint64_t seq_ = 0;
     SimTime now_ = 0;

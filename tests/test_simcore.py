@@ -131,3 +131,42 @@ def test_infeasible_config_raises(product):
     spec = S.shape_spec("llama3.1-8b", "m", chunk=512)
     with pytest.raises(msim.capi.UsageError):
         _run(product, 1, [(spec, 1.0)], [msim.TraceEvent(0.0, "unknown", 10, 2)])
+
+
+@pytest.mark.parametrize("policy", ["mux_flexible", "static_partition"])
+def test_baseline_policies_match_reference_build(product, reference, policy):
+    """SPEC policies module: the baselines run in the same harness; the
+    reference-source build agrees record for record."""
+    models, trace = _c2(product)
+    a, b = (_run(lib, 1, models, trace, capacity=37_000, policy=policy) for lib in (product, reference))
+    assert a.summary == b.summary and a.requests == b.requests
+    _check_invariants(a, trace)
+    assert a.summary["evictions"] == 0
+    assert a.summary["activations"] == len(models)  # frozen colocation: placed once
+
+
+def test_static_partition_cannot_borrow_idle_memory(product):
+    """SPEC §3.2 behaviour: two llama-8B-shaped models on one GPU, A idle,
+    B overloaded. static_partition caps B at half the KV pages (no borrowing)
+    -> more preemptions than mux_flexible (shares on demand); prism also
+    evicts the idle A under pressure and hands its weight pages to B."""
+    specs = _models(2, ["llama3.1-8b"])
+    a, b = specs
+    prof = [msim.ModelProfile(b.model_id, [(0.0, 40.0, 8.0)], 1500.0, 0.3, 200.0, 0.3)]
+    trace = msim.synth_trace(prof, 7, lib=product)
+    models = [(a, 1.0), (b, 8.0)]
+    runs = {p: _run(product, 1, models, trace, capacity=20_000, policy=p, tick_s=2.0, idle_evict_s=2.0)
+            for p in ("prism", "mux_flexible", "static_partition")}
+    for r in runs.values():
+        _check_invariants(r, trace)
+    assert runs["static_partition"].summary["preemptions"] > runs["mux_flexible"].summary["preemptions"]
+    assert runs["prism"].summary["evictions"] >= 1
+    for scale in (1.0, 4.0, 16.0):
+        att = {p: r.attainment(scale)["both"] for p, r in runs.items()}
+        assert att["prism"] > att["mux_flexible"] > att["static_partition"], (scale, att)
+
+
+def test_frozen_policy_needs_everything_placed(product):
+    models, trace = _c5(product, copies=6, horizon=60.0)
+    with pytest.raises(msim.capi.UsageError):
+        _run(product, 1, models, trace, policy="mux_flexible")
