@@ -72,24 +72,24 @@ __device__ __forceinline__ void k4_mark(unsigned* dbg, int slot, unsigned v) {
 template <int D>
 struct PfShape {
     static constexpr int kM = 128;            // MMA rows (packed token x head)
-    static constexpr int kN = 64;             // keys per K/V tile
-    static constexpr int kStages = 5;         // K/V ring depth
+    static constexpr int kN = 128;            // keys per K/V tile
+    static constexpr int kStages = 3;         // K/V ring depth
     static constexpr int kSub = D / 64;       // 64-element (128 B) swizzle atoms along head_dim
     static constexpr int kQB = kM * D * 2;    // Q tile bytes
     static constexpr int kKB = kN * D * 2;    // K (or V) tile bytes
     static constexpr int kStageB = 2 * kKB;   // K + V
-    static constexpr int kPB = kM * kN * 2;   // P tile bytes
     static constexpr int kOffQ = 0;
     static constexpr int kOffKV = kOffQ + kQB;
-    static constexpr int kOffP = kOffKV + kStages * kStageB;
-    static constexpr int kOffRows = kOffP + 2 * kPB;  // P double buffer; then [2][kN] K row offsets / 128 B
+    static constexpr int kOffRows = kOffKV + kStages * kStageB;  // [2][kN] K row offsets / 128 B (loaders)
     static constexpr int kOffBar = kOffRows + 2 * kN * 4;
     static constexpr int kBars = 2 * kStages + 8;
     static constexpr int kSmem = kOffBar + kBars * 8 + 16 + 1024;  // + TMEM address slot + alignment slack
     static constexpr int kThreads = 256;
     static constexpr int kLoaders = 96;   // warps 4-6
     static constexpr std::uint32_t kTmemCols = 512;  // S0 [0,128) S1 [128,256) O [256, 256+D)
-    static constexpr std::uint32_t kColO = 256;
+    // TMEM columns: S(t & 1) [kN each] | P(t & 1) [kN / 2 each: bf16 pairs] | O [D]
+    static constexpr std::uint32_t kColP = 2 * kN;
+    static constexpr std::uint32_t kColO = kColP + kN;
 };
 
 // ---------------------------------------------------------------- PTX helpers
@@ -173,6 +173,26 @@ __device__ __forceinline__ void tc_st32(std::uint32_t taddr, const float (&v)[32
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
 }
 
+// D[tmem] (+)= A[tmem] · B[smem]: the A operand (P) read from tensor memory,
+// lane = row, two bf16 K-elements per 32-bit column (8 columns per K=16 step)
+__device__ __forceinline__ void tc_mma_ts(std::uint32_t d_tmem, std::uint32_t a_tmem, std::uint64_t b_desc,
+                                          std::uint32_t idesc, std::uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// 16 consecutive 32-bit columns of this thread's TMEM lane (no wait)
+__device__ __forceinline__ void tc_st16_nowait(std::uint32_t taddr, const std::uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16};\n" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+        : "memory");
+}
+
 // Shared-memory matrix descriptor (sm_100 "version 1"), 128-byte swizzle.
 // K-major canonical layout ((8,m),(T,2)):((8T,SBO),(1,T)): rows of 128 B,
 // 8-row groups 1024 B apart (SBO), LBO unused (1). MN-major canonical layout
@@ -218,7 +238,6 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
 
     const std::uint32_t sQ = saddr(smem + S::kOffQ);
     const std::uint32_t sKV = saddr(smem + S::kOffKV);
-    const std::uint32_t sP = saddr(smem + S::kOffP);
     const std::uint32_t bar = saddr(smem + S::kOffBar);
     // mbarriers: q | kv_full[kStages] | kv_empty[kStages] | s_full[2] | s_free[2] | p_full | pv_done[2]
     const std::uint32_t b_q = bar, b_kvfull = bar + 8, b_kvempty = b_kvfull + 8 * S::kStages,
@@ -360,9 +379,8 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
                 const std::uint32_t vt = sKV + (t % S::kStages) * S::kStageB + S::kKB;
 #pragma unroll
                 for (int k = 0; k < S::kN / 16; ++k) {
-                    const std::uint32_t poff = (k >> 2) * (S::kM * 128) + (k & 3) * 32;
-                    tc_mma(tmem + S::kColO, sw128_desc(sP + (t & 1) * S::kPB + poff, 16), sw128_desc(vt + k * 2048, S::kN * 128),
-                           idesc_o, (t > 0 || k > 0) ? 1u : 0u);
+                    tc_mma_ts(tmem + S::kColO, tmem + S::kColP + (t & 1) * (S::kN / 2) + k * 8,
+                              sw128_desc(vt + k * 2048, S::kN * 128), idesc_o, (t > 0 || k > 0) ? 1u : 0u);
                 }
                 tc_commit(b_pvdone + 8 * (t & 1));
                 tc_commit(b_kvempty + 8 * (t % S::kStages));
@@ -449,13 +467,10 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
                     ls[(j >> 1) & 7] += p0 + p1;
                     pk[j >> 1] = pack_bf16(p0, p1);
                 }
-#pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    const int chunk = cc * 4 + q4;  // 16-byte chunk of the 256-byte P row
-                    unsigned char* dst = smem + S::kOffP + (t & 1) * S::kPB + sw_off<S::kM>(r, chunk);
-                    *reinterpret_cast<uint4*>(dst) = make_uint4(pk[q4 * 4], pk[q4 * 4 + 1], pk[q4 * 4 + 2], pk[q4 * 4 + 3]);
-                }
+                // P straight into tensor memory (the P·V MMA reads A from TMEM)
+                tc_st16_nowait(tmem + lane_base + S::kColP + (t & 1) * (S::kN / 2) + cc * 16, pk);
             }
+            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
             l_run += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
             tc_fence_before();
             mb_arrive(b_sfree + 8 * s);
@@ -473,7 +488,6 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
                     tc_st32(to, v);
                 }
             }
-            fence_proxy_async();
             tc_fence_before();
             mb_arrive(b_pfull);
             if (r == 0) k4_mark(a.dbg, 6, 100 + t);
