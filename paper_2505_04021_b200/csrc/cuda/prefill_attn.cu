@@ -58,8 +58,19 @@ struct PrefillArgs {
     int chunk;                // query tokens
     float scale_log2;
     float rescale_thr;        // lazy-rescale threshold (log2 units; 8)
+    unsigned long long* trace;  // PRISM_K4_TRACE: [5][1024] globaltimer stamps of CTA (0,0), else null
     unsigned* dbg;            // PRISM_K4_DEBUG: host-mapped progress words (CTA (0,0) only), else null
 };
+
+// timeline stamp (no-op unless PRISM_K4_TRACE): role 0 loader issued tile t,
+// 1 S(t) issued, 2 P(t)·V(t) issued, 3 softmax has S(t), 4 softmax posted P(t)
+__device__ __forceinline__ void k4_stamp(unsigned long long* tr, int role, int t) {
+    if (tr && blockIdx.x == 0 && blockIdx.y == 0 && t < 1024) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        tr[role * 1024 + t] = ns;
+    }
+}
 
 // progress marker for hang diagnosis (no-op unless PRISM_K4_DEBUG)
 __device__ __forceinline__ void k4_mark(unsigned* dbg, int slot, unsigned v) {
@@ -342,6 +353,7 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
             }
             cp_async_arrive(b_kvfull + 8 * s);
             if (lt == 0) k4_mark(a.dbg, 1, 100 + t);
+            if (lt == 0) k4_stamp(a.trace, 0, t);
             if (t + 1 < n_tiles) {
                 store_offs(t + 1, n0, n1);
                 asm volatile("bar.sync 2, %0;\n" ::"n"(S::kLoaders) : "memory");
@@ -370,6 +382,7 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
                 }
                 tc_commit(b_sfull + 8 * s);
                 k4_mark(a.dbg, 3, 100 + t);
+                k4_stamp(a.trace, 1, t);
             };
             issue_s(0);
             for (int t = 0; t < n_tiles; ++t) {
@@ -385,6 +398,7 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
                 tc_commit(b_pvdone + 8 * (t & 1));
                 tc_commit(b_kvempty + 8 * (t % S::kStages));
                 k4_mark(a.dbg, 4, 100 + t);
+                k4_stamp(a.trace, 2, t);
             }
         }
         __syncwarp();
@@ -408,6 +422,7 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
             mb_wait(b_sfull + 8 * s, (t >> 1) & 1);
             tc_fence_after();
             if (r == 0) k4_mark(a.dbg, 5, 100 + t);
+            if (r == 0) k4_stamp(a.trace, 3, t);
             const std::uint32_t ts = tmem + lane_base + s * S::kN;
             const int k0 = t * S::kN;
             // pass 1: row max of this tile (scaled, log2 domain)
@@ -491,6 +506,7 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
             tc_fence_before();
             mb_arrive(b_pfull);
             if (r == 0) k4_mark(a.dbg, 6, 100 + t);
+            if (r == 0) k4_stamp(a.trace, 4, t);
         }
         // epilogue: O / l -> bf16 -> out[token][h*G + g][:]
         ensure_pv(n_tiles - 1);
@@ -568,6 +584,27 @@ static unsigned* k4_debug_words() {
 
 // Progress words of the last K4 launch's CTA (0,0) (PRISM_K4_DEBUG), readable
 // while the kernel runs; 0 words when debugging is off.
+static unsigned long long* k4_trace_buf() {
+    static unsigned long long* dev = [] {
+        if (!std::getenv("PRISM_K4_TRACE")) return static_cast<unsigned long long*>(nullptr);
+        unsigned long long* p = nullptr;
+        PRISM_CUDA(cudaMalloc(&p, 5 * 1024 * sizeof(unsigned long long)));
+        PRISM_CUDA(cudaMemset(p, 0, 5 * 1024 * sizeof(unsigned long long)));
+        return p;
+    }();
+    return dev;
+}
+
+// Timeline of the last traced K4 launch (synchronous copy); 0 when off.
+int k4_trace_read(unsigned long long* out, int n) {
+    unsigned long long* d = k4_trace_buf();
+    if (!d) return 0;
+    const int m = n < 5 * 1024 ? n : 5 * 1024;
+    PRISM_CUDA(cudaDeviceSynchronize());
+    PRISM_CUDA(cudaMemcpy(out, d, m * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    return m;
+}
+
 int k4_debug_read(unsigned* out, int n) {
     if (!g_k4_dbg_host) return 0;
     const int m = n < 64 ? n : 64;
@@ -590,6 +627,7 @@ void launch_prefill_attention(EngineDeviceImpl& d, int layer, const void* q, voi
     a.chunk = d.prefill_chunk;
     a.scale_log2 = scale * 1.4426950408889634f;
     a.dbg = k4_debug_words();
+    a.trace = k4_trace_buf();
     static const float thr = [] {
         const char* e = std::getenv("PRISM_K4_RESCALE_THR");
         return e ? static_cast<float>(std::atof(e)) : 8.f;
