@@ -253,7 +253,9 @@ def gpu_arm(args, rank, world):
     import torch
     import torch.distributed as dist
 
-    torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
+    # PRISM_BENCH_DEVICE pins every rank to one device (validation of the
+    # multi-rank path on a single-GPU box; timings are then meaningless)
+    torch.cuda.set_device(int(os.environ.get("PRISM_BENCH_DEVICE", os.environ.get("LOCAL_RANK", 0))))
     steps, warm = args.steps, args.warmup
     mids = placement_for(world, rank)
     dev, gpu, models = setup_gpu(rank, mids, steps * 2 + warm * 2 + 8)
@@ -722,7 +724,8 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl")
+        # nccl; PRISM_BENCH_BACKEND=gloo for the single-GPU multi-rank validation
+        dist.init_process_group(os.environ.get("PRISM_BENCH_BACKEND", "nccl"))
     res = gpu_arm(args, rank, world)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
