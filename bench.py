@@ -602,7 +602,7 @@ def slo_c5(copies=6, horizon=240.0):
                                "preemptions": r.summary["preemptions"],
                                "sim_iterations_per_s": round(r.summary["iterations"] / wall, 1)}
         # SPEC policies: frozen-colocation baselines where all 48 models fit at once
-        for pol in ("mux_flexible", "static_partition"):
+        for pol in ("mux_flexible", "static_partition", "qlm_timeshare"):
             try:
                 b = msim.simulate(msim.SimConfig(n_gpus=n, capacity_pages=85_830, policy=pol), models, trace)
                 out["gpus"][str(n)][pol] = {str(k): round(b.attainment(k)["both"], 4) for k in (1, 2, 4)}

@@ -56,8 +56,13 @@ struct ModelEntry {
 //                    activation; colocated models share KV on demand;
 //   static_partition the same frozen colocation, but each pool is hard-capped
 //                    (KvPool::set_mapped_page_cap) at an equal share of its
-//                    GPU's KV pages: no cross-model borrowing.
-enum class Policy { prism = 0, mux_flexible = 1, static_partition = 2 };
+//                    GPU's KV pages: no cross-model borrowing;
+//   qlm_timeshare    QLM stand-in: one resident model per GPU; when a GPU's
+//                    resident model has drained, the oldest waiting request's
+//                    model is swapped in on the first such GPU (no residency
+//                    awareness) at stop-and-restart cost (engine init + naive
+//                    weight load).
+enum class Policy { prism = 0, mux_flexible = 1, static_partition = 2, qlm_timeshare = 3 };
 
 struct SimConfig {
     Policy policy = Policy::prism;

@@ -322,7 +322,7 @@ int prism_parse_trace_text(const char* text, const char* origin, prism_trace_eve
 typedef struct prism_sim prism_sim;
 
 typedef struct {
-    int32_t policy; /* 0 prism, 1 mux_flexible, 2 static_partition */
+    int32_t policy; /* 0 prism, 1 mux_flexible, 2 static_partition, 3 qlm_timeshare */
     int32_t n_gpus;
     uint64_t capacity_pages, page_bytes; /* per GPU */
     prism_engine_params params;

@@ -880,7 +880,7 @@ int prism_sim_run(const prism_sim_config* cfg, const prism_model_spec* specs, co
         if (n_models) need(specs, "specs");
         if (n_trace) need(trace, "trace");
         sc::SimConfig c;
-        if (cfg->policy < 0 || cfg->policy > 2) throw std::invalid_argument("prism_sim_run: unknown policy");
+        if (cfg->policy < 0 || cfg->policy > 3) throw std::invalid_argument("prism_sim_run: unknown policy");
         c.policy = static_cast<sc::Policy>(cfg->policy);
         c.n_gpus = cfg->n_gpus;
         c.capacity_pages = cfg->capacity_pages;

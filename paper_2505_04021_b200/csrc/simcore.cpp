@@ -85,7 +85,7 @@ public:
     }
 
     SimMetrics run() {
-        if (cfg_.initial_placement && !models_.empty()) place_all();
+        if (cfg_.initial_placement && !models_.empty() && cfg_.policy != Policy::qlm_timeshare) place_all();
         if (!trace_.empty()) push(seconds_to_us(cfg_.tick_s), kSchedulerTick, 0);
         while (!q_.empty()) {
             if (m_.events >= cfg_.max_events) {
@@ -238,7 +238,53 @@ private:
             return;
         }
         s.waiting.push_back(ti);
-        if (s.gpu < 0) try_activate(mi);
+        if (s.gpu < 0) {
+            if (cfg_.policy == Policy::qlm_timeshare) {
+                qlm_swap();
+            } else {
+                try_activate(mi);
+            }
+        }
+    }
+
+    // QLM time sharing: a GPU whose resident model has drained (or that has
+    // none) takes the model of the oldest waiting request, paying engine init
+    // + the naive weight load.
+    void qlm_swap() {
+        for (Gpu& g : gpus_) {
+            int res = -1;
+            for (std::size_t i = 0; i < models_.size(); ++i) {
+                if (state_[i].gpu == g.gs.gpu_id) res = static_cast<int>(i);
+            }
+            if (res >= 0 && (state_[res].loading || state_[res].outstanding > 0)) continue;
+            std::size_t best = models_.size(), oldest = 0;
+            for (std::size_t i = 0; i < models_.size(); ++i) {
+                const ModelState& c = state_[i];
+                if (c.gpu >= 0 || c.waiting.empty()) continue;
+                if (best == models_.size() || c.waiting.front() < oldest) {
+                    best = i;
+                    oldest = c.waiting.front();
+                }
+            }
+            if (best == models_.size()) return;
+            if (res >= 0) {
+                ModelState& r = state_[res];
+                me::deactivate(g.gs, r.engine);
+                r.gpu = -1;
+                r.engine = -1;
+                ++m_.evictions;
+            }
+            const auto act = me::activate(g.gs, models_[best].spec, me::ActivationMethod::naive, cfg_.activation,
+                                          cfg_.params);
+            if (!act) continue;
+            ModelState& s = state_[best];
+            s.gpu = g.gs.gpu_id;
+            s.engine = act->engine_index;
+            s.loading = true;
+            ++m_.activations;
+            const SimTime cost = seconds_to_us(cfg_.params.engine_init_s) + act->realign_us + act->load_us;
+            push(now_ + cost, kActivationDone, static_cast<std::int64_t>(best));
+        }
     }
 
     // ------------------------------------------------------------ iterations
@@ -285,6 +331,7 @@ private:
     void on_iteration_done(int gpu) {
         gpus_[static_cast<std::size_t>(gpu)].busy = false;
         step_next(gpu);
+        if (cfg_.policy == Policy::qlm_timeshare) qlm_swap();
     }
 
     // ------------------------------------------------------------ global tick

@@ -836,7 +836,7 @@ class SimConfig:
     n_gpus: int = 1
     capacity_pages: int = 0
     page_bytes: int = 2 << 20
-    policy: str = "prism"  # | "mux_flexible" | "static_partition"
+    policy: str = "prism"  # | "mux_flexible" | "static_partition" | "qlm_timeshare"
     params: EngineParams = field(default_factory=EngineParams)
     parallel_activation: bool = True
     tau_per_gb: float = 0.05
@@ -884,7 +884,7 @@ def simulate(cfg: SimConfig, models: Sequence, trace: Sequence[TraceEvent], lib=
     lib = _lib(lib)
     c = capi.SimConfig()
     lib.dll.prism_default_sim_config(C.byref(c))
-    c.policy = {"prism": 0, "mux_flexible": 1, "static_partition": 2}[cfg.policy]
+    c.policy = {"prism": 0, "mux_flexible": 1, "static_partition": 2, "qlm_timeshare": 3}[cfg.policy]
     c.n_gpus, c.capacity_pages, c.page_bytes = cfg.n_gpus, cfg.capacity_pages, cfg.page_bytes
     c.params = cfg.params.to_c()
     c.method = 1 if cfg.parallel_activation else 0

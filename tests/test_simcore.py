@@ -170,3 +170,25 @@ def test_frozen_policy_needs_everything_placed(product):
     models, trace = _c5(product, copies=6, horizon=60.0)
     with pytest.raises(msim.capi.UsageError):
         _run(product, 1, models, trace, policy="mux_flexible")
+
+
+def test_qlm_timeshare_swaps(product, reference):
+    """SPEC qlm_timeshare: alternating arrivals for two models on one GPU pay
+    a swap on every alternation; a single-model workload pays none beyond
+    the first load; the reference-source build agrees."""
+    specs = _models(1, ["llama3.1-8b", "qwen2.5-7b"])
+    alt = [msim.TraceEvent(2.0 + 30.0 * i, specs[i % 2].model_id, 200, 20) for i in range(6)]
+    models = [(s, 1.0) for s in specs]
+    a, b = (_run(lib, 1, models, alt, capacity=30_000, policy="qlm_timeshare") for lib in (product, reference))
+    assert a.summary == b.summary and a.requests == b.requests
+    _check_invariants(a, alt)
+    assert a.summary["activations"] == 6 and a.summary["evictions"] == 5
+    p = msim.EngineParams()
+    for r in a.requests:  # every request waits for a stop-and-restart activation
+        assert r["first_token_us"] - r["arrival_us"] >= int(p.engine_init_s * 1e6)
+    one = [msim.TraceEvent(2.0 + 30.0 * i, specs[0].model_id, 200, 20) for i in range(6)]
+    c = _run(product, 1, models, one, capacity=30_000, policy="qlm_timeshare")
+    assert c.summary["activations"] == 1 and c.summary["evictions"] == 0
+    # more GPUs with the same load: swaps do not decrease (SPEC, directional)
+    two = _run(product, 2, models, alt, capacity=30_000, policy="qlm_timeshare")
+    assert two.summary["activations"] >= 2
