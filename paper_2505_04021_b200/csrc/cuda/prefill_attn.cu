@@ -235,8 +235,9 @@ template <int D, int G>
 __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
     using S = PfShape<D>;
     extern __shared__ unsigned char smem_raw[];
-    unsigned char* smem = reinterpret_cast<unsigned char*>((reinterpret_cast<std::uintptr_t>(smem_raw) + 1023) &
-                                                           ~static_cast<std::uintptr_t>(1023));
+    // 1024-byte aligned base (SW128 atoms), derived by pointer arithmetic on
+    // the shared array so accesses through it stay LDS / STS
+    unsigned char* smem = smem_raw + ((1024u - (saddr(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int kTQ = S::kM / G;  // query tokens per tile
     const int h = blockIdx.y;       // kv head
