@@ -354,6 +354,7 @@ def gpu_arm(args, rank, world):
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_kind,
+                     "frac_of_nominal_8000": round(achieved / 8000.0, 4),
                      "kernel": "k3_decode (paged GQA decode attention)",
                      "k3_mean_ms": round(avg_ms, 5), "k3_bytes_per_launch": int(avg_bytes),
                      "k3_share_of_step": round(sum(k3_ms) * L / ms_total, 4)},
@@ -577,6 +578,60 @@ def prefill_c3(chunk=512, ctx=32768, every=8, reps=2, layers=8):
             "flops": "causal: 4 * n_q * head_dim * sum over queries of visible keys"}
 
 
+def decode_c3(batch=16, ctx=32768, reps=3):
+    """BASELINE config 3 decode: 16 requests x 32K context (llama3.1-8b KV
+    shape) grown by 8K-token prefill chunks, then K3 over all 32 layers,
+    timed with CUDA events around back-to-back launches (one step's PDL
+    chain). Algorithmic bytes as for C1 (K+V of every context token + q +
+    out); against the measured copy bandwidth."""
+    import torch
+
+    from paper_2505_04021_b200 import msim
+
+    dev = msim.Device(0)
+    gpu = msim.GpuState(0, batch * (ctx + 600) // 16 + 200)
+    gpu.ledger.attach_device(dev)
+    spec = msim.ModelSpec.llm("c3-decode", L, NQ, NKV, D, chunk_size=8192)
+    act = gpu.activate(spec)
+    gpu.finish_activation(act.engine_index)
+    eng = gpu.engine(act.engine_index)
+    eng.attach_device(max_step_tokens=8192 + batch + 8)
+    for i in range(batch):
+        eng.push(i + 1, ctx - 1, 1_000_000)
+    while eng.counts()[1] or any(r.prompt_done < r.prompt_tokens for r in eng.batch()):
+        eng.step()
+        eng.append_kv_synthetic(0, L, SEED)
+    eng.step()
+    eng.append_kv_synthetic(0, L, SEED)
+    stream = torch.cuda.ExternalStream(dev.stream())
+    q = torch.empty((L, batch, NQ, D), dtype=torch.bfloat16, device="cuda")
+    o = torch.empty_like(q)
+    for layer in range(L):
+        eng.synth_q(layer, SEED, 1.0, q[layer].data_ptr())
+    scale = 1.0 / math.sqrt(D)
+    for layer in range(L):  # warm
+        eng.decode_attention(layer, q[layer].data_ptr(), o[layer].data_ptr(), scale)
+    dev.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(reps):
+        for layer in range(L):
+            eng.decode_attention(layer, q[layer].data_ptr(), o[layer].data_ptr(), scale)
+    e.record(stream)
+    e.synchronize()
+    ms = s.elapsed_time(e) / (reps * L)
+    ctxs = [r.live_slots() for r in eng.batch()]
+    nbytes = sum(ctxs) * NKV * D * 2 * 2 + 2 * len(ctxs) * NQ * D * 2
+    peak, kind = measured_peaks()
+    gbs = nbytes / (ms / 1e3) / 1e9
+    return {"workload": f"C3: {batch} decodes x {ctx} ctx, llama3.1-8b KV shape, 32 K3 launches back to back",
+            "kernel": "k3_decode_streamk", "ms_per_launch": round(ms, 4), "bytes_per_launch": int(nbytes),
+            "achieved": round(gbs, 1), "peak": peak, "unit": "GB/s", "frac": round(gbs / peak, 4),
+            "peak_source": kind, "frac_of_nominal_8000": round(gbs / 8000.0, 4),
+            "note": "the measured peak is a device-to-device copy (read + write); a read-only stream can exceed it",
+            "decode_tokens_per_s": round(batch / (ms * L / 1e3), 1)}
+
+
 def slo_c5(copies=6, horizon=240.0):
     """BASELINE config 5 through simcore (include/msim/simcore.hpp, the
     native discrete-event driver of SPEC.md:514-579): the 8 SURVEY §8d shapes
@@ -739,6 +794,10 @@ def main():
             except Exception as e:
                 res["page_map_c2"] = {"error": str(e)}
         if world == 1 and not args.no_prefill:
+            try:
+                res["decode_c3"] = decode_c3()
+            except Exception as e:
+                res["decode_c3"] = {"error": str(e)}
             try:
                 res["prefill_c3"] = prefill_c3()
             except Exception as e:
