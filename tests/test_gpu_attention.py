@@ -278,3 +278,40 @@ def test_decode_host_buffers_match_device_path(product, device, use_async):
         for rid in out.completions:
             store.pop(rid, None)
     assert checked > 10
+
+
+def test_per_layer_append_then_attend_matches_batched(product, device):
+    """A model's real order is K2(layer l) then K3(layer l), layer by layer:
+    every K2 breaks the K3 programmatic-dependent chain, which must not change
+    any result. Two identical engines, one appending all layers first and
+    running the K3 chain, one interleaving per layer: bitwise equal outputs."""
+    outs = []
+    for interleave in (False, True):
+        gpu, spec, eng = _engine(product, device, "llama3.1-8b", chunk=256)
+        L, nkv, nq, d = spec.n_layers, spec.n_kv_heads, spec.n_q_heads, spec.head_dim
+        for i, p in enumerate([300, 70, 513, 129]):
+            eng.push(i + 1, p, 6)
+        gen = torch.Generator(device="cuda").manual_seed(11)
+        res = []
+        while sum(eng.counts()):
+            eng.step()
+            n_tok, n_dec = eng.step_info()
+            if n_tok == 0:
+                continue
+            k = (torch.rand((L, n_tok, nkv, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+            v = (torch.rand((L, n_tok, nkv, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+            q = (torch.rand((L, max(n_dec, 1), nq, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+            o = torch.zeros_like(q)
+            if not interleave:
+                eng.append_kv(0, L, k.data_ptr(), v.data_ptr())
+            for layer in range(L):
+                if interleave:
+                    eng.append_kv(layer, layer + 1, k[layer].data_ptr(), v[layer].data_ptr())
+                if n_dec:
+                    eng.decode_attention(layer, q[layer].data_ptr(), o[layer].data_ptr(), 1 / math.sqrt(d))
+            eng.synchronize()
+            res.append(o.cpu())
+        outs.append(res)
+    assert len(outs[0]) == len(outs[1]) > 5
+    for a, b in zip(*outs):
+        assert torch.equal(a.view(torch.int16), b.view(torch.int16))
