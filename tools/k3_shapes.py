@@ -17,7 +17,10 @@ peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspa
                                    "MEASURED_PEAKS.json")))["hbm_gbs"]
 dev = msim.Device(0)
 torch.cuda.set_stream(torch.cuda.ExternalStream(dev.stream()))
+ONLY = os.environ.get("SHAPES")
 for name, (L, nq, nkv, d, _) in SHAPES.items():
+    if ONLY and name not in ONLY.split(","):
+        continue
     spec = shape_spec(name, name, chunk=8192, weight_scale=0.0)
     tpp = (2 << 20) // spec.token_kv_bytes
     gpu = msim.GpuState(0, B * (CTX + 64) // tpp + 400)
