@@ -447,6 +447,9 @@ int prism_debug_k4_progress(uint32_t* out, int32_t n, int32_t* got);
 /* Diagnostics: timeline of the last K4 launch's CTA (0,0) (PRISM_K4_TRACE=1): [5][1024] globaltimer ns
  * (loader tile issued, S issued, P·V issued, softmax has S, softmax posted P). */
 int prism_debug_k4_trace(uint64_t* out, int32_t n, int32_t* got);
+/* Diagnostics: per-CTA stamps of the last K3 launch (PRISM_K3_TRACE=1): [grid][8] globaltimer ns
+ * (running, prologue issued, after the PDL wait, first tile, last tile, done, tiles). */
+int prism_debug_k3_trace(uint64_t* out, int32_t n, int32_t* got);
 int prism_engine_synth_q(prism_gpu* g, int engine_index, int layer, uint64_t seed, float q_scale, void* q);
 /* End-to-end: the same attention with HOST buffers (pinned or pageable);
  * copies q in, runs K2 for new_k/new_v (host, may be null) over all layers

@@ -296,6 +296,7 @@ _DEVICE_DECLS = {
     "prism_engine_prefill_attention": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_float]),
     "prism_debug_k4_progress": (c_int, [P(c_uint32), c_int32, P(c_int32)]),
     "prism_debug_k4_trace": (c_int, [P(c_uint64), c_int32, P(c_int32)]),
+    "prism_debug_k3_trace": (c_int, [P(c_uint64), c_int32, P(c_int32)]),
     "prism_engine_synth_q": (c_int, [c_void_p, c_int, c_int, c_uint64, c_float, c_void_p]),
     "prism_set_attention_variant": (c_int, [c_int]),
     "prism_engine_decode_host": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_float]),

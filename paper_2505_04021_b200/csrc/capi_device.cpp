@@ -296,6 +296,7 @@ namespace prism {
 void launch_decode_attention(class EngineDeviceImpl& d, int layer, const void* q, void* out, float scale, int chunk);
 int k4_debug_read(unsigned* out, int n);
 int k4_trace_read(unsigned long long* out, int n);
+int k3_trace_read(unsigned long long* out, int n);
 EngineDeviceImpl& impl_of(const msim::engine::Engine& eng);
 void set_attention_variant(int v);
 }  // namespace prism
@@ -333,6 +334,14 @@ int prism_debug_k4_progress(uint32_t* out, int32_t n, int32_t* got) {
     return dguard([&] {
         need(out, "out");
         const int m = prism::k4_debug_read(out, n);
+        if (got) *got = m;
+    });
+}
+
+int prism_debug_k3_trace(uint64_t* out, int32_t n, int32_t* got) {
+    return dguard([&] {
+        need(out, "out");
+        const int m = prism::k3_trace_read(reinterpret_cast<unsigned long long*>(out), n);
         if (got) *got = m;
     });
 }

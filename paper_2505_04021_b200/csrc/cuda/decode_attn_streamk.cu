@@ -51,7 +51,16 @@ struct SkArgs {
     int total_tiles;
     int per_cta;                      // W
     int max_parts;                    // partial slots per pair
+    unsigned long long* trace;        // PRISM_K3_TRACE: [grid][8] globaltimer stamps, else null
 };
+
+__device__ __forceinline__ void k3_stamp(unsigned long long* tr, int k) {
+    if (tr && threadIdx.x == 0) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        tr[blockIdx.x * 8 + k] = ns;
+    }
+}
 
 template <int D>
 __device__ __forceinline__ int swz_sk(int row, int chunk) {
@@ -74,6 +83,7 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
     const int g_begin = blockIdx.x * sk.per_cta;
     const int g_end = min(sk.total_tiles, g_begin + sk.per_cta);
     if (g_begin >= g_end) return;
+    k3_stamp(sk.trace, 0);  // CTA running
 
     // first pair of the range: largest p with T[p] <= g_begin
     auto pair_of = [&](int g) {
@@ -314,8 +324,10 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
     // descriptors, tile prefix, K/V pages — see EngineDeviceImpl::k3_chain),
     // so it overlaps that kernel's tail. q, out and the split-K workspace
     // (shared with the previous K3) are touched only after it completed.
+    k3_stamp(sk.trace, 1);  // prologue copies issued
     asm volatile("griddepcontrol.wait;\n" ::: "memory");
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    k3_stamp(sk.trace, 2);  // previous kernel complete
     ctx = a.desc[cp / n_kv].ctx;
     start_pair();
     const int wrow = warp * 16;
@@ -393,6 +405,8 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
                 mma_bf16_16816(o[mt], af, pb0, pb1);
             }
         }
+        if (g == g_begin) k3_stamp(sk.trace, 3);  // first tile computed
+        if (g + 1 == g_end) k3_stamp(sk.trace, 4);  // last tile computed
         // end of this pair's segment inside the range?
         if (g + 1 == cp_end || g + 1 == g_end) {
             finish_pair(cp_first);
@@ -406,6 +420,8 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
         }
     }
     cp_async_wait<0>();
+    k3_stamp(sk.trace, 5);  // done (incl. the last pair's merge)
+    if (sk.trace && threadIdx.x == 0) sk.trace[blockIdx.x * 8 + 6] = static_cast<unsigned long long>(g_end - g_begin);
 }
 
 template <int D, int G>
@@ -482,6 +498,18 @@ void launch_sk_d(int group, const SkArgs& s, cudaStream_t stream, int sms, bool 
 
 // Host side of the stream-K launch. The pair-tile prefix depends only on the
 // step's decode descriptors, so it is rebuilt once per step (not per layer).
+static unsigned long long* g_k3_trace = nullptr;
+
+// stamps of the last traced K3 launch: [grid][8] (0 running, 1 prologue issued,
+// 2 after griddepcontrol.wait, 3 first tile, 4 last tile, 5 done, 6 tiles)
+int k3_trace_read(unsigned long long* out, int n) {
+    if (!g_k3_trace) return 0;
+    const int m = n < 4096 * 8 ? n : 4096 * 8;
+    PRISM_CUDA(cudaDeviceSynchronize());
+    PRISM_CUDA(cudaMemcpy(out, g_k3_trace, m * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    return m;
+}
+
 void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec) {
     constexpr int kT = 64;
     static int sms = [] {
@@ -526,7 +554,15 @@ void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec) {
         for (int b = 0; b < n_dec; ++b) max_tiles = std::max(max_tiles, (d.decode_desc.host[b].ctx + kT - 1) / kT);
         d.sk_max_parts = (max_tiles + d.sk_per_cta - 1) / d.sk_per_cta + 1;
     }
+    static unsigned long long* trace = [] {
+        if (!std::getenv("PRISM_K3_TRACE")) return static_cast<unsigned long long*>(nullptr);
+        unsigned long long* p = nullptr;
+        PRISM_CUDA(cudaMalloc(&p, 4096 * 8 * sizeof(unsigned long long)));
+        return p;
+    }();
+    g_k3_trace = trace;
     SkArgs s{};
+    s.trace = trace;
     s.a = a;
     s.pair_tiles = d.sk_prefix.dev;
     s.n_pairs = n_pairs;
