@@ -219,7 +219,6 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
     float* red_o = reinterpret_cast<float*>(smem + S::kRingB);  // [warps][G][D]
     float* red_m = red_o + S::kWarps * G * D;                  // [warps][8]
     float* red_l = red_m + S::kWarps * 8;                      // [warps][8]
-    __shared__ int s_last;
 
     // finish pair cp: merge warps, write out or a partial (+ merge if last)
     auto finish_pair = [&](int seg_first) {
@@ -256,7 +255,18 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
         const int part = blockIdx.x - first_cta;
         __nv_bfloat16* out = a.out + (static_cast<std::size_t>(b) * n_q + static_cast<std::size_t>(h) * G) * D;
         const std::size_t pslot = static_cast<std::size_t>(cp) * sk.max_parts + part;
-        for (int idx = tid; idx < G * D; idx += S::kThreads) {
+        // A cut pair is merged by its FIRST CTA (part 0): that CTA reaches the
+        // pair at the end of its range, after the later parts (computed at
+        // the start of the next CTAs' ranges) were published. It keeps its
+        // own (m, l, O) in registers, waits for the ticket to count the other
+        // parts (almost never an actual wait) and combines; the other parts
+        // write a partial, fence once and bump the ticket.
+        constexpr int kPer = (G * D + S::kThreads - 1) / S::kThreads;
+        float own_m[kPer], own_l[kPer], own_o[kPer];
+#pragma unroll
+        for (int k = 0; k < kPer; ++k) {
+            const int idx = tid + k * S::kThreads;
+            if (idx >= G * D) break;
             const int g = idx / D, d = idx % D;
             float mm = -INFINITY;
 #pragma unroll
@@ -269,9 +279,12 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
                 ll += red_l[w * 8 + g] * f;
                 oo += red_o[(w * G + g) * D + d] * f;
             }
+            own_m[k] = mm;
+            own_l[k] = ll;
+            own_o[k] = oo;
             if (parts == 1) {
                 out[idx] = __float2bfloat16_rn(oo / ll);
-            } else {
+            } else if (part > 0) {
                 a.part_o[pslot * G * D + idx] = oo;
                 if (d == 0) {
                     a.part_ml[(pslot * G + g) * 2] = mm;
@@ -279,28 +292,39 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
                 }
             }
         }
-        if (parts > 1) {
-            __threadfence();
-            __syncthreads();
-            if (tid == 0) s_last = atomicAdd(&a.tickets[cp], 1) == parts - 1;
-            __syncthreads();
-            if (s_last) {
+        if (parts > 1 && part > 0) {
+            __syncthreads();  // all of this CTA's partial stores precede the fence
+            if (tid == 0) {
                 __threadfence();
-                const std::size_t p0 = static_cast<std::size_t>(cp) * sk.max_parts;
-                for (int idx = tid; idx < G * D; idx += S::kThreads) {
-                    const int g = idx / D;
-                    float mm = -INFINITY;
-                    for (int sp = 0; sp < parts; ++sp) mm = fmaxf(mm, __ldcg(&a.part_ml[((p0 + sp) * G + g) * 2]));
-                    float ll = 0.f, oo = 0.f;
-                    for (int sp = 0; sp < parts; ++sp) {
-                        const float f = fast_exp2(__ldcg(&a.part_ml[((p0 + sp) * G + g) * 2]) - mm);
-                        ll += __ldcg(&a.part_ml[((p0 + sp) * G + g) * 2 + 1]) * f;
-                        oo += __ldcg(&a.part_o[(p0 + sp) * G * D + idx]) * f;
-                    }
-                    out[idx] = __float2bfloat16_rn(oo / ll);
-                }
-                if (tid == 0) a.tickets[cp] = 0;
+                atomicAdd(&a.tickets[cp], 1);
             }
+        } else if (parts > 1) {
+            if (tid == 0) {
+                const int* tk = &a.tickets[cp];
+                int seen;
+                do {
+                    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(seen) : "l"(tk) : "memory");
+                } while (seen < parts - 1);
+            }
+            __syncthreads();
+            const std::size_t p0 = static_cast<std::size_t>(cp) * sk.max_parts;
+#pragma unroll
+            for (int k = 0; k < kPer; ++k) {
+                const int idx = tid + k * S::kThreads;
+                if (idx >= G * D) break;
+                const int g = idx / D;
+                float mm = own_m[k];
+                for (int sp = 1; sp < parts; ++sp) mm = fmaxf(mm, __ldcg(&a.part_ml[((p0 + sp) * G + g) * 2]));
+                const float f0 = fast_exp2(own_m[k] - mm);
+                float ll = own_l[k] * f0, oo = own_o[k] * f0;
+                for (int sp = 1; sp < parts; ++sp) {
+                    const float f = fast_exp2(__ldcg(&a.part_ml[((p0 + sp) * G + g) * 2]) - mm);
+                    ll += __ldcg(&a.part_ml[((p0 + sp) * G + g) * 2 + 1]) * f;
+                    oo += __ldcg(&a.part_o[(p0 + sp) * G * D + idx]) * f;
+                }
+                out[idx] = __float2bfloat16_rn(oo / ll);
+            }
+            if (tid == 0) a.tickets[cp] = 0;  // next launch touches tickets only after its PDL wait
         }
         __syncthreads();  // red_* reused by the next pair
         (void)seg_first;
