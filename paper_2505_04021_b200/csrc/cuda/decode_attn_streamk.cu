@@ -313,14 +313,19 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
                 const int idx = tid + k * S::kThreads;
                 if (idx >= G * D) break;
                 const int g = idx / D;
-                float mm = own_m[k];
-                for (int sp = 1; sp < parts; ++sp) mm = fmaxf(mm, __ldcg(&a.part_ml[((p0 + sp) * G + g) * 2]));
-                const float f0 = fast_exp2(own_m[k] - mm);
-                float ll = own_l[k] * f0, oo = own_o[k] * f0;
+                // one pass, online combination: each part's (m, l, o) loads are
+                // independent of the running state, so they go out together
+                float mm = own_m[k], ll = own_l[k], oo = own_o[k];
+#pragma unroll 2
                 for (int sp = 1; sp < parts; ++sp) {
-                    const float f = fast_exp2(__ldcg(&a.part_ml[((p0 + sp) * G + g) * 2]) - mm);
-                    ll += __ldcg(&a.part_ml[((p0 + sp) * G + g) * 2 + 1]) * f;
-                    oo += __ldcg(&a.part_o[(p0 + sp) * G * D + idx]) * f;
+                    const float pm = __ldcg(&a.part_ml[((p0 + sp) * G + g) * 2]);
+                    const float pl = __ldcg(&a.part_ml[((p0 + sp) * G + g) * 2 + 1]);
+                    const float po = __ldcg(&a.part_o[(p0 + sp) * G * D + idx]);
+                    const float nm = fmaxf(mm, pm);
+                    const float fa = fast_exp2(mm - nm), fb = fast_exp2(pm - nm);
+                    ll = ll * fa + pl * fb;
+                    oo = oo * fa + po * fb;
+                    mm = nm;
                 }
                 out[idx] = __float2bfloat16_rn(oo / ll);
             }
