@@ -368,6 +368,11 @@ int prism_device_chunk_pages(const prism_device* d, uint64_t* out);
 void prism_device_close(prism_device* d);
 /* Ledger capacity in pages after leaving reserve_bytes of free HBM. */
 int prism_device_capacity_pages(const prism_device* d, uint64_t reserve_bytes, uint64_t* out);
+/* Startup reservation of physical memory: create handles for `pages` logical
+ * pages (bounded by the ledger's physical budget) on the VMM worker and keep
+ * that many ready, so maps while serving never wait on cuMemCreate. Pair with
+ * prism_device_quiesce to wait for it. */
+int prism_device_reserve(prism_device* d, uint64_t pages);
 typedef struct {
     uint64_t maps, revived, creates, unmaps, driver_unmaps;
     double map_ns_total, unmap_ns_total;

@@ -277,6 +277,7 @@ _DEVICE_DECLS = {
     "prism_device_reset_stats": (c_int, [c_void_p]),
     "prism_device_reclaim": (c_int, [c_void_p, c_int]),
     "prism_device_quiesce": (c_int, [c_void_p]),
+    "prism_device_reserve": (c_int, [c_void_p, c_uint64]),
     "prism_device_fence": (c_int, [c_void_p]),
     "prism_device_synchronize": (c_int, [c_void_p]),
     "prism_device_stream": (c_void_p, [c_void_p]),

@@ -161,6 +161,13 @@ int prism_device_chunk_pages(const prism_device* d, uint64_t* out) {
     });
 }
 
+int prism_device_reserve(prism_device* d, uint64_t pages) {
+    return dguard([&] {
+        need(d, "device");
+        d->dev->reserve_physical(pages);
+    });
+}
+
 int prism_device_quiesce(prism_device* d) {
     return dguard([&] {
         need(d, "device");

@@ -509,7 +509,16 @@ void VmmDevice::forget(std::uint64_t owner) {
 void VmmDevice::prefill_cache(std::uint64_t pages) {
     {
         Lock lk(mu_);
-        cache_target_ = (pages + chunk_pages_ - 1) / chunk_pages_;
+        cache_target_ = std::max(reserve_target_, (pages + chunk_pages_ - 1) / chunk_pages_);
+    }
+    cv_.notify_one();
+}
+
+void VmmDevice::reserve_physical(std::uint64_t pages) {
+    {
+        Lock lk(mu_);
+        reserve_target_ = (pages + chunk_pages_ - 1) / chunk_pages_;
+        cache_target_ = std::max(cache_target_, reserve_target_);
     }
     cv_.notify_one();
 }

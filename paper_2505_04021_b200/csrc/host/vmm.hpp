@@ -115,6 +115,10 @@ public:
     void forget(std::uint64_t owner);
     // Keep created handles for `pages` logical pages ready (worker).
     void prefill_cache(std::uint64_t pages);
+    // Startup reservation: create physical handles for `pages` logical pages
+    // (bounded by the budget) and keep that many ready from now on, so page
+    // maps during serving never wait on cuMemCreate (the OS allocation).
+    void reserve_physical(std::uint64_t pages);
 
     // Physically unmap idle chunks (wait=true: all, after draining the worker
     // and the stream; false: released chunks whose fence passed).
@@ -193,6 +197,7 @@ private:
     std::map<std::uint64_t, std::uint64_t> ranges_;              // reserved VA base -> end
     std::map<std::uint64_t, std::pair<std::uint64_t, std::uint64_t>> window_;  // owner -> [lo, hi) chunk VAs
     std::uint64_t cache_target_ = 0;   // chunks
+    std::uint64_t reserve_target_ = 0; // chunks: floor of cache_target_ (reserve())
     std::uint64_t worker_busy_ = 0;
     bool stop_ = false;
     std::string failed_;  // first driver error on the worker (reported to callers)

@@ -553,6 +553,11 @@ class Device:
     def reset_stats(self) -> None:
         self.lib.call("prism_device_reset_stats", self.h)
 
+    def reserve(self, pages: int) -> None:
+        """Create physical handles for `pages` pages up front (startup
+        reservation; bounded by the ledger budget)."""
+        self.lib.call("prism_device_reserve", self.h, pages)
+
     def quiesce(self) -> None:
         """Wait until the background VMM worker has no queued work."""
         self.lib.call("prism_device_quiesce", self.h)
