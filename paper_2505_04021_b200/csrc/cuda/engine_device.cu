@@ -2,6 +2,7 @@
 // prism:: device API entry points (msim/kvcache_device.hpp) that do not
 // launch the append / attention kernels.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "cuda/device_impl.cuh"
@@ -268,7 +269,11 @@ void decode_host(me::Engine& eng, const void* new_k, const void* new_v, const vo
     // the compute stream once; outputs go back in groups of kOutGroup layers
     // while the following layers' K3 run. Few cross-stream edges keep the K3
     // launches back to back (programmatic-dependent chain).
-    constexpr int kOutGroup = 8;
+    static const int kOutGroup = [] {  // layers per output copy (PRISM_E2E_OUT_GROUP, default 4)
+        const char* e = std::getenv("PRISM_E2E_OUT_GROUP");
+        const int v = e ? std::atoi(e) : 4;
+        return v > 0 ? v : 4;
+    }();
     const bool with_kv = new_k && new_v && n_tok;
     if (with_kv) {
         PRISM_CUDA(cudaMemcpyAsync(dk, new_k, kv_bytes, cudaMemcpyHostToDevice, cs));
