@@ -251,18 +251,21 @@ bool VmmDevice::take_handle(Lock& lk, bool urgent, std::uint64_t& h) {
         return true;
     };
     if (total_locked() < budget_chunks() && create()) return true;
-    if (!urgent) return false;
+    if (!urgent) return steal_for_worker(lk, h, /*premap=*/true);
     if (steal_for_worker(lk, h)) return true;
     // Nothing idle to move (the budget shrank under queued maps): past it.
     return create();
 }
 
-bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h) {
+bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h, bool premap) {
     // Move the highest idle chunk that is safe (look-ahead and never read,
     // or released before a fence that passed), preferring chunks outside
     // every pool's look-ahead window: allocation reuses the lowest unmapped
     // page indices, so high idle chunks are the least likely to be revived.
     // The handle keeps its mapped_ count (it moves from chunk to chunk).
+    // premap: a look-ahead map may take only a safe chunk outside every
+    // window, and never waits for a fence (memory moves to growing pools
+    // ahead of need instead of on an urgent map the caller waits for).
     while (!stop_) {
         advance_fences(false);
         std::uint64_t pick = 0, fallback = 0;
@@ -277,6 +280,7 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h) {
             }
             if (++scanned >= kStealScan) break;
         }
+        if (premap && !pick) return false;
         if (!pick) pick = fallback;
         if (pick) {
             const auto vit = chunks_.find(pick);
@@ -325,7 +329,7 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h) {
             done_cv_.notify_all();
             return true;
         }
-        if (idle_.empty()) return false;
+        if (idle_.empty() || premap) return false;
         // Every idle chunk may still be read by queued kernels: fence and
         // poll until that fence passes.
         fence_locked();

@@ -171,7 +171,7 @@ private:
     // worker
     void worker_main();
     bool take_handle(Lock& lk, bool urgent, std::uint64_t& h);
-    bool steal_for_worker(Lock& lk, std::uint64_t& h);
+    bool steal_for_worker(Lock& lk, std::uint64_t& h, bool premap = false);
     bool map_chunk(Lock& lk, std::uint64_t va, std::uint64_t h, bool urgent);
     void trace(char kind, std::uint32_t n, Clock::time_point t0, double ns);
     void dump_trace() const;
