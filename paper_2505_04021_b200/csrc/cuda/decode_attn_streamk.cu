@@ -591,7 +591,14 @@ void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec) {
     }();
     g_k3_trace = trace;
     SkArgs s{};
-    s.trace = trace;
+    // PRISM_K3_TRACE_LAUNCH=n: stamp only the n-th traced-enabled launch
+    static const long long trace_pick = [] {
+        const char* e = std::getenv("PRISM_K3_TRACE_LAUNCH");
+        return e ? std::atoll(e) : -1LL;
+    }();
+    static long long launch_no = 0;
+    s.trace = (trace_pick < 0 || launch_no == trace_pick) ? trace : nullptr;
+    ++launch_no;
     s.a = a;
     s.pair_tiles = d.sk_prefix.dev;
     s.n_pairs = n_pairs;
