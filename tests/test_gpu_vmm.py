@@ -169,3 +169,32 @@ def test_concurrent_pools_with_worker_keep_data(product, device):
             steps += 1
         assert gpu.ledger.mapped_pages() == 0
     device.quiesce()
+
+
+def test_startup_reservation_backs_later_maps(product):
+    """prism_device_reserve: physical handles for the requested pages are
+    created up front and that many are kept ready (bounded by the ledger's
+    physical budget); the data path is unchanged."""
+    dev = msim.Device(0, lib=product)
+    try:
+        gpu = msim.GpuState(0, 600, lib=product)
+        gpu.ledger.attach_device(dev)
+        spec = S.shape_spec("llama3.2-1b", "resv", chunk=256, weight_scale=0.0)
+        act = gpu.activate(spec)
+        gpu.finish_activation(act.engine_index)
+        eng = gpu.engine(act.engine_index)
+        eng.attach_device()
+        dev.reserve(400)
+        dev.quiesce()
+        st = dev.stats()
+        assert st["cached"] * st["chunk_pages"] >= 400 and st["creates"] * st["chunk_pages"] >= 400
+        for i, p in enumerate([300, 500, 120]):
+            eng.push(i + 1, p, 8)
+        while sum(eng.counts()):
+            eng.step()
+            eng.append_kv_synthetic(0, spec.n_layers, SEED)
+            _attn_ok(eng, spec)
+        st = dev.stats()
+        assert st["total_chunks"] * st["chunk_pages"] <= 600  # never past the physical budget
+    finally:
+        dev.close()
