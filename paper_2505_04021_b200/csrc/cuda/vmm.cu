@@ -11,6 +11,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <chrono>
 #include <cstring>
 
@@ -77,6 +78,8 @@ void sample(std::vector<float>& ring, double ns) {
     if (ring.size() < kMaxSamples) ring.push_back(static_cast<float>(ns));
 }
 
+// Idle chunks moved per steal (one cuMemUnmap over a contiguous run).
+constexpr int kStealBatch = 8;
 // How many in-window idle chunks a steal skips over looking for one outside
 // every look-ahead window (bounds the scan).
 constexpr int kStealScan = 256;
@@ -251,7 +254,16 @@ bool VmmDevice::take_handle(Lock& lk, bool urgent, std::uint64_t& h) {
         return true;
     };
     if (total_locked() < budget_chunks() && create()) return true;
-    if (!urgent) return steal_for_worker(lk, h, /*premap=*/true);
+    if (!urgent) {
+        // Look-ahead steals (PRISM_VMM_PREMAP_STEAL=1) move memory to growing
+        // pools ahead of need, but in C2 churn they raised the driver unmap
+        // count ~40% (memory moved back and forth), so they are off by default.
+        static const bool premap_steal = [] {
+            const char* e = std::getenv("PRISM_VMM_PREMAP_STEAL");
+            return e && e[0] == '1';
+        }();
+        return premap_steal && steal_for_worker(lk, h, /*premap=*/true);
+    }
     if (steal_for_worker(lk, h)) return true;
     // Nothing idle to move (the budget shrank under queued maps): past it.
     return create();
@@ -283,48 +295,83 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h, bool premap) {
         if (premap && !pick) return false;
         if (!pick) pick = fallback;
         if (pick) {
-            const auto vit = chunks_.find(pick);
-            Chunk& v = vit->second;
-            idle_.erase(pick);
-            if (v.clean) {
-                --clean_;
-                ++stats_.caller_steals_clean;
+            // Take the pick and up to kStealBatch - 1 idle chunks directly
+            // below it in the same reservation (safe and outside every
+            // window) in ONE cuMemUnmap: the driver cost of an unmap is mostly
+            // per call, and a pool that needed one stolen chunk needs more.
+            // The extra handles go to the cache for the next maps.
+            auto r = ranges_.upper_bound(pick);
+            const std::uint64_t res_lo = r == ranges_.begin() ? pick : std::prev(r)->first;
+            std::uint64_t lo = pick;
+            int n = 1;
+            while (n < kStealBatch && lo >= res_lo + chunk_bytes_) {
+                const std::uint64_t va = lo - chunk_bytes_;
+                if (!idle_.count(va)) break;
+                const Chunk& c = chunks_.find(va)->second;
+                if (!(c.clean || c.epoch < fenced_) || in_window(va)) break;
+                lo = va;
+                ++n;
             }
-            h = v.handle;
-            v.handle = 0;
-            v.mapped = false;
-            v.clean = false;
-            v.inflight = true;
+            std::vector<std::uint64_t> handles;
+            for (std::uint64_t va = lo; va <= pick; va += chunk_bytes_) {
+                Chunk& v = chunks_.find(va)->second;
+                idle_.erase(va);
+                if (v.clean) {
+                    --clean_;
+                    ++stats_.caller_steals_clean;
+                }
+                handles.push_back(v.handle);
+                v.handle = 0;
+                v.mapped = false;
+                v.clean = false;
+                v.inflight = true;
+            }
             lk.unlock();
             const auto t0 = Clock::now();
-            const CUresult r = drv().unmap(static_cast<CUdeviceptr>(pick), chunk_bytes_);
+            const CUresult res = drv().unmap(static_cast<CUdeviceptr>(lo), chunk_bytes_ * static_cast<std::uint64_t>(n));
             const double ns = ns_since(t0);
             lk.lock();
-            v.inflight = false;
-            if (r != CUDA_SUCCESS) {
-                v.handle = h;
-                v.mapped = true;
-                if (v.refs == 0) {
-                    set_idle(pick, v);
-                } else {
-                    --unready_;  // a caller revived it meanwhile: still mapped
+            if (res != CUDA_SUCCESS) {
+                std::size_t k = 0;
+                for (std::uint64_t va = lo; va <= pick; va += chunk_bytes_, ++k) {
+                    Chunk& v = chunks_.find(va)->second;
+                    v.inflight = false;
+                    v.handle = handles[k];
+                    v.mapped = true;
+                    if (v.refs == 0) {
+                        set_idle(va, v);
+                    } else {
+                        --unready_;  // a caller revived it meanwhile: still mapped
+                    }
                 }
-                failed_ = "cuMemUnmap failed (" + std::to_string(r) + ")";
+                failed_ = "cuMemUnmap failed (" + std::to_string(res) + ")";
                 done_cv_.notify_all();
                 return false;
             }
             ++stats_.driver_unmaps;
-            ++stats_.steals;
+            stats_.steals += static_cast<std::uint64_t>(n);
             stats_.steal_ns_total += ns;
-            trace('U', 1, t0, ns);
-            if (v.refs > 0) {
-                // its pool mapped a page in it again meanwhile: map it back
-                if (!v.queued) {
-                    urgent_.push_back(pick);
-                    v.queued = true;
+            trace('U', n, t0, ns);
+            // the pick's handle goes to the caller (keeps its mapped_ count);
+            // the others become cached, unmapped handles
+            h = handles.back();
+            for (std::size_t k = 0; k + 1 < handles.size(); ++k) {
+                cache_.push_back(handles[k]);
+                --mapped_;
+            }
+            for (std::uint64_t va = lo; va <= pick; va += chunk_bytes_) {
+                const auto vit = chunks_.find(va);
+                Chunk& v = vit->second;
+                v.inflight = false;
+                if (v.refs > 0) {
+                    // its pool mapped a page in it again meanwhile: map it back
+                    if (!v.queued) {
+                        urgent_.push_back(va);
+                        v.queued = true;
+                    }
+                } else {
+                    drop_if_empty(vit);
                 }
-            } else {
-                drop_if_empty(vit);
             }
             done_cv_.notify_all();
             return true;
