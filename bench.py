@@ -485,6 +485,20 @@ def page_churn_c2(max_rounds=2500, kv_pages=6000, horizon_s=60.0):
     return res
 
 
+def page_churn_c2_median(reps=3):
+    """page_churn_c2 `reps` times in this process (a fresh device, ledger and
+    engines each time; identical seeded trace, so identical logical and driver
+    call counts): the per-call cost of the CUDA VMM driver calls varies up to
+    ~10x between runs on the same box (tools/vmm_churn_repeat.py), so the
+    median run is reported, with every run's amortised figure beside it."""
+    runs = [page_churn_c2() for _ in range(reps)]
+    order = sorted(range(reps), key=lambda i: runs[i]["amortised_us_per_page_op"])
+    res = dict(runs[order[reps // 2]])
+    res["amortised_us_per_page_op_runs"] = [r["amortised_us_per_page_op"] for r in runs]
+    res["reported"] = f"median of {reps} runs"
+    return res
+
+
 def page_map_summary(st, steps):
     """amortised_us_per_page_op = host time the CALLER's thread (the engine /
     scheduler loop) spends in the VMM layer per logical map+unmap: revives,
@@ -798,7 +812,7 @@ def main():
                 res["cpu_baseline"] = {"error": str(e)}
         if world == 1 and not args.no_churn:
             try:
-                res["page_map_c2"] = page_churn_c2()
+                res["page_map_c2"] = page_churn_c2_median()
             except Exception as e:
                 res["page_map_c2"] = {"error": str(e)}
         if world == 1 and not args.no_prefill:

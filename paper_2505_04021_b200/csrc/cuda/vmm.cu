@@ -78,6 +78,15 @@ void sample(std::vector<float>& ring, double ns) {
     if (ring.size() < kMaxSamples) ring.push_back(static_cast<float>(ns));
 }
 
+// Minimum idle time of a chunk a look-ahead map may steal.
+std::chrono::steady_clock::duration premap_steal_age() {
+    static const auto age = [] {
+        const char* e = std::getenv("PRISM_VMM_PREMAP_STEAL_AGE_MS");
+        return std::chrono::duration_cast<std::chrono::steady_clock::duration>(
+            std::chrono::duration<double, std::milli>(e ? std::atof(e) : 200.0));
+    }();
+    return age;
+}
 // Idle chunks moved per steal (one cuMemUnmap over a contiguous run).
 constexpr int kStealBatch = 8;
 // How many in-window idle chunks a steal skips over looking for one outside
@@ -202,6 +211,7 @@ bool VmmDevice::in_window(std::uint64_t chunk_va) const {
 
 void VmmDevice::set_idle(std::uint64_t va, Chunk& c) {
     idle_.insert(va);
+    c.idle_at = Clock::now();
     if (c.clean) ++clean_;
 }
 
@@ -255,12 +265,14 @@ bool VmmDevice::take_handle(Lock& lk, bool urgent, std::uint64_t& h) {
     };
     if (total_locked() < budget_chunks() && create()) return true;
     if (!urgent) {
-        // Look-ahead steals (PRISM_VMM_PREMAP_STEAL=1) move memory to growing
-        // pools ahead of need, but in C2 churn they raised the driver unmap
-        // count ~40% (memory moved back and forth), so they are off by default.
+        // Look-ahead steals move memory to growing pools ahead of need, but
+        // only chunks idle for at least PRISM_VMM_PREMAP_STEAL_AGE_MS (a
+        // model that went quiet): stealing recently released chunks moved
+        // memory back and forth (C2 churn: ~40% more driver unmaps).
+        // PRISM_VMM_PREMAP_STEAL=0 turns them off.
         static const bool premap_steal = [] {
             const char* e = std::getenv("PRISM_VMM_PREMAP_STEAL");
-            return e && e[0] == '1';
+            return !(e && e[0] == '0');
         }();
         return premap_steal && steal_for_worker(lk, h, /*premap=*/true);
     }
@@ -282,9 +294,11 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h, bool premap) {
         advance_fences(false);
         std::uint64_t pick = 0, fallback = 0;
         int scanned = 0;
+        const auto now = Clock::now();
+        const auto aged = [&](const Chunk& v) { return !premap || now - v.idle_at >= premap_steal_age(); };
         for (auto it = idle_.rbegin(); it != idle_.rend(); ++it) {
             const Chunk& v = chunks_.find(*it)->second;
-            if (!(v.clean || v.epoch < fenced_)) continue;
+            if (!(v.clean || v.epoch < fenced_) || !aged(v)) continue;
             if (!fallback) fallback = *it;
             if (!in_window(*it)) {
                 pick = *it;
@@ -308,7 +322,7 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h, bool premap) {
                 const std::uint64_t va = lo - chunk_bytes_;
                 if (!idle_.count(va)) break;
                 const Chunk& c = chunks_.find(va)->second;
-                if (!(c.clean || c.epoch < fenced_) || in_window(va)) break;
+                if (!(c.clean || c.epoch < fenced_) || in_window(va) || !aged(c)) break;
                 lo = va;
                 ++n;
             }

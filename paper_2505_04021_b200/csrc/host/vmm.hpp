@@ -154,6 +154,7 @@ private:
         bool inflight = false;     // the worker is mapping / unmapping it now
         bool queued = false;       // in urgent_
         bool clean = false;        // mapped by the look-ahead, never referenced
+        std::chrono::steady_clock::time_point idle_at{};  // when it last became idle
     };
     using ChunkMap = std::map<std::uint64_t, Chunk>;
 
