@@ -652,6 +652,55 @@ def decode_c3(batch=16, ctx=32768, reps=3):
             "decode_tokens_per_s": round(batch / (ms * L / 1e3), 1)}
 
 
+def activation_f2(gib=2.0, copies=6, horizon=240.0):
+    """model weight loading for activation
+    through the native WeightLoader, replacing the modelled latency curve
+    (reference ActivationParams::load_latency_s, engine.hpp:46-48,
+    src/engine.cpp:44-51; paper anchors on H100: 8B in 0.7 s parallel, 3.36 s
+    naive). Times, on this GPU, `gib` GiB host -> HBM: one cudaMemcpyAsync
+    from pageable memory (the naive path), one from pinned memory, and the
+    chunked multi-stream path (4 streams x 32 MiB) from pinned memory; device
+    time by CUDA events, best of 3. Then re-runs C5 on 1 and 2 GPUs in
+    simcore with the measured bandwidths in place of the modelled curves.
+    The multi-GPU fan-in (tools/wload_fanin.py) needs more than one GPU."""
+    import torch
+
+    from paper_2505_04021_b200 import msim
+    from paper_2505_04021_b200.configs import c5_case
+
+    n = int(gib * (1 << 30))
+    pinned = torch.empty(n, dtype=torch.uint8).pin_memory()
+    pageable = torch.empty(n, dtype=torch.uint8)
+    pinned[::4096] = 1
+    pageable[::4096] = 1
+    dst = torch.empty(n, dtype=torch.uint8, device="cuda")
+    res = {"workload": f"{gib:g} GiB host -> HBM on one B200, best of 3 (CUDA events)"}
+    wl = msim.WeightLoader(torch.cuda.current_device(), 4, 32 << 20)
+    for name, src, fn in (("naive_pageable", pageable, wl.load_naive), ("naive_pinned", pinned, wl.load_naive),
+                          ("chunked_pinned", pinned, wl.load)):
+        best = None
+        for _ in range(3):
+            torch.cuda.synchronize()
+            fn(src.data_ptr(), dst.data_ptr(), n)
+            ms = wl.wait()
+            best = ms if best is None else min(best, ms)
+        if not torch.equal(dst[::4096].cpu(), pinned[::4096]):
+            raise RuntimeError(f"weight load {name}: bytes differ")
+        res[name] = {"ms": round(best, 2), "gbs": round(n / best / 1e6, 2)}
+    wl.close()
+    fast, slow = res["chunked_pinned"]["gbs"], res["naive_pageable"]["gbs"]
+    res["llama3.1-8b_load_s"] = {"parallel": round(16.06e9 / fast / 1e9, 3), "naive": round(16.06e9 / slow / 1e9, 3),
+                                 "paper_h100_parallel": 0.7, "paper_h100_naive": 3.36}
+    models, prof = c5_case(copies=copies, horizon=horizon)
+    trace = msim.synth_trace(prof, TRACE_SEED)
+    res["c5_attainment_measured_load"] = {}
+    for g in (1, 2):
+        cfg = msim.SimConfig(n_gpus=g, capacity_pages=85_830, parallel_load_gbs=fast, naive_load_gbs=slow)
+        r = msim.simulate(cfg, models, trace)
+        res["c5_attainment_measured_load"][str(g)] = {str(k): round(r.attainment(k)["both"], 4) for k in (1, 2, 4)}
+    return res
+
+
 def slo_c5(copies=6, horizon=240.0):
     """BASELINE config 5 through simcore (include/msim/simcore.hpp, the
     native discrete-event driver of SPEC.md:514-579): the 8 SURVEY §8d shapes
@@ -829,6 +878,10 @@ def main():
                 res["slo_c5"] = slo_c5()
             except Exception as e:
                 res["slo_c5"] = {"error": str(e)}
+            try:
+                res["activation_f2"] = activation_f2()
+            except Exception as e:
+                res["activation_f2"] = {"error": str(e)}
         print(json.dumps(res))
     if world > 1:
         import torch.distributed as dist

@@ -331,6 +331,10 @@ typedef struct {
     uint64_t buffer_target_pages;
     int32_t initial_placement;
     uint64_t max_events;
+    /* measured weight-load bandwidths (GB/s; 0 = the reference's modelled
+     * curves, engine.hpp ActivationParams) and fixed cost (s) per load:
+     * load_latency = fixed + weight_bytes / bandwidth (prism_wloader_*). */
+    double parallel_load_gbs, naive_load_gbs, load_fixed_s;
 } prism_sim_config;
 
 typedef struct {
@@ -467,6 +471,31 @@ int prism_engine_decode_host_async(prism_gpu* g, int engine_index, const void* n
                                    const void* q, void* out, float scale);
 int prism_engine_wait_host(prism_gpu* g, int engine_index);
 int prism_engine_synchronize(prism_gpu* g, int engine_index);
+
+/* ---- model weight loading for activation ----
+ * Replaces the modelled weight-load latency of activation
+ * (ActivationParams::load_latency_s, reference engine.hpp:46-48,
+ * src/engine.cpp:44-51) with the paper's data path:
+ * chunked multi-stream loads, and the per-helper half of a staged fan-in into
+ * another GPU (peer or IPC pointer). Enqueue-only; prism_wloader_wait
+ * synchronises and reports device milliseconds. Host memory must be pinned. */
+typedef struct prism_wloader prism_wloader;
+int prism_wloader_create(int device, int n_streams, uint64_t chunk_bytes, prism_wloader** out);
+int prism_wloader_destroy(prism_wloader* w);
+/* host -> dst (this loader's GPU), chunks round-robin over the streams */
+int prism_wloader_load(prism_wloader* w, const void* host, void* dst, uint64_t bytes);
+/* baseline: one cudaMemcpyAsync */
+int prism_wloader_load_naive(prism_wloader* w, const void* host, void* dst, uint64_t bytes);
+/* fan-in helper: chunks i % n_parts == part, host -> this GPU's staging -> dst (any GPU) */
+int prism_wloader_load_part(prism_wloader* w, const void* host, void* dst, uint64_t bytes, int part, int n_parts);
+int prism_wloader_wait(prism_wloader* w, double* ms);
+/* cudaHostRegister / Unregister (pin an existing host buffer) */
+int prism_host_register(void* host, uint64_t bytes);
+int prism_host_unregister(void* host);
+/* CUDA IPC for fan-in across processes: 64-byte handle of a cudaMalloc'ed pointer */
+int prism_ipc_handle(const void* dptr, void* handle64);
+int prism_ipc_open(int device, const void* handle64, void** dptr);
+int prism_ipc_close(int device, void* dptr);
 
 #ifdef __cplusplus
 }

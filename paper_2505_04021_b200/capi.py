@@ -146,7 +146,8 @@ class SimConfig(C.Structure):
     _fields_ = [("policy", c_int32), ("n_gpus", c_int32), ("capacity_pages", c_uint64), ("page_bytes", c_uint64),
                 ("params", EngineParams), ("method", c_int32), ("tau_per_gb", c_double), ("tick_s", c_double),
                 ("idle_evict_s", c_double), ("pressure_free_frac", c_double), ("buffer_target_pages", c_uint64),
-                ("initial_placement", c_int32), ("max_events", c_uint64)]
+                ("initial_placement", c_int32), ("max_events", c_uint64), ("parallel_load_gbs", c_double),
+                ("naive_load_gbs", c_double), ("load_fixed_s", c_double)]
 
 
 class SimSummary(C.Structure):
@@ -304,6 +305,17 @@ _DEVICE_DECLS = {
     "prism_engine_synchronize": (c_int, [c_void_p, c_int]),
     "prism_engine_decode_host_async": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_float]),
     "prism_engine_wait_host": (c_int, [c_void_p, c_int]),
+    "prism_wloader_create": (c_int, [c_int, c_int, c_uint64, P(c_void_p)]),
+    "prism_wloader_destroy": (c_int, [c_void_p]),
+    "prism_wloader_load": (c_int, [c_void_p, c_void_p, c_void_p, c_uint64]),
+    "prism_wloader_load_naive": (c_int, [c_void_p, c_void_p, c_void_p, c_uint64]),
+    "prism_wloader_load_part": (c_int, [c_void_p, c_void_p, c_void_p, c_uint64, c_int, c_int]),
+    "prism_wloader_wait": (c_int, [c_void_p, P(c_double)]),
+    "prism_host_register": (c_int, [c_void_p, c_uint64]),
+    "prism_host_unregister": (c_int, [c_void_p]),
+    "prism_ipc_handle": (c_int, [c_void_p, c_void_p]),
+    "prism_ipc_open": (c_int, [c_int, c_void_p, P(c_void_p)]),
+    "prism_ipc_close": (c_int, [c_int, c_void_p]),
 }
 
 HOST_SYMBOLS = sorted(_HOST_DECLS)

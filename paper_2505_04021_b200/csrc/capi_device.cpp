@@ -10,6 +10,7 @@
 
 #include "host/pool_state.hpp"
 #include "host/vmm.hpp"
+#include "host/weight_load.hpp"
 #include "msim/kvcache_device.hpp"
 #include "prism_capi.h"
 #include "capi_handles.hpp"
@@ -401,6 +402,116 @@ int prism_engine_synchronize(prism_gpu* g, int engine_index) {
     return dguard([&] {
         auto stream = static_cast<cudaStream_t>(prism::engine_stream(engine_at(g, engine_index)));
         check(cudaStreamSynchronize(stream), "cudaStreamSynchronize");
+    });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- weight loading (§8f-2)
+
+struct prism_wloader {
+    std::unique_ptr<prism::WeightLoader> w;
+};
+
+namespace {
+struct DevSet {
+    int prev = 0;
+    explicit DevSet(int d) {
+        if (cudaGetDevice(&prev) != cudaSuccess) throw std::runtime_error("cudaGetDevice failed");
+        if (cudaSetDevice(d) != cudaSuccess) throw std::runtime_error("cudaSetDevice failed");
+    }
+    ~DevSet() { cudaSetDevice(prev); }
+};
+void rt_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+}  // namespace
+
+extern "C" {
+
+int prism_wloader_create(int device, int n_streams, uint64_t chunk_bytes, prism_wloader** out) {
+    return dguard([&] {
+        need(out, "out");
+        auto h = std::make_unique<prism_wloader>();
+        h->w = std::make_unique<prism::WeightLoader>(device, n_streams, static_cast<std::size_t>(chunk_bytes));
+        *out = h.release();
+    });
+}
+
+int prism_wloader_destroy(prism_wloader* w) {
+    return dguard([&] { delete w; });
+}
+
+int prism_wloader_load(prism_wloader* w, const void* host, void* dst, uint64_t bytes) {
+    return dguard([&] {
+        need(w, "loader");
+        w->w->load(host, dst, static_cast<std::size_t>(bytes));
+    });
+}
+
+int prism_wloader_load_naive(prism_wloader* w, const void* host, void* dst, uint64_t bytes) {
+    return dguard([&] {
+        need(w, "loader");
+        w->w->load_naive(host, dst, static_cast<std::size_t>(bytes));
+    });
+}
+
+int prism_wloader_load_part(prism_wloader* w, const void* host, void* dst, uint64_t bytes, int part, int n_parts) {
+    return dguard([&] {
+        need(w, "loader");
+        w->w->load_part(host, dst, static_cast<std::size_t>(bytes), part, n_parts);
+    });
+}
+
+int prism_wloader_wait(prism_wloader* w, double* ms) {
+    return dguard([&] {
+        need(w, "loader");
+        const double t = w->w->wait();
+        if (ms) *ms = t;
+    });
+}
+
+int prism_host_register(void* host, uint64_t bytes) {
+    return dguard([&] {
+        need(host, "host");
+        rt_check(cudaHostRegister(host, static_cast<std::size_t>(bytes), cudaHostRegisterDefault), "cudaHostRegister");
+    });
+}
+
+int prism_host_unregister(void* host) {
+    return dguard([&] {
+        need(host, "host");
+        rt_check(cudaHostUnregister(host), "cudaHostUnregister");
+    });
+}
+
+int prism_ipc_handle(const void* dptr, void* handle64) {
+    return dguard([&] {
+        need(dptr, "dptr");
+        need(handle64, "handle");
+        cudaIpcMemHandle_t h;
+        rt_check(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)), "cudaIpcGetMemHandle");
+        static_assert(sizeof(h) == 64, "CUDA IPC handle is 64 bytes");
+        std::memcpy(handle64, &h, sizeof(h));
+    });
+}
+
+int prism_ipc_open(int device, const void* handle64, void** dptr) {
+    return dguard([&] {
+        need(handle64, "handle");
+        need(dptr, "dptr");
+        DevSet g(device);
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle64, sizeof(h));
+        rt_check(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+    });
+}
+
+int prism_ipc_close(int device, void* dptr) {
+    return dguard([&] {
+        need(dptr, "dptr");
+        DevSet g(device);
+        rt_check(cudaIpcCloseMemHandle(dptr), "cudaIpcCloseMemHandle");
     });
 }
 

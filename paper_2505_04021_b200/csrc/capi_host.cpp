@@ -887,6 +887,13 @@ int prism_sim_run(const prism_sim_config* cfg, const prism_model_spec* specs, co
         c.page_bytes = cfg->page_bytes;
         c.params = to_params(&cfg->params);
         c.method = cfg->method ? me::ActivationMethod::parallel : me::ActivationMethod::naive;
+        const auto curve = [&](double gbs) {
+            std::vector<std::pair<double, double>> c2;
+            for (double b : {16e9, 28e9}) c2.emplace_back(b, cfg->load_fixed_s + b / (gbs * 1e9));
+            return c2;
+        };
+        if (cfg->parallel_load_gbs > 0.0) c.activation.parallel_curve = curve(cfg->parallel_load_gbs);
+        if (cfg->naive_load_gbs > 0.0) c.activation.naive_curve = curve(cfg->naive_load_gbs);
         c.tau_per_gb = cfg->tau_per_gb;
         c.tick_s = cfg->tick_s;
         c.idle_evict_s = cfg->idle_evict_s;

@@ -579,6 +579,89 @@ class Device:
 
 
 @dataclass
+class WeightLoader:
+    """prism::WeightLoader — model weight loading for activation (SURVEY
+    §8f-2; replaces the modelled
+    ActivationParams::load_latency_s, reference engine.hpp:46-48 /
+    src/engine.cpp:44-51). Pointers are plain integers (device or pinned
+    host addresses, e.g. ``tensor.data_ptr()``); every load is enqueued on the
+    loader's own streams and ``wait()`` returns its device milliseconds."""
+
+    def __init__(self, device: int = 0, n_streams: int = 4, chunk_bytes: int = 8 << 20, lib=None):
+        self.lib = _lib(lib)
+        if not self.lib.has_device:
+            raise capi.CudaError(5, f"{self.lib.path} has no GPU data path")
+        self.device = device
+        self.h = C.c_void_p()
+        self.lib.call("prism_wloader_create", device, n_streams, chunk_bytes, C.byref(self.h))
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            self.lib.prism_wloader_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load(self, host: int, dst: int, nbytes: int) -> None:
+        """Chunked load, chunks round-robin over the loader's streams."""
+        self.lib.call("prism_wloader_load", self.h, C.c_void_p(host), C.c_void_p(dst), nbytes)
+
+    def load_naive(self, host: int, dst: int, nbytes: int) -> None:
+        """Baseline: one cudaMemcpyAsync."""
+        self.lib.call("prism_wloader_load_naive", self.h, C.c_void_p(host), C.c_void_p(dst), nbytes)
+
+    def load_part(self, host: int, dst: int, nbytes: int, part: int, n_parts: int) -> None:
+        """Fan-in helper: chunks i % n_parts == part through this GPU's staging into dst (any GPU)."""
+        self.lib.call("prism_wloader_load_part", self.h, C.c_void_p(host), C.c_void_p(dst), nbytes, part, n_parts)
+
+    def wait(self) -> float:
+        ms = C.c_double()
+        self.lib.call("prism_wloader_wait", self.h, C.byref(ms))
+        return ms.value
+
+
+def ipc_handle(dptr: int, lib=None) -> bytes:
+    """64-byte CUDA IPC handle of a cudaMalloc'ed device pointer."""
+    lib = _lib(lib)
+    buf = (C.c_ubyte * 64)()
+    lib.call("prism_ipc_handle", C.c_void_p(dptr), buf)
+    return bytes(buf)
+
+
+def ipc_open(device: int, handle: bytes, lib=None) -> int:
+    lib = _lib(lib)
+    buf = (C.c_ubyte * 64).from_buffer_copy(handle)
+    p = C.c_void_p()
+    lib.call("prism_ipc_open", device, buf, C.byref(p))
+    return p.value
+
+
+def ipc_close(device: int, dptr: int, lib=None) -> None:
+    _lib(lib).call("prism_ipc_close", device, C.c_void_p(dptr))
+
+
+def fanin_parts(n_bytes: int, chunk_bytes: int, n_parts: int) -> list:
+    """Which byte ranges each helper of an n_parts fan-in copies (chunk i goes
+    to part i % n_parts) — the plan WeightLoader.load_part executes; every
+    byte is covered exactly once."""
+    parts = [[] for _ in range(n_parts)]
+    for i, off in enumerate(range(0, n_bytes, chunk_bytes)):
+        parts[i % n_parts].append((off, min(chunk_bytes, n_bytes - off)))
+    return parts
+
+
+def measured_activation_curve(gbs: float, fixed_s: float = 0.0, sizes=(16e9, 28e9)) -> list:
+    """ActivationParams.parallel_curve points (weight bytes, seconds) from a
+    measured load bandwidth: seconds = fixed_s + bytes / (gbs * 1e9); the
+    reference interpolates linearly between such anchors
+    (src/engine.cpp:44-51)."""
+    return [(float(b), fixed_s + float(b) / (gbs * 1e9)) for b in sizes]
+
+
 class ResidentModel:
     idle_s: float = 0.0
     ttft_slo_s: float = 0.0
@@ -851,6 +934,11 @@ class SimConfig:
     buffer_target_pages: int = 8
     initial_placement: bool = True
     max_events: int = 200_000_000
+    # measured weight-load bandwidth (GB/s) replacing the modelled activation
+    # curves (WeightLoader; 0 = the reference's curves) + fixed s per load
+    parallel_load_gbs: float = 0.0
+    naive_load_gbs: float = 0.0
+    load_fixed_s: float = 0.0
 
 
 class SimResult:
@@ -896,6 +984,7 @@ def simulate(cfg: SimConfig, models: Sequence, trace: Sequence[TraceEvent], lib=
     c.tau_per_gb, c.tick_s, c.idle_evict_s = cfg.tau_per_gb, cfg.tick_s, cfg.idle_evict_s
     c.pressure_free_frac, c.buffer_target_pages = cfg.pressure_free_frac, cfg.buffer_target_pages
     c.initial_placement, c.max_events = int(cfg.initial_placement), cfg.max_events
+    c.parallel_load_gbs, c.naive_load_gbs, c.load_fixed_s = cfg.parallel_load_gbs, cfg.naive_load_gbs, cfg.load_fixed_s
     specs = (capi.ModelSpec * max(len(models), 1))(*[m[0].to_c() for m in models])
     rates = (C.c_double * max(len(models), 1))(*[m[1] for m in models])
     arr = (capi.TraceEvent * max(len(trace), 1))()

@@ -192,3 +192,27 @@ def test_qlm_timeshare_swaps(product, reference):
     # more GPUs with the same load: swaps do not decrease (SPEC, directional)
     two = _run(product, 2, models, alt, capacity=30_000, policy="qlm_timeshare")
     assert two.summary["activations"] >= 2
+
+
+def test_measured_load_bandwidth_replaces_modelled_curve(product, reference):
+    """a measured weight-load bandwidth (WeightLoader) replaces
+    the modelled activation curve. Config 1's two models are activated at
+    t = 0 (initial placement, parallel load), so the first request's TTFT
+    moves by exactly the load-time difference between two bandwidths; the
+    reference-source build agrees record for record."""
+    models, trace = _c1(product)
+    slow = _run(product, 1, models, trace, capacity=18_000, parallel_load_gbs=10.0)
+    fast = _run(product, 1, models, trace, capacity=18_000, parallel_load_gbs=100.0)
+    ref = _run(reference, 1, models, trace, capacity=18_000, parallel_load_gbs=10.0)
+    assert slow.requests == ref.requests and slow.summary == ref.summary
+    _check_invariants(slow, trace)
+    _check_invariants(fast, trace)
+    w = models[0][0].weight_bytes
+    first = min(range(len(trace)), key=lambda i: trace[i].arrival_s)
+    d = slow.requests[first]["first_token_us"] - fast.requests[first]["first_token_us"]
+    assert d > 0
+    assert abs(d - (w / 10e9 - w / 100e9) * 1e6) < 0.02 * (w / 10e9) * 1e6 + 10
+    # the default (0) keeps the reference's modelled curve
+    dflt = _run(product, 1, models, trace, capacity=18_000)
+    base = _run(reference, 1, models, trace, capacity=18_000)
+    assert dflt.requests == base.requests
