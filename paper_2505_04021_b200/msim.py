@@ -575,10 +575,9 @@ class Device:
         return self.lib.prism_device_stream(self.h) or 0
 
 
-# ---------------------------------------------------------------- schedulers
+# ---------------------------------------------------------------- weight loading
 
 
-@dataclass
 class WeightLoader:
     """prism::WeightLoader — model weight loading for activation (SURVEY
     §8f-2; replaces the modelled
@@ -662,6 +661,10 @@ def measured_activation_curve(gbs: float, fixed_s: float = 0.0, sizes=(16e9, 28e
     return [(float(b), fixed_s + float(b) / (gbs * 1e9)) for b in sizes]
 
 
+# ---------------------------------------------------------------- schedulers
+
+
+@dataclass
 class ResidentModel:
     idle_s: float = 0.0
     ttft_slo_s: float = 0.0
