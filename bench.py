@@ -850,8 +850,16 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        # nccl; PRISM_BENCH_BACKEND=gloo for the single-GPU multi-rank validation
-        dist.init_process_group(os.environ.get("PRISM_BENCH_BACKEND", "nccl"))
+        import torch
+
+        # nccl; PRISM_BENCH_BACKEND=gloo for the single-GPU multi-rank validation.
+        # The rank's GPU is bound before the process group so every NCCL
+        # collective (plan broadcast, barriers, max-over-ranks) runs on it.
+        dev = int(os.environ.get("PRISM_BENCH_DEVICE", os.environ.get("LOCAL_RANK", 0)))
+        torch.cuda.set_device(dev)
+        backend = os.environ.get("PRISM_BENCH_BACKEND", "nccl")
+        kw = {"device_id": torch.device("cuda", dev)} if backend == "nccl" else {}
+        dist.init_process_group(backend, **kw)
     res = gpu_arm(args, rank, world)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
