@@ -472,6 +472,23 @@ int prism_engine_decode_host_async(prism_gpu* g, int engine_index, const void* n
 int prism_engine_wait_host(prism_gpu* g, int engine_index);
 int prism_engine_synchronize(prism_gpu* g, int engine_index);
 
+/* ---- pool-level K2 / K3 over caller-owned block tables ----
+ * For an engine that keeps its own scheduler and slot tables (SURVEY §8b's
+ * suggested kv_append / decode_attn; the reference has no attention,
+ * SPEC.md:278): slot ids are page * tpp + slot of handles from prism_kv_alloc
+ * (pagealloc.hpp:188) in token order. Runs on the pool's device stream
+ * (prism_device_stream); the pool must outlive the handle. */
+typedef struct prism_paged prism_paged;
+int prism_paged_create(const prism_pool* p, int n_layers, int n_q_heads, int n_kv_heads, int head_dim,
+                       prism_paged** out);
+int prism_paged_destroy(prism_paged* pa);
+/* K2: slots device int32 [n_tokens]; k, v device bf16 [layer_end-layer_begin][n_tokens][n_kv][head_dim] */
+int prism_paged_kv_append(prism_paged* pa, int layer_begin, int layer_end, const int32_t* slots, int32_t n_tokens,
+                          const void* k, const void* v);
+/* K3: seq_offsets HOST int32 [n_seqs+1] into slot_ids (device int32); q, out device bf16 [n_seqs][n_q][head_dim] */
+int prism_paged_decode_attention(prism_paged* pa, int layer, const int32_t* seq_offsets, int32_t n_seqs,
+                                 const int32_t* slot_ids, const void* q, void* out, float scale);
+
 /* ---- model weight loading for activation ----
  * Replaces the modelled weight-load latency of activation
  * (ActivationParams::load_latency_s, reference engine.hpp:46-48,

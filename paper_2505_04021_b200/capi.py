@@ -305,6 +305,11 @@ _DEVICE_DECLS = {
     "prism_engine_synchronize": (c_int, [c_void_p, c_int]),
     "prism_engine_decode_host_async": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_float]),
     "prism_engine_wait_host": (c_int, [c_void_p, c_int]),
+    "prism_paged_create": (c_int, [c_void_p, c_int, c_int, c_int, c_int, P(c_void_p)]),
+    "prism_paged_destroy": (c_int, [c_void_p]),
+    "prism_paged_kv_append": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int32, c_void_p, c_void_p]),
+    "prism_paged_decode_attention": (c_int, [c_void_p, c_int, P(c_int32), c_int32, c_void_p, c_void_p, c_void_p,
+                                             c_float]),
     "prism_wloader_create": (c_int, [c_int, c_int, c_uint64, P(c_void_p)]),
     "prism_wloader_destroy": (c_int, [c_void_p]),
     "prism_wloader_load": (c_int, [c_void_p, c_void_p, c_void_p, c_uint64]),

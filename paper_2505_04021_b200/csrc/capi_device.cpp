@@ -11,6 +11,7 @@
 #include "host/pool_state.hpp"
 #include "host/vmm.hpp"
 #include "host/weight_load.hpp"
+#include "host/paged_op.hpp"
 #include "msim/kvcache_device.hpp"
 #include "prism_capi.h"
 #include "capi_handles.hpp"
@@ -512,6 +513,47 @@ int prism_ipc_close(int device, void* dptr) {
         need(dptr, "dptr");
         DevSet g(device);
         rt_check(cudaIpcCloseMemHandle(dptr), "cudaIpcCloseMemHandle");
+    });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- pool-level K2 / K3
+
+struct prism_paged {
+    std::unique_ptr<prism::PagedOp> op;
+};
+
+extern "C" {
+
+int prism_paged_create(const prism_pool* p, int n_layers, int n_q_heads, int n_kv_heads, int head_dim,
+                       prism_paged** out) {
+    return dguard([&] {
+        need(p, "pool");
+        need(out, "out");
+        auto h = std::make_unique<prism_paged>();
+        h->op = prism::make_paged_op(p->pool, n_layers, n_q_heads, n_kv_heads, head_dim);
+        *out = h.release();
+    });
+}
+
+int prism_paged_destroy(prism_paged* pa) {
+    return dguard([&] { delete pa; });
+}
+
+int prism_paged_kv_append(prism_paged* pa, int layer_begin, int layer_end, const int32_t* slots, int32_t n_tokens,
+                          const void* k, const void* v) {
+    return dguard([&] {
+        need(pa, "paged");
+        pa->op->kv_append(layer_begin, layer_end, slots, n_tokens, k, v);
+    });
+}
+
+int prism_paged_decode_attention(prism_paged* pa, int layer, const int32_t* seq_offsets, int32_t n_seqs,
+                                 const int32_t* slot_ids, const void* q, void* out, float scale) {
+    return dguard([&] {
+        need(pa, "paged");
+        pa->op->decode_attention(layer, seq_offsets, n_seqs, slot_ids, q, out, scale);
     });
 }
 

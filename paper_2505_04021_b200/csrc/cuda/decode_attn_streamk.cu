@@ -539,7 +539,10 @@ int k3_trace_read(unsigned long long* out, int n) {
     return m;
 }
 
-void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec) {
+// Ctx: EngineDeviceImpl (the engine's step) or PagedCtx (caller block tables):
+// the same K3 scratch members (prefix staging, workspace, counters, chain).
+template <class Ctx>
+void launch_k3_streamk_t(Ctx& d, AttnArgs a, int n_dec) {
     constexpr int kT = 64;
     static int sms = [] {
         int dev = 0, n = 148;
@@ -618,5 +621,8 @@ void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec) {
     }
     d.k3_chain = true;
 }
+
+void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec) { launch_k3_streamk_t(d, a, n_dec); }
+void launch_k3_streamk(PagedCtx& d, AttnArgs a, int n_dec) { launch_k3_streamk_t(d, a, n_dec); }
 
 }  // namespace prism

@@ -11,6 +11,7 @@
 
 #include "cuda/common.cuh"
 #include "host/engine_device.hpp"
+#include "host/paged_op.hpp"
 #include "host/pool_state.hpp"
 #include "host/vmm.hpp"
 #include "msim/kvcache_device.hpp"
@@ -166,6 +167,45 @@ public:
     std::size_t host_stage_bytes = 0;
     std::vector<cudaEvent_t> host_events;
     cudaEvent_t host_done = nullptr;
+};
+
+// K2 / K3 over CALLER-owned block tables (pool-level op, C-ABI
+// prism_paged_*): an engine that keeps its own scheduler and slot tables
+// (SURVEY §8b's suggested kv_append / decode_attn entry points) uses the
+// pool's pages directly. Runs on the pool's VMM stream (so the VMM's release
+// fences cover its reads); the same K3 scratch members as EngineDeviceImpl.
+struct PagedCtx final : PagedOp {
+    PagedCtx(const msim::pagealloc::KvPool& pool, int n_layers, int n_q, int n_kv, int head_dim);
+    ~PagedCtx() override;
+    PagedCtx(const PagedCtx&) = delete;
+    PagedCtx& operator=(const PagedCtx&) = delete;
+
+    // offsets: HOST int32 [n_seqs + 1], non-decreasing, offsets[0] = 0, every
+    // sequence >= 1 token; slot_ids: DEVICE int32 [offsets[n_seqs]] (page *
+    // tpp + slot, in token order); q / out: device bf16 [n_seqs][n_q][head_dim]
+    void decode_attention(int layer, const std::int32_t* offsets, int n_seqs, const std::int32_t* slot_ids,
+                          const void* q, void* out, float scale) override;
+    // slots: DEVICE int32 [n_tok]; k / v: device bf16 [layer_end - layer_begin][n_tok][n_kv][head_dim]
+    void kv_append(int layer_begin, int layer_end, const std::int32_t* slots, int n_tok, const void* k,
+                   const void* v) override;
+
+    float* attn_workspace(std::size_t floats);
+    int* attn_counters(std::size_t n);
+
+    VmmDevice* vmm = nullptr;
+    cudaStream_t stream = nullptr;
+    KvGeom geom{};
+    int n_q = 0, n_kv = 0, head_dim = 0, group = 0, n_layers = 0;
+    Staging<DecodeDesc> decode_desc;
+    Staging<TokenMeta> token_meta;  // all live (K2 skips dead tokens only in engine steps)
+    Staging<std::int32_t> sk_prefix;
+    std::uint64_t step_serial = 0, sk_step = ~0ull;
+    int sk_total = 0, sk_per_cta = 1, sk_max_parts = 1;
+    bool k3_chain = false;
+    float* workspace = nullptr;
+    std::size_t workspace_floats = 0;
+    int* counters = nullptr;
+    std::size_t counters_n = 0;
 };
 
 EngineDeviceImpl& impl_of(const msim::engine::Engine& eng);

@@ -127,4 +127,28 @@ void synth_decode_q(msim::engine::Engine& eng, int layer, std::uint64_t seed, fl
     PRISM_CUDA(cudaGetLastError());
 }
 
+void PagedCtx::kv_append(int layer_begin, int layer_end, const std::int32_t* slots, int n_tok, const void* k,
+                         const void* v) {
+    if (layer_begin < 0 || layer_end > n_layers || layer_begin >= layer_end) {
+        throw std::out_of_range("paged kv_append: bad layer range");
+    }
+    if (n_tok <= 0) return;
+    if (!slots || !k || !v) throw std::invalid_argument("paged kv_append: null pointer");
+    if ((reinterpret_cast<std::uintptr_t>(k) | reinterpret_cast<std::uintptr_t>(v)) & 15) {
+        throw std::invalid_argument("paged kv_append: k/v must be 16-byte aligned");
+    }
+    PRISM_CUDA(cudaSetDevice(vmm->ordinal()));
+    if (token_meta.cap < static_cast<std::size_t>(n_tok)) {
+        token_meta.ensure(static_cast<std::size_t>(n_tok));
+        for (std::size_t i = 0; i < token_meta.cap; ++i) token_meta.host[i] = TokenMeta{0, 0, 0};  // all live
+        token_meta.upload(token_meta.cap, stream);
+    }
+    k3_chain = false;
+    AppendArgs a{geom, slots, token_meta.dev, static_cast<const uint4*>(k), static_cast<const uint4*>(v),
+                 layer_begin, layer_end - layer_begin, n_tok, 0};
+    const std::uint64_t work = static_cast<std::uint64_t>(n_tok) * n_kv * (head_dim / 8) * 2 * (layer_end - layer_begin);
+    k2_append<false><<<grid_for(work, 256), 256, 0, stream>>>(a);
+    PRISM_CUDA(cudaGetLastError());
+}
+
 }  // namespace prism

@@ -575,6 +575,43 @@ class Device:
         return self.lib.prism_device_stream(self.h) or 0
 
 
+class PagedOp:
+    """Pool-level K2 / K3 over caller-owned block tables (C-ABI prism_paged_*;
+    SURVEY §8b's suggested kv_append / decode_attn): for an engine with its
+    own scheduler. Slot ids are page * tokens_per_page + slot of handles from
+    alloc_kv. Pointers are integers (``tensor.data_ptr()``); everything runs on
+    the pool's device stream (``Device.stream()``)."""
+
+    def __init__(self, pool: KvPool, n_layers: int, n_q_heads: int, n_kv_heads: int, head_dim: int):
+        self.lib, self.pool = pool.lib, pool  # the pool outlives this op
+        self.h = C.c_void_p()
+        self.lib.call("prism_paged_create", pool.h, n_layers, n_q_heads, n_kv_heads, head_dim, C.byref(self.h))
+
+    def close(self):
+        if getattr(self, "h", None) and self.h.value:
+            self.lib.prism_paged_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def kv_append(self, layer_begin: int, layer_end: int, slots: int, n_tokens: int, k: int, v: int) -> None:
+        """K2: slots device int32 [n_tokens]; k / v device bf16 [layers][n_tokens][n_kv][head_dim]."""
+        self.lib.call("prism_paged_kv_append", self.h, layer_begin, layer_end, C.c_void_p(slots), n_tokens,
+                      C.c_void_p(k), C.c_void_p(v))
+
+    def decode_attention(self, layer: int, seq_offsets: Sequence[int], slot_ids: int, q: int, out: int,
+                         scale: float) -> None:
+        """K3: seq_offsets (host) [n_seqs + 1] into the device slot-id array."""
+        n = len(seq_offsets) - 1
+        offs = (C.c_int32 * len(seq_offsets))(*seq_offsets)
+        self.lib.call("prism_paged_decode_attention", self.h, layer, offs, n, C.c_void_p(slot_ids), C.c_void_p(q),
+                      C.c_void_p(out), scale)
+
+
 # ---------------------------------------------------------------- weight loading (SURVEY 8f-2)
 
 
