@@ -86,6 +86,19 @@ def main():
         ts.sort()
         out[f"map_access_{'busy' if busy else 'idle'}"] = {
             "calls": len(ts), "us_p50": round(ts[len(ts) // 2], 1), "us_max": round(ts[-1], 1)}
+    # cuMemSetAccess: 8 chunks in one call vs one call per chunk (GPU idle)
+    for batch in (1, 8):
+        ts = []
+        for rep in range(4):
+            for i, h in enumerate(handles):
+                ck(cu.cuMemMap(int(va) + i * chunk, chunk, 0, h, 0))
+            t0 = time.perf_counter()
+            for i in range(0, n, batch):
+                ck(cu.cuMemSetAccess(int(va) + i * chunk, chunk * batch, [acc], 1))
+            ts.append((time.perf_counter() - t0) * 1e6 / n)
+            ck(cu.cuMemUnmap(va, chunk * n))
+        ts.sort()
+        out[f"set_access_batch{batch}_us_per_chunk"] = round(ts[len(ts) // 2], 1)
     print(json.dumps(out))
 
 
