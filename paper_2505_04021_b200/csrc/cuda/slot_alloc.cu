@@ -43,7 +43,7 @@ constexpr std::uint32_t kAlloc = 1, kFreeList = 2, kFreeRow = 3;
 struct K1Args {
     std::uint32_t* occ;
     std::uint32_t* bits;
-    std::uint32_t vpages, tpp, words;
+    std::uint32_t vpages, tpp, words;  // vpages: pages scanned (the pool's high-water mark, 4-aligned)
     std::uint64_t magic;
     const DevOp* ops;
     int n_ops;
@@ -358,7 +358,12 @@ std::int64_t DevicePool::replay(msim::pagealloc::detail::PoolState& s, std::int3
     freed.ensure(std::max<std::size_t>(s.freed_slots.size(), 1));
     if (!s.freed_slots.empty()) std::memcpy(freed.host, s.freed_slots.data(), s.freed_slots.size() * sizeof(std::int32_t));
     freed.upload(s.freed_slots.size(), stream);
-    K1Args a{occ, bits, vpages, tpp, words, div_magic40(tpp), ops.dev, static_cast<int>(s.ops.size()), freed.dev,
+    // Every page this step's replay can pick was picked by the host allocator
+    // (bit-exact replay), so it lies below the pool's high-water mark; pages
+    // at or above it were never mapped (occupancy 0) and are never chosen:
+    // K1 scans [0, hw) instead of all V virtual pages (C1: ~8K of 85,830).
+    const std::uint32_t scan = static_cast<std::uint32_t>(std::min<std::uint64_t>(vpages, (s.hw + 3) / 4 * 4));
+    K1Args a{occ, bits, scan, tpp, words, div_magic40(tpp), ops.dev, static_cast<int>(s.ops.size()), freed.dev,
              table, out, d_status};
     k1_slot_alloc<<<1, kThreads, 0, stream>>>(a);
     PRISM_CUDA(cudaGetLastError());

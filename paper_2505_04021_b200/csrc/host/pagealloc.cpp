@@ -411,6 +411,7 @@ AllocResult detail::alloc_kv_into(KvPool& pool, PhysicalLedger& ledger, std::uin
         if (needs_map) {
             ++s.mapped;
             s.unmapped.clear(page);
+            s.hw = std::max<std::uint64_t>(s.hw, static_cast<std::uint64_t>(page) + 1);
         }
         // First free slots in ascending order (:225-241).
         std::uint64_t* words = s.page_bits(page);

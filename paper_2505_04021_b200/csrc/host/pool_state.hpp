@@ -170,6 +170,7 @@ struct PoolState {
     std::uint64_t vpages = 0;    // virtual capacity in pages
     std::uint64_t mapped = 0;
     std::uint64_t occupied = 0;
+    std::uint64_t hw = 0;        // 1 + highest page index ever mapped (K1 scans [0, hw) only)
     std::uint32_t words = 0;     // 64-bit bitmap words per page
     PagePlacement placement = PagePlacement::most_occupied_first;
     std::optional<std::uint64_t> cap;
