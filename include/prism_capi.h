@@ -485,6 +485,10 @@ int prism_paged_destroy(prism_paged* pa);
 /* K2: slots device int32 [n_tokens]; k, v device bf16 [layer_end-layer_begin][n_tokens][n_kv][head_dim] */
 int prism_paged_kv_append(prism_paged* pa, int layer_begin, int layer_end, const int32_t* slots, int32_t n_tokens,
                           const void* k, const void* v);
+/* K4: one request's prefill chunk; slot_ids device int32 = its keys 0..first+n_tokens-1 (append the chunk first);
+ * query i attends keys 0..first+i; q, out device bf16 [n_tokens][n_q][head_dim] */
+int prism_paged_prefill_attention(prism_paged* pa, int layer, const int32_t* slot_ids, int32_t first, int32_t n_tokens,
+                                  const void* q, void* out, float scale);
 /* K3: seq_offsets HOST int32 [n_seqs+1] into slot_ids (device int32); q, out device bf16 [n_seqs][n_q][head_dim] */
 int prism_paged_decode_attention(prism_paged* pa, int layer, const int32_t* seq_offsets, int32_t n_seqs,
                                  const int32_t* slot_ids, const void* q, void* out, float scale);

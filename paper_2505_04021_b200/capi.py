@@ -308,6 +308,8 @@ _DEVICE_DECLS = {
     "prism_paged_create": (c_int, [c_void_p, c_int, c_int, c_int, c_int, P(c_void_p)]),
     "prism_paged_destroy": (c_int, [c_void_p]),
     "prism_paged_kv_append": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int32, c_void_p, c_void_p]),
+    "prism_paged_prefill_attention": (c_int, [c_void_p, c_int, c_void_p, c_int32, c_int32, c_void_p, c_void_p,
+                                              c_float]),
     "prism_paged_decode_attention": (c_int, [c_void_p, c_int, P(c_int32), c_int32, c_void_p, c_void_p, c_void_p,
                                              c_float]),
     "prism_wloader_create": (c_int, [c_int, c_int, c_uint64, P(c_void_p)]),

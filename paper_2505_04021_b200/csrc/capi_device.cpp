@@ -549,6 +549,14 @@ int prism_paged_kv_append(prism_paged* pa, int layer_begin, int layer_end, const
     });
 }
 
+int prism_paged_prefill_attention(prism_paged* pa, int layer, const int32_t* slot_ids, int32_t first, int32_t n_tokens,
+                                  const void* q, void* out, float scale) {
+    return dguard([&] {
+        need(pa, "paged");
+        pa->op->prefill_attention(layer, slot_ids, first, n_tokens, q, out, scale);
+    });
+}
+
 int prism_paged_decode_attention(prism_paged* pa, int layer, const int32_t* seq_offsets, int32_t n_seqs,
                                  const int32_t* slot_ids, const void* q, void* out, float scale) {
     return dguard([&] {

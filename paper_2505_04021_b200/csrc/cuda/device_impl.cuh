@@ -188,6 +188,8 @@ struct PagedCtx final : PagedOp {
     // slots: DEVICE int32 [n_tok]; k / v: device bf16 [layer_end - layer_begin][n_tok][n_kv][head_dim]
     void kv_append(int layer_begin, int layer_end, const std::int32_t* slots, int n_tok, const void* k,
                    const void* v) override;
+    void prefill_attention(int layer, const std::int32_t* slot_ids, int first, int n_tokens, const void* q, void* out,
+                           float scale) override;
 
     float* attn_workspace(std::size_t floats);
     int* attn_counters(std::size_t n);

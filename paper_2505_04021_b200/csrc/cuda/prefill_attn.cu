@@ -645,6 +645,33 @@ void prefill_attention(msim::engine::Engine& eng, int layer, const void* q, void
     launch_prefill_attention(impl_of(eng), layer, q, out, scale);
 }
 
+void PagedCtx::prefill_attention(int layer, const std::int32_t* slot_ids, int first, int n_tokens, const void* q,
+                                 void* out, float scale) {
+    if (layer < 0 || layer >= n_layers) throw std::out_of_range("paged prefill_attention: bad layer");
+    if (n_tokens <= 0) return;
+    if (first < 0) throw std::invalid_argument("paged prefill_attention: first must be >= 0");
+    if (!slot_ids || !q || !out) throw std::invalid_argument("paged prefill_attention: null pointer");
+    PRISM_CUDA(cudaSetDevice(vmm->ordinal()));
+    k3_chain = false;
+    PrefillArgs a{};
+    a.g = geom;
+    a.layer = layer;
+    a.q = static_cast<const __nv_bfloat16*>(q);
+    a.out = static_cast<__nv_bfloat16*>(out);
+    a.row = slot_ids;
+    a.first = first;
+    a.chunk = n_tokens;
+    a.scale_log2 = scale * 1.4426950408889634f;
+    a.dbg = k4_debug_words();
+    a.trace = k4_trace_buf();
+    a.rescale_thr = 8.f;
+    if (head_dim == 128) {
+        launch_pf_d<128>(group, a, stream);
+    } else {
+        launch_pf_d<64>(group, a, stream);
+    }
+}
+
 int last_step_prefill_tokens(const msim::engine::Engine& eng) { return impl_of(eng).prefill_chunk; }
 int last_step_prefill_first(const msim::engine::Engine& eng) { return impl_of(eng).prefill_first; }
 std::uint64_t last_step_prefill_request(const msim::engine::Engine& eng) { return impl_of(eng).prefill_request; }

@@ -20,6 +20,12 @@ public:
     // device bf16 [n_seqs][n_q][head_dim]
     virtual void decode_attention(int layer, const std::int32_t* offsets, int n_seqs, const std::int32_t* slot_ids,
                                   const void* q, void* out, float scale) = 0;
+    // K4, one request's prefill chunk: slot_ids DEVICE int32 = the request's
+    // keys 0 .. first + n_tokens - 1 in token order (append the chunk's K/V
+    // first); query i (position first + i) attends keys 0 .. first + i;
+    // q / out: device bf16 [n_tokens][n_q][head_dim]
+    virtual void prefill_attention(int layer, const std::int32_t* slot_ids, int first, int n_tokens, const void* q,
+                                   void* out, float scale) = 0;
     // slots: DEVICE int32 [n_tok]; k / v: device bf16 [layer_end - layer_begin][n_tok][n_kv][head_dim]
     virtual void kv_append(int layer_begin, int layer_end, const std::int32_t* slots, int n_tok, const void* k,
                            const void* v) = 0;

@@ -603,6 +603,12 @@ class PagedOp:
         self.lib.call("prism_paged_kv_append", self.h, layer_begin, layer_end, C.c_void_p(slots), n_tokens,
                       C.c_void_p(k), C.c_void_p(v))
 
+    def prefill_attention(self, layer: int, slot_ids: int, first: int, n_tokens: int, q: int, out: int,
+                          scale: float) -> None:
+        """K4: one request's chunk; slot_ids = its keys 0 .. first + n_tokens - 1 (device int32)."""
+        self.lib.call("prism_paged_prefill_attention", self.h, layer, C.c_void_p(slot_ids), first, n_tokens,
+                      C.c_void_p(q), C.c_void_p(out), scale)
+
     def decode_attention(self, layer: int, seq_offsets: Sequence[int], slot_ids: int, q: int, out: int,
                          scale: float) -> None:
         """K3: seq_offsets (host) [n_seqs + 1] into the device slot-id array."""

@@ -86,3 +86,41 @@ def test_paged_bad_arguments(device):
     with pytest.raises(capi.PrismError):
         op.decode_attention(5, [0, 1], sids.data_ptr(), q.data_ptr(), q.data_ptr(), 1.0)  # layer
     op.close()
+
+
+@pytest.mark.parametrize("n_q,n_kv,d,first,n", [(32, 8, 128, 0, 200), (32, 8, 128, 1000, 512), (14, 2, 64, 77, 130)])
+def test_paged_prefill_matches_torch_causal(device, n_q, n_kv, d, first, n):
+    """K4 through the pool-level op: one request whose first `first` keys are
+    already cached gets an n-token chunk; query i attends keys 0..first+i."""
+    layers = 2
+    token_bytes = 2 * layers * n_kv * d * 2
+    gpu = msim.GpuState(0, 4096)
+    gpu.ledger.attach_device(device)
+    pool = msim.alloc_kvcache(gpu.ledger, "pf", token_bytes, 4096)
+    tpp = pool.tokens_per_page()
+    total = first + n
+    r = msim.alloc_kv(pool, gpu.ledger, total)
+    assert r.ok()
+    sids = torch.tensor([h.page * tpp + h.slot for h in r.handles], dtype=torch.int32, device="cuda")
+    g = torch.Generator(device="cuda").manual_seed(99)
+    k = (torch.rand((layers, total, n_kv, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    v = (torch.rand((layers, total, n_kv, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    q = (torch.rand((n, n_q, d), generator=g, device="cuda") * 2 - 1).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    op = msim.PagedOp(pool, layers, n_q, n_kv, d)
+    torch.cuda.synchronize()
+    op.kv_append(0, layers, sids.data_ptr(), total, k.data_ptr(), v.data_ptr())
+    scale = 1.0 / math.sqrt(d)
+    layer = 1
+    op.prefill_attention(layer, sids.data_ptr(), first, n, q.data_ptr(), out.data_ptr(), scale)
+    device.synchronize()
+    grp = n_q // n_kv
+    kh = k[layer].float().repeat_interleave(grp, dim=1)  # [total][n_q][d]
+    vh = v[layer].float().repeat_interleave(grp, dim=1)
+    s = torch.einsum("ihd,thd->hit", q.float(), kh) * scale  # [n_q][n][total]
+    mask = torch.arange(total, device="cuda")[None, :] <= (first + torch.arange(n, device="cuda"))[:, None]
+    s = s.masked_fill(~mask[None], float("-inf"))
+    ref = torch.einsum("hit,thd->ihd", torch.softmax(s, dim=-1), vh)
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-3 + 1e-2 * ref.abs().max().item(), err
+    op.close()
