@@ -259,6 +259,13 @@ def gpu_arm(args, rank, world):
     steps, warm = args.steps, args.warmup
     mids = placement_for(world, rank)
     dev, gpu, models = setup_gpu(rank, mids, steps * 2 + warm * 2 + 8)
+    # startup reservation (as in page_churn_c2): physical handles for the KV
+    # the warm-up, timed and e2e decode steps will append, plus each pool's
+    # look-ahead window, so maps while serving are cuMemMap + cuMemSetAccess
+    # only (no cuMemCreate behind them)
+    tpp = (2 << 20) // (2 * L * NKV * D * 2)
+    dev.reserve(len(models) * (B_PER_MODEL * (2 * steps + 2 * warm + 8) // tpp + 2 * 256))
+    dev.quiesce()
     stream = torch.cuda.ExternalStream(dev.stream())
     q_bufs, out_bufs = [], []
     for m in models:

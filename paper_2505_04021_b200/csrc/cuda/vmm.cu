@@ -518,7 +518,7 @@ void VmmDevice::worker_main() {
             continue;
         }
         // 3. ready handles
-        if (cache_.size() < cache_target_ && total_locked() < budget_chunks()) {
+        if ((cache_.size() < cache_target_ || reserve_pending_ > 0) && total_locked() < budget_chunks()) {
             ++worker_busy_;
             ++creating_;
             lk.unlock();
@@ -530,11 +530,13 @@ void VmmDevice::worker_main() {
             --creating_;
             if (r == CUDA_SUCCESS) {
                 cache_.push_back(static_cast<std::uint64_t>(h));
+                if (reserve_pending_ > 0) --reserve_pending_;
                 ++stats_.creates;
                 stats_.create_ns_total += ns;
                 trace('C', 1, t0, ns);
             } else {
                 cache_target_ = 0;  // out of memory: stop until asked again
+                reserve_pending_ = 0;
             }
             stats_.background_ns_total += ns;
             --worker_busy_;
@@ -574,7 +576,7 @@ void VmmDevice::forget(std::uint64_t owner) {
 void VmmDevice::prefill_cache(std::uint64_t pages) {
     {
         Lock lk(mu_);
-        cache_target_ = std::max(reserve_target_, (pages + chunk_pages_ - 1) / chunk_pages_);
+        cache_target_ = (pages + chunk_pages_ - 1) / chunk_pages_;
     }
     cv_.notify_one();
 }
@@ -582,8 +584,11 @@ void VmmDevice::prefill_cache(std::uint64_t pages) {
 void VmmDevice::reserve_physical(std::uint64_t pages) {
     {
         Lock lk(mu_);
-        reserve_target_ = (pages + chunk_pages_ - 1) / chunk_pages_;
-        cache_target_ = std::max(cache_target_, reserve_target_);
+        // one-shot: create handles until the cache holds `pages` worth; they
+        // are consumed by later maps and NOT refilled (a standing refill
+        // target would keep the worker creating handles while serving)
+        const std::uint64_t want = (pages + chunk_pages_ - 1) / chunk_pages_;
+        reserve_pending_ = want > cache_.size() ? want - cache_.size() : 0;
     }
     cv_.notify_one();
 }
@@ -594,7 +599,7 @@ void VmmDevice::quiesce() {
     done_cv_.wait(lk, [&] {
         return !failed_.empty() ||
                (worker_busy_ == 0 && urgent_.empty() && hints_.empty() &&
-                !(cache_.size() < cache_target_ && total_locked() < budget_chunks()));
+                !((cache_.size() < cache_target_ || reserve_pending_ > 0) && total_locked() < budget_chunks()));
     });
     check_failed();
 }

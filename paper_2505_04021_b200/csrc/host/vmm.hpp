@@ -198,7 +198,7 @@ private:
     std::map<std::uint64_t, std::uint64_t> ranges_;              // reserved VA base -> end
     std::map<std::uint64_t, std::pair<std::uint64_t, std::uint64_t>> window_;  // owner -> [lo, hi) chunk VAs
     std::uint64_t cache_target_ = 0;   // chunks
-    std::uint64_t reserve_target_ = 0; // chunks: floor of cache_target_ (reserve())
+    std::uint64_t reserve_pending_ = 0; // chunks still to create for reserve_physical() (one-shot)
     std::uint64_t worker_busy_ = 0;
     bool stop_ = false;
     std::string failed_;  // first driver error on the worker (reported to callers)
