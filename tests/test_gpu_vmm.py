@@ -173,8 +173,8 @@ def test_concurrent_pools_with_worker_keep_data(product, device):
 
 def test_startup_reservation_backs_later_maps(product):
     """prism_device_reserve: physical handles for the requested pages are
-    created up front and that many are kept ready (bounded by the ledger's
-    physical budget); the data path is unchanged."""
+    created up front, once (later maps consume them; no standing refill),
+    bounded by the ledger's physical budget; the data path is unchanged."""
     dev = msim.Device(0, lib=product)
     try:
         gpu = msim.GpuState(0, 600, lib=product)
