@@ -389,7 +389,7 @@ typedef struct {
     double background_ns_total; /* worker-thread driver time (all per-page driver calls run there) */
     uint64_t premaps;           /* chunks the worker mapped ahead of need */
     uint64_t premapped_hits;    /* logical maps that revived a chunk mapped ahead */
-    uint64_t batched_unmaps;    /* cuMemUnmap calls covering a run of >1 pages */
+    uint64_t over_budget;       /* urgent maps that found no safe idle chunk and created past the budget */
     uint64_t caller_steals_clean; /* steals that took a pre-mapped page */
     double wait_ns_total;       /* caller time waiting for the worker's queued maps (inside map_ns_total) */
     uint64_t urgent;            /* chunks the worker mapped on demand (not anticipated by the look-ahead) */

@@ -178,7 +178,7 @@ class DeviceStats(C.Structure):
                                 "unmap_ns_p99")] + [(n, c_uint64) for n in ("buffered", "cached", "pending")] + [
         (n, c_double) for n in ("create_ns_total", "map_call_ns_total", "access_ns_total")] + [
         ("access_calls", c_uint64), ("steals", c_uint64), ("steal_ns_total", c_double),
-        ("background_ns_total", c_double)] + [(n, c_uint64) for n in ("premaps", "premapped_hits", "batched_unmaps",
+        ("background_ns_total", c_double)] + [(n, c_uint64) for n in ("premaps", "premapped_hits", "over_budget",
                                                                  "caller_steals_clean")] + [
         ("wait_ns_total", c_double), ("urgent", c_uint64), ("total_chunks", c_uint64), ("chunk_pages", c_uint64)]
 

@@ -132,7 +132,7 @@ int prism_device_stats_get(const prism_device* d, prism_device_stats* out) {
         out->background_ns_total = s.background_ns_total;
         out->premaps = s.premaps;
         out->premapped_hits = s.premapped_hits;
-        out->batched_unmaps = s.batched_unmaps;
+        out->over_budget = s.over_budget;
         out->caller_steals_clean = s.caller_steals_clean;
         out->wait_ns_total = s.wait_ns_total;
         out->urgent = s.urgent;

@@ -51,6 +51,7 @@ struct SkArgs {
     int total_tiles;
     int per_cta;                      // W
     int max_parts;                    // partial slots per pair
+    int* cta_counter;                 // range ticket (zero between the launches that use it)
     unsigned long long* trace;        // PRISM_K3_TRACE: [grid][8] globaltimer stamps, else null
 };
 
@@ -80,7 +81,25 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
     const std::uint64_t v_delta = static_cast<std::uint64_t>(n_kv) * a.g.tpp * D * 2;
     const std::int32_t* T = sk.pair_tiles;
 
-    const int g_begin = blockIdx.x * sk.per_cta;
+    // Forward progress under any residency (MPS limits, green contexts,
+    // other persistent grids): a CTA's tile range comes from a ticket drawn
+    // when the CTA starts, in REVERSE — the first CTA to run owns the last
+    // range. A cut pair is merged by the CTA owning its first part, which
+    // waits only for the CTAs owning the later ranges; those drew earlier
+    // tickets, so they are already resident and (by induction from the last
+    // range, which waits for nobody) finish without waiting on a CTA that
+    // may never be scheduled. The last CTA to draw resets the counter: the
+    // next launch using it is ordered behind this one's completion (stream
+    // order, or the griddepcontrol.wait of the launch in between).
+    __shared__ int s_range;
+    if (tid == 0) {
+        const int t = atomicAdd(sk.cta_counter, 1);
+        if (t == static_cast<int>(gridDim.x) - 1) atomicExch(sk.cta_counter, 0);
+        s_range = static_cast<int>(gridDim.x) - 1 - t;
+    }
+    __syncthreads();
+    const int range = s_range;
+    const int g_begin = range * sk.per_cta;
     const int g_end = min(sk.total_tiles, g_begin + sk.per_cta);
     if (g_begin >= g_end) return;
     k3_stamp(sk.trace, 0);  // CTA running
@@ -252,7 +271,7 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
         const int first_cta = cp_first / sk.per_cta;
         const int last_cta = (cp_end - 1) / sk.per_cta;
         const int parts = last_cta - first_cta + 1;
-        const int part = blockIdx.x - first_cta;
+        const int part = range - first_cta;
         __nv_bfloat16* out = a.out + (static_cast<std::size_t>(b) * n_q + static_cast<std::size_t>(h) * G) * D;
         const std::size_t pslot = static_cast<std::size_t>(cp) * sk.max_parts + part;
         // A cut pair is merged by its FIRST CTA (part 0): that CTA reaches the
@@ -612,7 +631,9 @@ void launch_k3_streamk_t(Ctx& d, AttnArgs a, int n_dec) {
     float* ws = d.attn_workspace(per * d.head_dim + per * 2);
     s.a.part_o = ws;
     s.a.part_ml = ws + per * d.head_dim;
-    s.a.tickets = d.attn_counters(static_cast<std::size_t>(n_pairs));
+    // pair tickets, then two CTA range counters used by alternate launches
+    s.a.tickets = d.attn_counters(static_cast<std::size_t>(n_pairs) + 2);
+    s.cta_counter = s.a.tickets + n_pairs + (d.sk_launches++ & 1);
     chained = chained && d.k3_chain;  // a workspace reallocation breaks the chain
     if (d.head_dim == 128) {
         launch_sk_d<128>(d.group, s, d.stream, sms, chained);

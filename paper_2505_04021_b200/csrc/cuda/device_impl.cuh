@@ -153,6 +153,7 @@ public:
     std::uint64_t sk_step = ~0ull;
     Staging<std::int32_t> sk_prefix;
     int sk_total = 0, sk_per_cta = 1, sk_max_parts = 1;
+    std::uint64_t sk_launches = 0;  // selects the CTA range counter (alternate launches)
     // true while the last operation this engine put on `stream` is a
     // stream-K K3 launch (no K1 / K2 / upload / other kernel since): the next
     // K3 may then be launched as a programmatic dependent (PDL) of it.
@@ -203,6 +204,7 @@ struct PagedCtx final : PagedOp {
     Staging<std::int32_t> sk_prefix;
     std::uint64_t step_serial = 0, sk_step = ~0ull;
     int sk_total = 0, sk_per_cta = 1, sk_max_parts = 1;
+    std::uint64_t sk_launches = 0;  // selects the CTA range counter (alternate launches)
     bool k3_chain = false;
     float* workspace = nullptr;
     std::size_t workspace_floats = 0;

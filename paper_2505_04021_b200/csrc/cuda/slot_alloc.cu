@@ -308,6 +308,11 @@ void destroy_device_pool(DevicePool* p) { delete p; }
 
 DevicePool::DevicePool(const msim::pagealloc::detail::PoolState& s, int device) {
     if (s.tpp > kMaxTpp) throw std::runtime_error("device pool: tokens per page above 1024 is not supported");
+    // K1 replays pick_page's most-occupied-first order (reference
+    // src/pagealloc.cpp:162-170); a lowest-index-first pool would diverge.
+    if (s.placement != msim::pagealloc::PagePlacement::most_occupied_first) {
+        throw std::runtime_error("device pool: the K1 mirror replays most_occupied_first placement only");
+    }
     // slot ids are int32 and div_magic40 is exact while sid * tpp < 2^40.
     if (s.vpages * s.tpp >= (1ull << 31) || s.vpages * s.tpp * s.tpp >= (1ull << 40)) {
         throw std::runtime_error("device pool: slot id range too large for the device block table");

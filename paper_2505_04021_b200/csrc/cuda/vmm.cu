@@ -277,7 +277,9 @@ bool VmmDevice::take_handle(Lock& lk, bool urgent, std::uint64_t& h) {
         return premap_steal && steal_for_worker(lk, h, /*premap=*/true);
     }
     if (steal_for_worker(lk, h)) return true;
-    // Nothing idle to move (the budget shrank under queued maps): past it.
+    // Nothing idle is safe to move (the budget shrank under queued maps, or
+    // every idle chunk was released inside the open step): past the budget.
+    ++stats_.over_budget;
     return create();
 }
 
@@ -391,11 +393,26 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h, bool premap) {
             return true;
         }
         if (idle_.empty() || premap) return false;
-        // Every idle chunk may still be read by queued kernels: fence and
-        // poll until that fence passes.
-        fence_locked();
+        // Every idle chunk may still be read by kernels. Only fences the
+        // CALLER records can make one safe (the engine records one at
+        // begin_step, after every kernel of the earlier steps was launched).
+        // The worker never records a fence: one recorded mid-step, between
+        // the step's completion frees and its K2/K3 launches, would pass at
+        // once and let a chunk those launches still read be unmapped. Poll
+        // while a pending fence covers some idle chunk; otherwise the caller
+        // is inside a step waiting on this map: give up (take_handle then
+        // creates past the budget, counted in stats_.over_budget).
+        const std::uint64_t horizon = fenced_ + fences_.size();
+        bool coverable = false;
+        for (const std::uint64_t v : idle_) {
+            if (chunks_.find(v)->second.epoch < horizon) {
+                coverable = true;
+                break;
+            }
+        }
+        if (!coverable) return false;
         lk.unlock();
-        std::this_thread::sleep_for(std::chrono::microseconds(50));
+        std::this_thread::sleep_for(std::chrono::microseconds(20));
         lk.lock();
     }
     return false;
@@ -427,7 +444,14 @@ bool VmmDevice::map_chunk(Lock& lk, std::uint64_t va, std::uint64_t h, bool urge
         c.handle = 0;
         --mapped_;
         cache_.push_back(h);
-        if (urgent) failed_ = "cuMemMap/cuMemSetAccess failed (" + std::to_string(r) + ")";
+        if (urgent) {
+            failed_ = "cuMemMap/cuMemSetAccess failed (" + std::to_string(r) + ")";
+        } else if (c.refs > 0 && !c.queued) {
+            // a caller mapped a page into this look-ahead chunk meanwhile and
+            // counts it in unready_: retry it as an urgent map
+            urgent_.push_back(va);
+            c.queued = true;
+        }
         hints_.clear();
         if (c.refs == 0) drop_if_empty(it);
         return false;

@@ -370,6 +370,35 @@ AllocResult detail::alloc_kv_into(KvPool& pool, PhysicalLedger& ledger, std::uin
         Access::note(ledger, s.model, AllocEventKind::alloc_fail, res.shortfall_pages);
         return res;
     }
+    std::uint32_t next_unmapped = kNone;
+    if (s.dev && new_pages > 0) {
+        // Every partial slot is consumed before any new page, and each new
+        // page is the lowest unmapped one at that moment, so the pages this
+        // call maps are the new_pages lowest unmapped indices: map them in one
+        // batch, BEFORE any ledger / buffer state is committed, so a device
+        // failure (map_batch throws) leaves the ledger, the pool and the VMM
+        // references exactly as they were.
+        std::vector<std::uint64_t> vas;
+        vas.reserve(new_pages);
+        std::uint32_t p = s.unmapped.find_first();
+        for (std::uint64_t k = 0; k < new_pages && p != kNone; ++k) {
+            vas.push_back(s.va + static_cast<std::uint64_t>(p) * s.dev->page_bytes());
+            p = s.unmapped.find_next(static_cast<std::uint64_t>(p) + 1);
+        }
+        next_unmapped = p;
+        try {
+            s.dev->map_batch(vas.data(), vas.size(), std::min<std::uint64_t>(new_pages, ledger.buffer_pages()));
+        } catch (...) {
+            // map_batch took a reference on every page before waiting
+            for (const std::uint64_t va : vas) {
+                try {
+                    s.dev->unmap(va);
+                } catch (...) {
+                }
+            }
+            throw;
+        }
+    }
     res.buffer_hits = Access::take_buffer(ledger, new_pages);
     res.pages_mapped = new_pages - res.buffer_hits;
     if (res.buffer_hits) Access::note(ledger, s.model, AllocEventKind::buffer_hit, res.buffer_hits);
@@ -381,18 +410,8 @@ AllocResult detail::alloc_kv_into(KvPool& pool, PhysicalLedger& ledger, std::uin
     std::uint64_t remaining = num_tokens;
     const std::uint64_t last_word_bits = s.tpp - static_cast<std::uint64_t>(s.words - 1) * 64;
     if (s.dev && new_pages > 0) {
-        // Every partial slot is consumed before any new page, and each new
-        // page is the lowest unmapped one at that moment, so the pages this
-        // call maps are the new_pages lowest unmapped indices: map them in one
-        // batch (contiguous runs share a cuMemSetAccess).
         std::vector<std::uint64_t> vas;
-        vas.reserve(new_pages);
-        std::uint32_t p = s.unmapped.find_first();
-        for (std::uint64_t k = 0; k < new_pages && p != kNone; ++k) {
-            vas.push_back(s.va + static_cast<std::uint64_t>(p) * s.dev->page_bytes());
-            p = s.unmapped.find_next(static_cast<std::uint64_t>(p) + 1);
-        }
-        s.dev->map_batch(vas.data(), vas.size(), res.buffer_hits);
+        std::uint32_t p = next_unmapped;
         // The pool is growing: its next maps will be the following lowest
         // unmapped pages. Hand them to the device's worker thread to map
         // (and make accessible) ahead of time, so those maps become revives.

@@ -64,7 +64,7 @@ struct VmmStats {
     std::uint64_t unmaps = 0;         // logical page unmaps
     std::uint64_t driver_unmaps = 0;  // cuMemUnmap calls (chunks)
     std::uint64_t steals = 0;         // idle chunks moved to another VA
-    std::uint64_t batched_unmaps = 0; // unused (kept for ABI)
+    std::uint64_t over_budget = 0;    // urgent maps that found no safe idle chunk and created past the budget
     std::uint64_t premaps = 0;        // chunks mapped by the look-ahead
     std::uint64_t urgent = 0;         // chunks mapped on demand
     std::uint64_t caller_steals_clean = 0;  // steals that took a look-ahead chunk
