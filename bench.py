@@ -21,10 +21,13 @@ roofline: K3, algorithmic bytes (K+V rows of every context token + q + out)
           model step's 32 back-to-back K3 launches in the timed region
           (time / 32, so inter-launch gaps count against the kernel);
           against MEASURED_PEAKS.json hbm_gbs
-cpu_baseline: reference engine::step (oracle/_ref, the reference compiled
-          from its sources) for the allocation half + this repo's CPU port of
-          paged attention (oracle/restate) on a bounded sample, N=1 rank 0 only
---impl reference: that CPU path as the timed arm (no GPU work).
+cpu_baseline: 3 full C1 steps (after 1 warm-up) of the reference arm below,
+          rank 0 at N=1 only
+--impl reference: the CPU path of the same step for the declared --steps /
+          --warmup: the reference's engine::step (oracle/_ref, the reference
+          compiled from its sources) + this repo's fp32 CPU attention port
+          (oracle/restate; the reference has no attention) over all
+          sequences, layers and models, on the same 85,830-page ledger.
 """
 from __future__ import annotations
 
@@ -49,6 +52,8 @@ L, NQ, NKV, D = 32, 32, 8, 128
 B_PER_MODEL = 64
 CTX = 2048
 MODELS_PER_GPU = 2
+LEDGER_PAGES = 85_830          # B200 ledger (~180 GB / 2 MiB), both arms
+WEIGHT_BYTES = 16_060_000_000  # llama3.1-8b weights, accounted in the ledger (7,659 pages per model)
 WORKLOAD = ("C1: 2 x Llama-3-8B-shaped models (32L, 32q/8kv heads, d=128) time-sharing 1 B200; "
             "64 decode seqs x 2K ctx per model; prompts from a seeded Poisson trace, admitted before timing")
 
@@ -66,54 +71,94 @@ def measured_peaks():
 
 
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    """SM clock + clock-event (throttle) reasons sampled DURING the timed
+    region: a thread polls NVML every ~2 ms (an `nvidia-smi -lms` child
+    needs longer to start than the ~0.1 s timed region runs, so it recorded
+    nothing in r01). summary() keeps the samples inside [mark_start(),
+    mark_end()] (all samples when no marks were set)."""
 
-    def __init__(self, index: int):
-        self.index = index
-        self.proc = None
-        self.lines = []
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+    def __init__(self, cuda_index: int, period_s: float = 0.002):
+        self.cuda_index = cuda_index
+        self.period = period_s
+        self.samples = []  # (t_ns, sm_mhz, reason_mask)
+        self.sm_max = None
+        self.t0 = self.t1 = None
+        self.error = None
+        self._stop = threading.Event()
+        self._thread = None
+
+    def _handle(self, nv):
+        try:
+            import torch
+
+            p = torch.cuda.get_device_properties(self.cuda_index)
+            bus = f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(self.cuda_index)
+
+    def _run(self, nv, h, ready):
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((time.monotonic_ns(), float(sm), int(mask)))
+            except Exception as e:  # keep the first error for the record
+                self.error = self.error or repr(e)
+            ready.set()
+            time.sleep(self.period)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "50"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except Exception:
-            self.proc = None
+            import pynvml as nv
+
+            nv.nvmlInit()
+            h = self._handle(nv)
+            self.sm_max = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            self._nv = nv
+            ready = threading.Event()
+            self._thread = threading.Thread(target=self._run, args=(nv, h, ready), daemon=True)
+            self._thread.start()
+            ready.wait(2.0)
+        except Exception as e:
+            self.error = repr(e)
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def mark_start(self):
+        self.t0 = time.monotonic_ns()
+
+    def mark_end(self):
+        self.t1 = time.monotonic_ns()
 
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self._thread:
+            self._thread.join(timeout=2.0)
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 6:
-                continue
-            try:
-                sm.append(float(parts[0]))
-                mx = float(parts[1])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[2:6]):
-                if v.lower().startswith("active"):
-                    reasons.add(n)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        lo = self.t0 if self.t0 is not None else 0
+        hi = self.t1 if self.t1 is not None else 1 << 62
+        inside = [s for s in self.samples if lo <= s[0] <= hi]
+        reasons = set()
+        if inside:
+            nv = self._nv
+            for name, attr in self.REASONS:
+                bit = getattr(nv, attr, 0)
+                if any(m & bit for _, _, m in inside):
+                    reasons.add(name)
+        sm = [s[1] for s in inside]
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.sm_max,
+               "sm_mhz_min": min(sm) if sm else None, "reasons": sorted(reasons), "samples": len(sm),
+               "source": "nvml, ~2 ms polling inside the timed region"}
+        if self.error:
+            out["error"] = self.error
+        return out
 
 
 # ---------------------------------------------------------------- workload
@@ -139,15 +184,17 @@ def placement_for(world: int, rank: int):
     return [m.spec.model_id for m in cluster.shard(demands, plan, rank)]
 
 
-def c1_requests(mids):
-    """Per model: 64 requests from a seeded Poisson trace (prompt ~2K)."""
+def c1_requests(mids, lib=None):
+    """Per model: 64 requests from a seeded Poisson trace (prompt ~2K).
+    lib: the library that synthesises it (the reference arm passes the
+    compiled reference so the product library is never loaded there)."""
     from paper_2505_04021_b200 import msim
 
     out = []
     for mid in mids:
         prof = msim.ModelProfile(mid, [(0.0, 60.0, 30.0)], prompt_median=CTX - 1, prompt_sigma=0.0,
                                  output_median=256, output_sigma=0.4)
-        trace = [e for e in msim.synth_trace([prof], TRACE_SEED) if e.model_id == mid][:B_PER_MODEL]
+        trace = [e for e in msim.synth_trace([prof], TRACE_SEED, lib=lib) if e.model_id == mid][:B_PER_MODEL]
         out.append((mid, trace))
     return out
 
@@ -156,7 +203,7 @@ class Model:
     def __init__(self, gpu, mid, trace, max_steps):
         from paper_2505_04021_b200 import msim
 
-        spec = msim.ModelSpec.llm(mid, L, NQ, NKV, D, weight_bytes=0, chunk_size=4096)
+        spec = msim.ModelSpec.llm(mid, L, NQ, NKV, D, weight_bytes=WEIGHT_BYTES, chunk_size=4096)
         act = gpu.activate(spec)
         assert act is not None
         gpu.finish_activation(act.engine_index)
@@ -175,12 +222,10 @@ def setup_gpu(rank: int, mids, max_steps: int):
     from paper_2505_04021_b200 import msim
 
     dev = msim.Device(torch.cuda.current_device())
-    tpp = (2 << 20) // (2 * L * NKV * D * 2)
-    # contexts grow by one token per decode step: B_PER_MODEL prefill steps
-    # (earlier requests decode meanwhile) + every later step of the run
-    grow = B_PER_MODEL + max_steps
-    pages = len(mids) * (B_PER_MODEL * (CTX + grow + tpp) // tpp + 64)
-    gpu = msim.GpuState(rank, pages + 64)
+    # the reference's B200-sized ledger (the CPU arm uses the same one):
+    # every pool's virtual capacity V = 85,830 pages (finish_activation,
+    # reference src/engine.cpp:326-328), weights accounted at their real size
+    gpu = msim.GpuState(rank, LEDGER_PAGES)
     gpu.ledger.attach_device(dev)
     gpu.ledger.refill_buffer(8)
     models = [Model(gpu, mid, trace, max_steps) for mid, trace in c1_requests(mids)]
@@ -301,10 +346,12 @@ def gpu_arm(args, rank, world):
         if ncu_timed:
             torch.cuda.cudart().cudaProfilerStart()
         t_mark = time.monotonic_ns()
+        clk.mark_start()
         start.record(stream)
         launches = run_steps(models, steps, q_bufs, out_bufs, scale, events, kv_bufs)
         end.record(stream)
         end.synchronize()
+        clk.mark_end()
         if ncu_timed:
             torch.cuda.cudart().cudaProfilerStop()
     if os.environ.get("PRISM_VMM_TRACE"):
@@ -356,7 +403,8 @@ def gpu_arm(args, rank, world):
         "data": "synthetic (seeded hash K/V/Q content; prompts from seeded Poisson trace)",
         "config": {"workload": WORKLOAD, "models_per_gpu": MODELS_PER_GPU, "decode_seqs_per_model": B_PER_MODEL,
                    "ctx": CTX, "layers": L, "q_heads": NQ, "kv_heads": NKV, "head_dim": D, "page_bytes": 2 << 20,
-                   "tokens_per_page": 16, "parallelism": f"model placement, {world} GPU(s), no collective",
+                   "tokens_per_page": 16, "ledger_pages": LEDGER_PAGES,
+                   "weight_pages_per_model": math.ceil(WEIGHT_BYTES / (2 << 20)), "parallelism": f"model placement, {world} GPU(s), no collective",
                    "l2": "inputs larger than L2 (32 GiB KV read per step)"},
         "e2e": e2e,
         "gpu_launches": launches,
@@ -744,79 +792,137 @@ def slo_c5(copies=6, horizon=240.0):
     return out
 
 
-def cpu_arm(args, sample_seqs=8, sample_layers=4, ref_steps=4):
-    """CPU path of the same step: reference engine::step (allocation half, the
-    reference itself) + CPU paged attention port (all host threads) on a
-    bounded sample, scaled to the full step."""
+def loaded_native_libs():
+    """In-repo / torch-extension shared objects mapped into this process."""
+    out = set()
+    try:
+        with open("/proc/self/maps") as f:
+            for ln in f:
+                path = ln.split()[-1] if ln.strip() else ""
+                if path.endswith(".so") and (path.startswith(ROOT) or "torch_extensions" in path):
+                    out.add(os.path.relpath(path, ROOT))
+    except OSError:
+        pass
+    return sorted(out)
+
+
+def reference_arm(args):
+    """--impl reference: the CPU path of the SAME C1 step, measured for the
+    declared --warmup / --steps (no extrapolation):
+      * allocation half: the reference's own engine::step (oracle/_ref, the
+        reference compiled from its sources; one thread, as the reference is
+        single-threaded per ledger) for both models on the 85,830-page B200
+        ledger (pools with V = 85,830, reference src/engine.cpp:326-328);
+      * attention half: this repo's fp32 CPU port of paged GQA decode
+        attention (oracle/restate, all host threads) for all 64 sequences x
+        32 layers x 2 models, reading K/V through the slot ids of the
+        reference's own block tables (EngineRequest.kv) from a host copy of
+        each pool's pages. The reference itself has no attention
+        (SPEC.md:278), so this half is a port, labelled as such.
+    The trace is synthesised by the reference library too: libprism_b200.so
+    is never loaded (checked from /proc/self/maps, reported)."""
     import numpy as np
 
     import oracle
     from paper_2505_04021_b200 import msim
 
-    cores = os.cpu_count() or 1
-    # (1) allocation half: the reference's own engine::step on a B200-sized
-    # ledger (85,830 pages -> pools with V = 85,830 as finish_activation sets).
-    alloc_ms = None
-    if oracle.have_reference():
-        ref = oracle.reference()
-        gpu = msim.GpuState(0, 85830, lib=ref)
-        engines = []
-        for mid, trace in c1_requests(model_ids(1)):
-            spec = msim.ModelSpec.llm(mid, L, NQ, NKV, D, weight_bytes=16_060_000_000, chunk_size=4096)
-            act = gpu.activate(spec)
-            gpu.finish_activation(act.engine_index)
-            e = gpu.engine(act.engine_index)
-            for i, ev in enumerate(trace):
-                e.push(i + 1, ev.prompt_tokens, 10_000)
-            while e.counts()[1] or any(r.prompt_done < r.prompt_tokens for r in e.batch()):
-                e.step()
-            engines.append(e)
-        e0 = [e.step() for e in engines]  # first decode
-        t0 = time.perf_counter()
-        for _ in range(ref_steps):
-            for e in engines:
-                e.step()
-        alloc_ms = (time.perf_counter() - t0) * 1e3 / ref_steps
-    # (2) attention half: CPU port over a host copy of the paged layout.
+    t_all = time.perf_counter()
+    ref = oracle.reference()
     lib = oracle.restate()
-    tpp = 16
+    cores = os.cpu_count() or 1
+    tpp = (2 << 20) // (2 * L * NKV * D * 2)
     page_bytes = 2 << 20
-    n_pages = sample_seqs * CTX // tpp
-    pool = np.zeros(n_pages * page_bytes // 2, dtype=np.uint16)
+    gpu = msim.GpuState(0, LEDGER_PAGES, lib=ref)
+    engines = []
+    for mid, trace in c1_requests(model_ids(1), lib=ref):
+        spec = msim.ModelSpec.llm(mid, L, NQ, NKV, D, weight_bytes=WEIGHT_BYTES, chunk_size=4096)
+        act = gpu.activate(spec)
+        gpu.finish_activation(act.engine_index)
+        e = gpu.engine(act.engine_index)
+        for i, ev in enumerate(trace):
+            e.push(i + 1, ev.prompt_tokens, 1_000_000)
+        while e.counts()[1] or any(r.prompt_done < r.prompt_tokens for r in e.batch()):
+            e.step()
+        engines.append(e)
+
+    def table_of(e):
+        sids, ctx = [], []
+        for r in e.batch():
+            buf, n = e.request_kv_raw(r.id)
+            h = np.frombuffer(buf, dtype=np.uint32, count=3 * n).reshape(n, 3)
+            sids.append((h[:, 1].astype(np.int64) * tpp + h[:, 2]).astype(np.int32))
+            ctx.append(n)
+        rows = np.zeros(len(ctx), dtype=np.int64)
+        rows[1:] = np.cumsum(ctx[:-1])
+        return np.concatenate(sids), rows, np.asarray(ctx, dtype=np.int32)
+
+    # host copies of each pool's pages, sized for the whole run's growth
+    grow_pages = (args.warmup + args.steps + 2) * B_PER_MODEL // tpp + 16
+    pools, shared = [], False
+    need = [int(table_of(e)[0].max()) // tpp + 1 + grow_pages for e in engines]
+    avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+    if sum(need) * page_bytes > 0.7 * avail:  # one buffer for both models (same shape) if RAM is short
+        shared = True
+        buf = np.empty(max(need) * page_bytes // 2, dtype=np.uint16)
+        pools = [buf, buf]
+    else:
+        pools = [np.empty(n * page_bytes // 2, dtype=np.uint16) for n in need]
     rng = np.random.default_rng(SEED)
-    pool[:] = rng.integers(0x3c00, 0x3f80, size=pool.size, dtype=np.uint16)  # bf16 values in [~0.0078, 1)
-    # interleave sequences across pages like most-occupied-first packing does
-    table = np.arange(sample_seqs * CTX, dtype=np.int32).reshape(CTX, sample_seqs).T.copy().reshape(-1)
-    rows = (np.arange(sample_seqs, dtype=np.int64) * CTX)
-    ctx = np.full(sample_seqs, CTX, dtype=np.int32)
-    q = rng.integers(0x3c00, 0x3f80, size=sample_seqs * NQ * D, dtype=np.uint16)
-    out = np.zeros(sample_seqs * NQ * D, dtype=np.float32)
-    lib.po_paged_attention_cpu(pool.ctypes.data, page_bytes, tpp, NKV, D, 0, table.ctypes.data, rows.ctypes.data,
-                               ctx.ctypes.data, sample_seqs, q.ctypes.data, NQ, 1 / math.sqrt(D),
-                               out.ctypes.data, cores)  # warm
+    page = rng.integers(0x3c00, 0x3f80, size=page_bytes // 2, dtype=np.uint16)  # bf16 in [~0.0078, 1)
+    for pbuf in ({id(p): p for p in pools}).values():
+        pbuf.reshape(-1, page_bytes // 2)[:] = page
+    q = [rng.integers(0x3c00, 0x3f80, size=B_PER_MODEL * NQ * D, dtype=np.uint16) for _ in engines]
+    out = np.zeros(B_PER_MODEL * NQ * D, dtype=np.float32)
+    scale = 1 / math.sqrt(D)
+    alloc_s = attn_s = 0.0
+
+    def step():
+        nonlocal alloc_s, attn_s
+        t0 = time.perf_counter()
+        for e in engines:
+            e.step()  # the reference's engine::step: one decode token per request
+        t1 = time.perf_counter()
+        for e, pool, qq in zip(engines, pools, q):
+            table, rows, ctx = table_of(e)
+            if (int(table.max()) // tpp + 1) * page_bytes > pool.nbytes:
+                raise RuntimeError("reference arm: host pool too small for the run's growth")
+            for layer in range(L):
+                lib.po_paged_attention_cpu(pool.ctypes.data, page_bytes, tpp, NKV, D, layer, table.ctypes.data,
+                                           rows.ctypes.data, ctx.ctypes.data, len(ctx), qq.ctypes.data, NQ, scale,
+                                           out.ctypes.data, cores)
+        t2 = time.perf_counter()
+        alloc_s += t1 - t0
+        attn_s += t2 - t1
+
+    setup_s = time.perf_counter() - t_all
+    for _ in range(args.warmup):
+        step()
+    alloc_s = attn_s = 0.0
     t0 = time.perf_counter()
-    for layer in range(sample_layers):
-        lib.po_paged_attention_cpu(pool.ctypes.data, page_bytes, tpp, NKV, D, layer % L, table.ctypes.data,
-                                   rows.ctypes.data, ctx.ctypes.data, sample_seqs, q.ctypes.data, NQ,
-                                   1 / math.sqrt(D), out.ctypes.data, cores)
-    attn_ms_sample = (time.perf_counter() - t0) * 1e3
-    # scale: sample covers sample_seqs seqs x sample_layers layers of one model
-    scale = (B_PER_MODEL / sample_seqs) * (L / sample_layers) * MODELS_PER_GPU
-    attn_ms = attn_ms_sample * scale
-    step_ms = attn_ms + (alloc_ms or 0.0)
-    tokens_per_step = MODELS_PER_GPU * B_PER_MODEL
-    return {
-        "value": round(tokens_per_step / (step_ms / 1e3), 2),
-        "unit": "tokens/s",
-        "cores": cores,
-        "kind": "port",
-        "sample": (f"reference engine::step (oracle/_ref, 1 thread) x {MODELS_PER_GPU} models x {ref_steps} decode "
-                   f"steps at V=85,830 pages = {alloc_ms and round(alloc_ms, 2)} ms/step; CPU paged attention port "
-                   f"(oracle/restate, fp32, {cores} threads) on {sample_seqs} seqs x {CTX} ctx x {sample_layers} "
-                   f"layers = {round(attn_ms_sample, 1)} ms, scaled x{scale:g} to the full step"),
-        "alloc_ms_per_step": alloc_ms and round(alloc_ms, 3),
-        "attention_ms_per_step": round(attn_ms, 2),
-    }
+    for _ in range(args.steps):
+        step()
+    sec = time.perf_counter() - t0
+    tokens = args.steps * len(engines) * B_PER_MODEL
+    value = tokens / sec
+    native = loaded_native_libs()
+    base = {"value": round(value, 2), "unit": "tokens/s", "cores": cores, "kind": "port",
+            "label": "this repo's fp32 CPU attention port + the reference allocator (engine::step)",
+            "sample": (f"the full C1 step for {args.steps} timed steps after {args.warmup} warm-up steps: reference "
+                       f"engine::step (oracle/_ref, 1 thread) x {len(engines)} models on the {LEDGER_PAGES}-page "
+                       f"ledger + CPU paged attention port (oracle/restate, fp32, {cores} threads) over all "
+                       f"{B_PER_MODEL} seqs x {L} layers x {len(engines)} models through the reference's block tables"
+                       + ("; both models' pages in one shared host buffer (host RAM)" if shared else "")),
+            "alloc_ms_per_step": round(alloc_s * 1e3 / args.steps, 3),
+            "attention_ms_per_step": round(attn_s * 1e3 / args.steps, 2)}
+    return {"metric": METRIC, "value": base["value"], "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(sec * 1e3 / args.steps, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (CPU)",
+            "data": "synthetic", "impl": "reference", "cpu_baseline": base,
+            "config": {"workload": WORKLOAD, "parallelism": "CPU, rank 0", "ledger_pages": LEDGER_PAGES,
+                       "weight_pages_per_model": math.ceil(WEIGHT_BYTES / (2 << 20))},
+            "e2e": {"value": base["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "native_so_loaded": native, "setup_s": round(setup_s, 2),
+            "wall_s": round(time.perf_counter() - t_all, 2)}
 
 
 # ---------------------------------------------------------------- main
@@ -839,21 +945,7 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        t0 = time.perf_counter()
-        # The CPU arm times its own bounded sample (the reference's engine::step
-        # after a first untimed decode step, the attention port after a
-        # warm-up pass), independent of --steps / --warmup, so the whole run
-        # stays within a minute or two.
-        base = cpu_arm(args)
-        res = {"metric": METRIC, "value": base["value"], "unit": "tokens/s", "n_gpus": args.gpus,
-               "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(MODELS_PER_GPU * B_PER_MODEL
-                                                                                  / base["value"] * 1e3, 3),
-               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 (CPU)",
-               "data": "synthetic", "config": {"workload": WORKLOAD, "parallelism": "CPU, rank 0"},
-               "impl": "reference", "cpu_baseline": base,
-               "e2e": {"value": base["value"], "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-               "wall_s": round(time.perf_counter() - t0, 2)}
-        print(json.dumps(res))
+        print(json.dumps(reference_arm(args)))
         return
 
     if world > 1:
@@ -873,7 +965,8 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
             try:
-                res["cpu_baseline"] = cpu_arm(args)
+                # a bounded sample of the reference arm: 3 full C1 steps after 1 warm-up step
+                res["cpu_baseline"] = reference_arm(argparse.Namespace(gpus=1, steps=3, warmup=1))["cpu_baseline"]
             except Exception as e:  # reported, never substituted for the GPU number
                 res["cpu_baseline"] = {"error": str(e)}
         if world == 1 and not args.no_churn:

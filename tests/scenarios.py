@@ -223,6 +223,71 @@ def engine_trace(lib, name, seed, capacity, models, rate, horizon, prompt, outpu
                 final_free=gpu.ledger.free_pages(), end_us=now)
 
 
+# C1 exactly as bench.py times it, on the B200-sized ledger: two
+# llama3.1-8b pools (weights accounted, 7,659 pages each) on 85,830 pages,
+# so every pool's V = 85,830 (reference src/engine.cpp:326-328); 64 prompts
+# of 2,047 tokens per model from the seeded C1 trace, prefilled in 4,096-token
+# chunks (model A, then model B), then `decode_steps` decode steps
+# alternating A / B. The reference runs it through its own engine::step.
+C1_FULL = dict(capacity=85_830, decode_steps=60, batch=64, ctx=2048, chunk=4096, weight_bytes=16_060_000_000)
+
+
+def c1_full_ledger(lib, capacity, decode_steps, batch, ctx, chunk, weight_bytes, device=None, on_step=None):
+    gpu = msim.GpuState(0, capacity, lib=lib)
+    if device is not None:
+        gpu.ledger.attach_device(device)
+    gpu.ledger.set_recording(True)
+    engines = []
+    for mid in ("llama3-8b#0", "llama3-8b#1"):
+        prof = msim.ModelProfile(mid, [(0.0, 60.0, 30.0)], prompt_median=ctx - 1, prompt_sigma=0.0,
+                                 output_median=256, output_sigma=0.4)
+        trace = [e for e in msim.synth_trace([prof], 42, lib=lib) if e.model_id == mid][:batch]
+        spec = msim.ModelSpec.llm(mid, 32, 32, 8, 128, weight_bytes=weight_bytes, chunk_size=chunk)
+        act = gpu.activate(spec)
+        gpu.finish_activation(act.engine_index)
+        e = gpu.engine(act.engine_index)
+        if device is not None:
+            e.attach_device(max_decode_batch=batch, max_step_tokens=chunk + batch + 8)
+        for i, ev in enumerate(trace):
+            e.push(i + 1, ev.prompt_tokens, 1_000_000)
+        engines.append((mid, e))
+    outcomes, step_handles = [], []
+
+    def one(mid, e):
+        before = {r.id: r.n_slots for r in e.batch()}
+        o = e.step()
+        outcomes.append([mid, o.duration_us, o.chunk_tokens, o.decode_tokens, o.first_tokens, o.completions,
+                         o.preemptions, o.pages_mapped_direct, o.prefill_paused])
+        # the step's new handles (per request, in admit order): the handle stream
+        new = []
+        for r in e.batch():
+            k = r.n_slots - before.get(r.id, 0)
+            if k:
+                buf, n = e.request_kv_raw(r.id)
+                new.append([r.id, [(s.page, s.slot) for s in buf[n - k:n]]])
+        step_handles.append(digest(new))
+        if on_step is not None:
+            on_step(mid, e, new)
+
+    for mid, e in engines:
+        while e.counts()[1] or any(r.prompt_done < r.prompt_tokens for r in e.batch()):
+            one(mid, e)
+    for _ in range(decode_steps):
+        for mid, e in engines:
+            one(mid, e)
+    gpu.ledger.check_invariants()
+    tables = {}
+    for mid, e in engines:
+        for r in e.batch():
+            buf, n = e.request_kv_raw(r.id)
+            tables[f"{mid}/{r.id}"] = digest([(s.page, s.slot) for s in buf[:n]])
+    events = [[ev.time_us, ev.model_id, ev.kind, ev.pages] for ev in gpu.ledger.events()]
+    return dict(steps=len(outcomes), outcome_digest=digest(outcomes), handle_stream_digest=digest(step_handles),
+                event_digest=digest(events), events=len(events), table_digest=digest(sorted(tables.items())),
+                mapped=gpu.ledger.mapped_pages(), free=gpu.ledger.free_pages(),
+                engines=engines, gpu=gpu)
+
+
 # ---------------------------------------------------------------- placement
 
 PLACEMENT_CASES = [

@@ -58,3 +58,14 @@ def test_admission(product, golden, i):
 @pytest.mark.parametrize("i", range(len(S.TRACE_CASES)))
 def test_traces(product, golden, i):
     assert _norm(S.trace_case(product, **S.TRACE_CASES[i])) == golden["traces"][i]
+
+
+def test_c1_full_b200_ledger(product, golden):
+    """C1 exactly as bench.py times it, on the 85,830-page B200 ledger (every
+    pool's V = 85,830): outcomes, per-step handle stream, events and block
+    tables equal the compiled reference's."""
+    got = S.c1_full_ledger(product, **S.C1_FULL)
+    ref = golden["c1_full_ledger"]
+    for k, v in ref.items():
+        assert _norm(got[k]) == v, k
+    assert ref["steps"] >= 2 * (64 + 50)

@@ -46,6 +46,8 @@ def main() -> None:
         "eviction": scenarios.eviction_cases(ref),
         "admission": [scenarios.admission_case(ref, **c) for c in scenarios.ADMISSION_CASES],
         "traces": [scenarios.trace_case(ref, **c) for c in scenarios.TRACE_CASES],
+        "c1_full_ledger": {k: v for k, v in scenarios.c1_full_ledger(ref, **scenarios.C1_FULL).items()
+                           if k not in ("engines", "gpu")},
     }
     path = os.path.join(OUT, "reference_golden.json")
     with open(path, "w") as f:
