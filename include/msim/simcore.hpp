@@ -15,7 +15,8 @@
 //   * t = 0: place_models (Algorithm 1) over all models with their demand
 //     rates; every placed model is activated on its GPU (activation_done
 //     after init + realign + load latency);
-//   * arrival: the request joins its model's engine queue; a model with no
+//   * arrival: the request joins its GPU's shared queue (Algorithm 2, see
+//     LocalScheduler; FIFO: its model's engine queue); a model with no
 //     engine is activated on the lowest-KVPR GPU whose free pages fit its
 //     weights (activate_on_arrival), else it waits for a later tick;
 //   * a GPU runs one iteration at a time (SPEC enginemodel, Open Questions):
@@ -64,8 +65,26 @@ struct ModelEntry {
 //                    weight load).
 enum class Policy { prism = 0, mux_flexible = 1, static_partition = 2, qlm_timeshare = 3 };
 
+// Local (per-GPU) scheduler ([MODULE] local_sched):
+//   moore_hodgson  Algorithm 2: every arrival for a resident model joins ONE
+//                  shared queue per GPU; on every arrival, iteration boundary
+//                  and activation the GPU runs admission::moore_hodgson over
+//                  it, then admission::dispatch hands admitted requests to
+//                  their engines in deadline order through a gate that only
+//                  lets IMMEDIATELY-runnable requests through (the engine has
+//                  no queued or in-flight prefill; the pool's
+//                  allocatable_tokens covers the first chunk, next_chunk_need
+//                  semantics, plus the engine's reserved_pages), and
+//                  admission::requeue_deferred merges the rest back;
+//   fifo           per-model FIFO: arrivals go straight into their engine's
+//                  local queue (the baselines' admission; SPEC property 10's
+//                  comparison point).
+// Policy::prism uses `local`; the baseline policies always use fifo.
+enum class LocalScheduler { moore_hodgson = 0, fifo = 1 };
+
 struct SimConfig {
     Policy policy = Policy::prism;
+    LocalScheduler local = LocalScheduler::moore_hodgson;
     int n_gpus = 1;
     std::uint64_t capacity_pages = 0;  // per GPU
     std::uint64_t page_bytes = 2ull << 20;
@@ -101,6 +120,8 @@ struct SimMetrics {
     std::uint64_t activations = 0;
     std::uint64_t evictions = 0;
     std::uint64_t preemptions = 0;
+    std::uint64_t dispatches = 0;         // Algorithm 2: requests handed to engines
+    std::uint64_t schedule_rounds = 0;    // Algorithm 2: moore_hodgson invocations
     std::uint64_t output_tokens = 0;      // tokens of completed requests
     std::vector<SimTime> gpu_busy_us;     // per GPU, time inside iterations
     bool truncated = false;

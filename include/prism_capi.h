@@ -335,12 +335,17 @@ typedef struct {
      * curves, engine.hpp ActivationParams) and fixed cost (s) per load:
      * load_latency = fixed + weight_bytes / bandwidth (prism_wloader_*). */
     double parallel_load_gbs, naive_load_gbs, load_fixed_s;
+    /* local scheduler of the prism policy: 0 Algorithm 2
+     * (moore_hodgson + dispatch gate + requeue_deferred over one queue per
+     * GPU), 1 per-model FIFO into the engine queues */
+    int32_t local_scheduler;
 } prism_sim_config;
 
 typedef struct {
     int64_t end_us;
     uint64_t events, iterations, activations, evictions, preemptions, output_tokens, n_requests, completed;
     int32_t truncated;
+    uint64_t dispatches, schedule_rounds; /* Algorithm 2 */
 } prism_sim_summary;
 
 typedef struct {

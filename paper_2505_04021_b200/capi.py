@@ -147,13 +147,13 @@ class SimConfig(C.Structure):
                 ("params", EngineParams), ("method", c_int32), ("tau_per_gb", c_double), ("tick_s", c_double),
                 ("idle_evict_s", c_double), ("pressure_free_frac", c_double), ("buffer_target_pages", c_uint64),
                 ("initial_placement", c_int32), ("max_events", c_uint64), ("parallel_load_gbs", c_double),
-                ("naive_load_gbs", c_double), ("load_fixed_s", c_double)]
+                ("naive_load_gbs", c_double), ("load_fixed_s", c_double), ("local_scheduler", c_int32)]
 
 
 class SimSummary(C.Structure):
     _fields_ = [("end_us", c_int64)] + [(n, c_uint64) for n in (
         "events", "iterations", "activations", "evictions", "preemptions", "output_tokens", "n_requests",
-        "completed")] + [("truncated", c_int32)]
+        "completed")] + [("truncated", c_int32), ("dispatches", c_uint64), ("schedule_rounds", c_uint64)]
 
 
 class SimRequest(C.Structure):

@@ -870,6 +870,7 @@ void prism_default_sim_config(prism_sim_config* out) {
     out->buffer_target_pages = d.buffer_target_pages;
     out->initial_placement = d.initial_placement ? 1 : 0;
     out->max_events = d.max_events;
+    out->local_scheduler = static_cast<int32_t>(d.local);
 }
 
 int prism_sim_run(const prism_sim_config* cfg, const prism_model_spec* specs, const double* rates, size_t n_models,
@@ -901,6 +902,10 @@ int prism_sim_run(const prism_sim_config* cfg, const prism_model_spec* specs, co
         c.buffer_target_pages = cfg->buffer_target_pages;
         c.initial_placement = cfg->initial_placement != 0;
         c.max_events = cfg->max_events;
+        if (cfg->local_scheduler < 0 || cfg->local_scheduler > 1) {
+            throw std::invalid_argument("prism_sim_run: unknown local scheduler");
+        }
+        c.local = static_cast<sc::LocalScheduler>(cfg->local_scheduler);
         auto sim = std::make_unique<prism_sim>();
         for (std::size_t i = 0; i < n_models; ++i) {
             sc::ModelEntry m;
@@ -935,6 +940,8 @@ int prism_sim_summary_get(const prism_sim* s, prism_sim_summary* out) {
         out->n_requests = m.requests.size();
         for (const auto& r : m.requests) out->completed += r.completion_us >= 0;
         out->truncated = m.truncated ? 1 : 0;
+        out->dispatches = m.dispatches;
+        out->schedule_rounds = m.schedule_rounds;
     });
 }
 

@@ -15,6 +15,7 @@
 #include <tuple>
 #include <vector>
 
+#include "msim/admission.hpp"
 #include "msim/defaults.hpp"
 #include "msim/errors.hpp"
 #include "msim/placement.hpp"
@@ -25,6 +26,7 @@ namespace {
 
 namespace me = msim::engine;
 namespace pl = msim::placement;
+namespace ad = msim::admission;
 
 enum Kind : int { kArrival = 0, kIterationDone = 1, kActivationDone = 2, kSchedulerTick = 3 };
 
@@ -49,6 +51,7 @@ struct Gpu {
     me::GpuState gs;
     bool busy = false;
     std::size_t rr = 0;  // next engine index the round robin looks at
+    std::vector<ad::QueuedRequest> queue;  // Algorithm 2: the GPU's shared request queue (arrival order)
     Gpu(int id, std::uint64_t cap, std::uint64_t page) : gs(id, cap, page) {}
 };
 
@@ -212,9 +215,10 @@ private:
         me::Engine& e = g.gs.engines[static_cast<std::size_t>(s.engine)];
         if (cfg_.policy == Policy::static_partition) e.pools.front().set_mapped_page_cap(cap_pages_[mi]);
         while (!s.waiting.empty()) {
-            enqueue(e, s.waiting.front(), s.gpu);
+            admit(e, s.waiting.front(), s.gpu);
             s.waiting.pop_front();
         }
+        schedule(s.gpu);
         wake(s.gpu);
     }
 
@@ -228,12 +232,93 @@ private:
         m_.requests[ti].gpu = gpu;
     }
 
+    bool algorithm2() const { return cfg_.policy == Policy::prism && cfg_.local == LocalScheduler::moore_hodgson; }
+
+    // A request for a resident, serving model: Algorithm 2 queues it on its
+    // GPU (dispatched by schedule()); FIFO hands it to the engine at once.
+    void admit(me::Engine& e, std::size_t ti, int gpu) {
+        if (!algorithm2()) {
+            enqueue(e, ti, gpu);
+            return;
+        }
+        const me::ModelSpec& spec = models_[index_.at(trace_[ti].model_id)].spec;
+        ad::QueuedRequest q;
+        q.id = ti + 1;
+        q.model_id = spec.model_id;
+        q.arrival_s = trace_[ti].arrival_s;
+        q.prompt_tokens = trace_[ti].prompt_tokens;
+        q.ttft_slo_s = spec.ttft_slo_s;
+        q.exec_estimate_s = static_cast<double>(q.prompt_tokens) / me::effective_prefill_tps(spec, cfg_.params);
+        gpus_[static_cast<std::size_t>(gpu)].queue.push_back(std::move(q));
+        m_.requests[ti].gpu = gpu;
+    }
+
+    // Algorithm 2 on one GPU: Moore-Hodgson over the GPU's
+    // queue, dispatch in deadline order through the immediately-runnable gate,
+    // deferred requests merged back (never dropped).
+    void schedule(int gpu) {
+        if (!algorithm2()) return;
+        Gpu& g = gpus_[static_cast<std::size_t>(gpu)];
+        if (g.queue.empty()) return;
+        ++m_.schedule_rounds;
+        ad::ScheduleDecision d = ad::moore_hodgson(g.queue, us_to_seconds(now_));
+        const std::vector<pagealloc::PhysicalLedger*> ledgers{&g.gs.ledger};
+        const auto gate = [&](const ad::QueuedRequest& r) {
+            const ModelState& s = state_[index_.at(r.model_id)];
+            if (s.gpu != gpu || s.loading) return ad::DispatchStatus::model_unavailable;
+            me::Engine& e = g.gs.engines[static_cast<std::size_t>(s.engine)];
+            if (!e.serving()) return ad::DispatchStatus::model_unavailable;
+            // no engine-local queuing: the engine's prefill pipeline must be empty
+            if (!e.local_queue.empty()) return ad::DispatchStatus::engine_busy;
+            for (const auto& b : e.batch) {
+                if (b.prompt_done < b.prompt_tokens) return ad::DispatchStatus::engine_busy;
+            }
+            // KV headroom: the first chunk (next_chunk_need, reference
+            // src/engine.cpp:63-78) plus the engine's reserved pages
+            const int chunk = std::min(e.model->chunk_size, r.prompt_tokens);
+            const std::uint64_t need = static_cast<std::uint64_t>(chunk) + (chunk == r.prompt_tokens ? 1 : 0);
+            const pagealloc::KvPool& pool = e.pools.front();
+            const std::uint64_t reserve = e.reserved_pages(cfg_.params.reserve_frac) * pool.tokens_per_page();
+            if (pool.allocatable_tokens(*ledgers.front()) < need + reserve) return ad::DispatchStatus::no_memory;
+            enqueue(e, static_cast<std::size_t>(r.id - 1), gpu);
+            return ad::DispatchStatus::dispatched;
+        };
+        // No starvation: the admit list (every request in
+        // it meets its deadline) goes first; the deferred ones — late under
+        // any schedule that keeps the admitted on time — stay eligible and
+        // follow in deadline order, so spare capacity still serves them.
+        ad::ScheduleDecision all;
+        all.now_s = d.now_s;
+        all.admit = d.admit;
+        std::vector<ad::QueuedRequest> late = d.deferred;
+        std::sort(late.begin(), late.end(), [](const ad::QueuedRequest& a, const ad::QueuedRequest& b) {
+            if (a.deadline_s() != b.deadline_s()) return a.deadline_s() < b.deadline_s();
+            if (a.arrival_s != b.arrival_s) return a.arrival_s < b.arrival_s;
+            return a.id < b.id;
+        });
+        all.admit.insert(all.admit.end(), late.begin(), late.end());
+        const std::vector<std::uint64_t> sent = ad::dispatch(all, gate);
+        m_.dispatches += sent.size();
+        if (sent.empty()) return;
+        std::vector<ad::QueuedRequest> rest;
+        rest.reserve(d.admit.size());
+        for (const ad::QueuedRequest& r : d.admit) {
+            if (std::find(sent.begin(), sent.end(), r.id) == sent.end()) rest.push_back(r);
+        }
+        std::vector<ad::QueuedRequest> deferred;
+        for (const ad::QueuedRequest& r : d.deferred) {
+            if (std::find(sent.begin(), sent.end(), r.id) == sent.end()) deferred.push_back(r);
+        }
+        g.queue = ad::requeue_deferred(deferred, std::move(rest));
+    }
+
     void on_arrival(std::size_t ti) {
         const std::size_t mi = index_.at(trace_[ti].model_id);
         ModelState& s = state_[mi];
         ++s.outstanding;
         if (s.gpu >= 0 && !s.loading) {
-            enqueue(gpus_[static_cast<std::size_t>(s.gpu)].gs.engines[static_cast<std::size_t>(s.engine)], ti, s.gpu);
+            admit(gpus_[static_cast<std::size_t>(s.gpu)].gs.engines[static_cast<std::size_t>(s.engine)], ti, s.gpu);
+            schedule(s.gpu);
             wake(s.gpu);
             return;
         }
@@ -330,6 +415,7 @@ private:
 
     void on_iteration_done(int gpu) {
         gpus_[static_cast<std::size_t>(gpu)].busy = false;
+        schedule(gpu);
         step_next(gpu);
         if (cfg_.policy == Policy::qlm_timeshare) qlm_swap();
     }
@@ -367,6 +453,14 @@ private:
         }
         for (std::size_t mi = 0; mi < models_.size(); ++mi) {
             if (state_[mi].gpu < 0 && !state_[mi].waiting.empty()) try_activate(mi);
+        }
+        // Evictions return weight pages to the GPU's free budget: an idle GPU
+        // whose work was blocked on memory (a paused prefill, a request the
+        // dispatch gate refused) may run again.
+        for (Gpu& g : gpus_) {
+            if (g.busy) continue;
+            schedule(g.gs.gpu_id);
+            wake(g.gs.gpu_id);
         }
         // keep ticking while requests are outstanding
         bool open = false;

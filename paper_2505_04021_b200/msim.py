@@ -985,6 +985,7 @@ class SimConfig:
     parallel_load_gbs: float = 0.0
     naive_load_gbs: float = 0.0
     load_fixed_s: float = 0.0
+    local_scheduler: str = "moore_hodgson"  # Algorithm 2, or "fifo" (per-model FIFO into engine queues)
 
 
 class SimResult:
@@ -1031,6 +1032,7 @@ def simulate(cfg: SimConfig, models: Sequence, trace: Sequence[TraceEvent], lib=
     c.pressure_free_frac, c.buffer_target_pages = cfg.pressure_free_frac, cfg.buffer_target_pages
     c.initial_placement, c.max_events = int(cfg.initial_placement), cfg.max_events
     c.parallel_load_gbs, c.naive_load_gbs, c.load_fixed_s = cfg.parallel_load_gbs, cfg.naive_load_gbs, cfg.load_fixed_s
+    c.local_scheduler = {"moore_hodgson": 0, "fifo": 1}[cfg.local_scheduler]
     specs = (capi.ModelSpec * max(len(models), 1))(*[m[0].to_c() for m in models])
     rates = (C.c_double * max(len(models), 1))(*[m[1] for m in models])
     arr = (capi.TraceEvent * max(len(trace), 1))()

@@ -63,19 +63,26 @@ def _check_invariants(res, trace):
     assert prev["both"] == 1.0
 
 
+@pytest.mark.parametrize("local", ["moore_hodgson", "fifo"])
 @pytest.mark.parametrize("case", ["c1", "c2", "c5x2"])
-def test_product_matches_reference_build(product, reference, case):
+def test_product_matches_reference_build(product, reference, case, local):
     """Same simcore source over the reference's engine / placement /
-    allocator vs over the product's: identical records and counters."""
+    allocator / admission vs over the product's: identical records and
+    counters, with Algorithm 2 (moore_hodgson -> dispatch gate ->
+    requeue_deferred) and with per-model FIFO admission."""
     if case == "c1":
         models, trace = _c1(product)
-        runs = [_run(lib, 1, models, trace, capacity=18_000) for lib in (product, reference)]
+        runs = [_run(lib, 1, models, trace, capacity=18_000, local_scheduler=local) for lib in (product, reference)]
     elif case == "c2":
         models, trace = _c2(product)
-        runs = [_run(lib, 1, models, trace, capacity=37_000) for lib in (product, reference)]
+        runs = [_run(lib, 1, models, trace, capacity=37_000, local_scheduler=local) for lib in (product, reference)]
     else:
         models, trace = _c5(product, copies=2, horizon=120.0)
-        runs = [_run(lib, 2, models, trace, capacity=24_000) for lib in (product, reference)]
+        runs = [_run(lib, 2, models, trace, capacity=24_000, local_scheduler=local) for lib in (product, reference)]
+    if local == "moore_hodgson":
+        assert runs[0].summary["dispatches"] == len(trace) and runs[0].summary["schedule_rounds"] > 0
+    else:
+        assert runs[0].summary["dispatches"] == 0
     a, b = runs
     assert a.summary == b.summary
     assert a.requests == b.requests
@@ -201,9 +208,12 @@ def test_measured_load_bandwidth_replaces_modelled_curve(product, reference):
     moves by exactly the load-time difference between two bandwidths; the
     reference-source build agrees record for record."""
     models, trace = _c1(product)
-    slow = _run(product, 1, models, trace, capacity=18_000, parallel_load_gbs=10.0)
-    fast = _run(product, 1, models, trace, capacity=18_000, parallel_load_gbs=100.0)
-    ref = _run(reference, 1, models, trace, capacity=18_000, parallel_load_gbs=10.0)
+    # FIFO admission isolates the load time (Algorithm 2 may reorder requests
+    # whose deadlines passed during the load)
+    kw = dict(capacity=18_000, local_scheduler="fifo")
+    slow = _run(product, 1, models, trace, parallel_load_gbs=10.0, **kw)
+    fast = _run(product, 1, models, trace, parallel_load_gbs=100.0, **kw)
+    ref = _run(reference, 1, models, trace, parallel_load_gbs=10.0, **kw)
     assert slow.requests == ref.requests and slow.summary == ref.summary
     _check_invariants(slow, trace)
     _check_invariants(fast, trace)
@@ -216,3 +226,40 @@ def test_measured_load_bandwidth_replaces_modelled_curve(product, reference):
     dflt = _run(product, 1, models, trace, capacity=18_000)
     base = _run(reference, 1, models, trace, capacity=18_000)
     assert dflt.requests == base.requests
+
+
+def _priority_case(lib, seed):
+    """SPEC.md:715 (acceptance 10): two colocated llama3.2-3b-shaped models
+    on one GPU under memory pressure (300 KV pages beside the weights): a
+    strict-SLO short-prompt model (TTFT 0.1 s, 128-token prompts, 25 req/s)
+    and a loose-SLO long-prompt model (TTFT 5 s, 3,000-token prompts, 3
+    req/s)."""
+    strict = S.shape_spec("llama3.2-3b", "strict", chunk=512, ttft=0.1)
+    loose = S.shape_spec("llama3.2-3b", "loose", chunk=512, ttft=5.0)
+    strict.tpot_slo_s = loose.tpot_slo_s = 1.0
+    prof = [msim.ModelProfile("strict", [(0.0, 60.0, 25.0)], 128.0, 0.3, 64.0, 0.4),
+            msim.ModelProfile("loose", [(0.0, 60.0, 3.0)], 3000.0, 0.3, 256.0, 0.4)]
+    trace = msim.synth_trace(prof, seed, lib=lib)
+    return [(strict, 25.0), (loose, 3.0)], trace
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3, 4, 5])
+def test_local_scheduler_priority_effect(product, seed):
+    """SPEC acceptance 10: enabling Algorithm 2 admission improves the
+    strict-SLO model's TTFT attainment by >= 0.20 absolute versus per-model
+    FIFO dispatch, without reducing the loose model's below FIFO - 0.05."""
+    models, trace = _priority_case(product, seed)
+    cap = 2 * 3067 + 300
+    mh = _run(product, 1, models, trace, capacity=cap, local_scheduler="moore_hodgson")
+    ff = _run(product, 1, models, trace, capacity=cap, local_scheduler="fifo")
+    _check_invariants(mh, trace)
+    _check_invariants(ff, trace)
+    gain = mh.attainment(1.0, "strict")["ttft"] - ff.attainment(1.0, "strict")["ttft"]
+    assert gain >= 0.20, gain
+    assert mh.attainment(1.0, "loose")["ttft"] >= ff.attainment(1.0, "loose")["ttft"] - 0.05
+
+
+def test_local_scheduler_priority_case_matches_reference_build(product, reference):
+    models, trace = _priority_case(product, 3)
+    a, b = (_run(lib, 1, models, trace, capacity=2 * 3067 + 300) for lib in (product, reference))
+    assert a.summary == b.summary and a.requests == b.requests
