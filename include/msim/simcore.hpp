@@ -82,6 +82,28 @@ enum class Policy { prism = 0, mux_flexible = 1, static_partition = 2, qlm_times
 // Policy::prism uses `local`; the baseline policies always use fifo.
 enum class LocalScheduler { moore_hodgson = 0, fifo = 1 };
 
+// Optional executor behind the modelled iterations (product only; the
+// reference has no device): with one attached, simcore is the serving loop
+// of the GPU data path. It gives each simulated GPU's ledger its device
+// (gpu_created, before any pool exists), gives every activated engine its
+// GPU half (attached, after finish_activation) and takes it back before
+// deactivate (detaching), brackets every engine::step — which, with a device
+// attached, runs K1 (batched slot allocation + block-table update) — and
+// then runs the iteration's kernels (iteration: K2 append, K4 chunked-prefill
+// attention and K3 decode attention over all layers) and returns the
+// duration to charge: the modelled one (decisions identical to the host-only
+// run) or the measured GPU time of the iteration.
+class IterationExecutor {
+public:
+    virtual ~IterationExecutor() = default;
+    virtual void gpu_created(int gpu, engine::GpuState& gs) = 0;
+    virtual void attached(int gpu, engine::GpuState& gs, int engine_index) = 0;
+    virtual void detaching(int gpu, engine::GpuState& gs, int engine_index) = 0;
+    virtual void before_step(int gpu, engine::GpuState& gs, int engine_index) = 0;
+    virtual SimTime iteration(int gpu, engine::GpuState& gs, int engine_index, const engine::IterationOutcome& out,
+                              SimTime modelled_us) = 0;
+};
+
 struct SimConfig {
     Policy policy = Policy::prism;
     LocalScheduler local = LocalScheduler::moore_hodgson;
@@ -98,6 +120,7 @@ struct SimConfig {
     std::uint64_t buffer_target_pages = 8;
     bool initial_placement = true;
     std::uint64_t max_events = 200'000'000;  // safety valve: the run stops (truncated) beyond it
+    IterationExecutor* executor = nullptr;   // not owned; null = host-only simulation
 };
 
 struct RequestRecord {

@@ -366,6 +366,40 @@ int prism_sim_attainment(const prism_sim* s, const char* model_id, double slo_sc
                          double* both, uint64_t* n);
 void prism_sim_free(prism_sim* s);
 
+/* The two-level scheduler driving the GPU data path (product only; north
+ * star (4)): prism_sim_run's event loop — place_models / eviction_tick /
+ * activate_on_arrival globally, Algorithm 2 per GPU, engine::step — with
+ * every simulated GPU in `owned` backed by a VmmDevice on a physical device
+ * (ordinals[g % n_ordinals]): pools reserve VA and map 2 MiB pages on
+ * demand, activation attaches each engine's GPU half, eviction frees the
+ * pool's VA and returns its chunks for reuse, and every iteration runs K1
+ * (inside engine::step), K2, K4 (prefill chunk) and K3 (decodes) for all
+ * layers. measured = 0: iterations are charged their modelled duration (the
+ * records equal prism_sim_run's); 1: the GPU time of the iteration's kernels
+ * (CUDA events on the engine stream; attention path only — there are no
+ * model weights / GEMMs). */
+typedef struct {
+    int32_t measured;
+    uint64_t seed;                 /* synthetic K/V content */
+    const int32_t* ordinals;       /* physical CUDA devices (NULL: device 0) */
+    size_t n_ordinals;
+    const int32_t* owned;          /* simulated GPUs run on a device (NULL / 0: all) */
+    size_t n_owned;
+    int32_t max_decode_batch;      /* per engine step (0: 512) */
+    uint64_t chunk_pages;          /* VMM chunk (0: default) */
+} prism_serving_options;
+typedef struct {
+    uint64_t iterations, attached, detached, k2_launches, k3_launches, k4_launches, decode_tokens, prefill_tokens;
+    uint64_t gpu_us, modelled_us; /* measured mode: charged GPU time and the cost model's for the same iterations */
+    uint64_t vmm_maps, vmm_unmaps, vmm_revived, vmm_creates, vmm_driver_unmaps, vmm_steals, vmm_urgent;
+    double vmm_caller_ns, vmm_worker_ns, wall_s;
+} prism_serving_stats;
+int prism_sim_run_device(const prism_sim_config* cfg, const prism_model_spec* specs, const double* rates,
+                         size_t n_models, const prism_trace_event* trace, size_t n_trace,
+                         const prism_serving_options* opts, prism_sim** out);
+/* PRISM_E_USAGE for a run without the device path */
+int prism_sim_serving_get(const prism_sim* s, prism_serving_stats* out);
+
 /* ------------------------------------------------------------------ GPU data path (product only; no reference counterpart) */
 
 /* prism::VmmDevice on CUDA device `ordinal` (2 MiB pages). Physical memory

@@ -162,6 +162,20 @@ class SimRequest(C.Structure):
                 ("preemptions", c_int32), ("gpu", c_int32)]
 
 
+class ServingOptions(C.Structure):
+    _fields_ = [("measured", c_int32), ("seed", c_uint64), ("ordinals", C.POINTER(c_int32)), ("n_ordinals", c_size_t),
+                ("owned", C.POINTER(c_int32)), ("n_owned", c_size_t), ("max_decode_batch", c_int32),
+                ("chunk_pages", c_uint64)]
+
+
+class ServingStats(C.Structure):
+    _fields_ = [(n, c_uint64) for n in (
+        "iterations", "attached", "detached", "k2_launches", "k3_launches", "k4_launches", "decode_tokens",
+        "prefill_tokens", "gpu_us", "modelled_us", "vmm_maps", "vmm_unmaps", "vmm_revived", "vmm_creates",
+        "vmm_driver_unmaps", "vmm_steals", "vmm_urgent")] + [(n, c_double) for n in (
+        "vmm_caller_ns", "vmm_worker_ns", "wall_s")]
+
+
 class RateSegment(C.Structure):
     _fields_ = [("start_s", c_double), ("end_s", c_double), ("rate_per_s", c_double)]
 
@@ -266,6 +280,7 @@ _HOST_DECLS = {
     "prism_sim_attainment": (c_int, [c_void_p, c_char_p, c_double, P(c_double), P(c_double), P(c_double),
                                      P(c_uint64)]),
     "prism_sim_free": (None, [c_void_p]),
+    "prism_sim_serving_get": (c_int, [c_void_p, P(ServingStats)]),
 }
 
 _DEVICE_DECLS = {
@@ -273,6 +288,8 @@ _DEVICE_DECLS = {
     "prism_device_open_chunked": (c_int, [c_int, c_uint64, c_uint64, P(c_void_p)]),
     "prism_device_chunk_pages": (c_int, [c_void_p, P(c_uint64)]),
     "prism_device_close": (None, [c_void_p]),
+    "prism_sim_run_device": (c_int, [P(SimConfig), P(ModelSpec), P(c_double), c_size_t, P(TraceEvent), c_size_t,
+                                     P(ServingOptions), P(c_void_p)]),
     "prism_device_capacity_pages": (c_int, [c_void_p, c_uint64, P(c_uint64)]),
     "prism_device_stats_get": (c_int, [c_void_p, P(DeviceStats)]),
     "prism_device_reset_stats": (c_int, [c_void_p]),

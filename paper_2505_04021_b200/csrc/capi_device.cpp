@@ -2,6 +2,7 @@
 // VMM device, pool mirror (K1), engine device (K1/K2/K3) and the host-buffer
 // end-to-end entry point.
 #include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <memory>
 #include <vector>
@@ -12,6 +13,7 @@
 #include "host/vmm.hpp"
 #include "host/weight_load.hpp"
 #include "host/paged_op.hpp"
+#include "host/serving.hpp"
 #include "msim/kvcache_device.hpp"
 #include "prism_capi.h"
 #include "capi_handles.hpp"
@@ -562,6 +564,39 @@ int prism_paged_decode_attention(prism_paged* pa, int layer, const int32_t* seq_
     return dguard([&] {
         need(pa, "paged");
         pa->op->decode_attention(layer, seq_offsets, n_seqs, slot_ids, q, out, scale);
+    });
+}
+
+int prism_sim_run_device(const prism_sim_config* cfg, const prism_model_spec* specs, const double* rates,
+                         size_t n_models, const prism_trace_event* trace, size_t n_trace,
+                         const prism_serving_options* opts, prism_sim** out) {
+    return dguard([&] {
+        need(out, "out");
+        prism::ServingOptions o;
+        std::vector<int> ordinals{0};
+        if (opts) {
+            o.measured = opts->measured != 0;
+            if (opts->seed) o.seed = opts->seed;
+            if (opts->ordinals && opts->n_ordinals) ordinals.assign(opts->ordinals, opts->ordinals + opts->n_ordinals);
+            if (opts->owned && opts->n_owned) o.owned.assign(opts->owned, opts->owned + opts->n_owned);
+            if (opts->max_decode_batch > 0) o.max_decode_batch = opts->max_decode_batch;
+            o.chunk_pages = opts->chunk_pages;
+        }
+        auto sim = std::make_unique<prism_sim>();
+        const auto t0 = std::chrono::steady_clock::now();
+        prism::DeviceExecutor ex(ordinals, o);
+        prism_capi_detail::sim_run(cfg, specs, rates, n_models, trace, n_trace, &ex, sim.get());
+        ex.synchronize();
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        const prism::ServingStats& st = ex.stats();
+        const prism::VmmStats v = ex.vmm_stats();
+        sim->device = true;
+        sim->serving = prism_serving_stats{st.iterations, st.attached, st.detached, st.k2_launches, st.k3_launches,
+                                           st.k4_launches, st.decode_tokens, st.prefill_tokens, st.gpu_us,
+                                           st.modelled_us, v.maps, v.unmaps, v.revived, v.creates,
+                                           v.driver_unmaps, v.steals, v.urgent,
+                                           v.map_ns_total + v.unmap_ns_total, v.background_ns_total, wall};
+        *out = sim.release();
     });
 }
 

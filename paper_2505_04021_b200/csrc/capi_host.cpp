@@ -31,12 +31,6 @@ namespace ad = msim::admission;
 namespace wl = msim::workload;
 namespace sc = msim::simcore;
 
-// prism_sim: a finished simcore run (metrics + the models it ran, for SLOs)
-struct prism_sim {
-    sc::SimMetrics metrics;
-    std::vector<sc::ModelEntry> models;
-};
-
 namespace prism_capi_detail {
 
 thread_local std::string g_error;
@@ -851,6 +845,61 @@ int prism_parse_trace_text(const char* text, const char* origin, prism_trace_eve
     });
 }
 
+}  // extern "C"
+
+namespace prism_capi_detail {
+
+void sim_run(const prism_sim_config* cfg, const prism_model_spec* specs, const double* rates, size_t n_models,
+             const prism_trace_event* trace, size_t n_trace, sc::IterationExecutor* executor, prism_sim* sim) {
+    need(cfg, "cfg");
+    if (n_models) need(specs, "specs");
+    if (n_trace) need(trace, "trace");
+    sc::SimConfig c;
+    if (cfg->policy < 0 || cfg->policy > 3) throw std::invalid_argument("prism_sim_run: unknown policy");
+    c.policy = static_cast<sc::Policy>(cfg->policy);
+    c.n_gpus = cfg->n_gpus;
+    c.capacity_pages = cfg->capacity_pages;
+    c.page_bytes = cfg->page_bytes;
+    c.params = to_params(&cfg->params);
+    c.method = cfg->method ? me::ActivationMethod::parallel : me::ActivationMethod::naive;
+    const auto curve = [&](double gbs) {
+        std::vector<std::pair<double, double>> c2;
+        for (double b : {16e9, 28e9}) c2.emplace_back(b, cfg->load_fixed_s + b / (gbs * 1e9));
+        return c2;
+    };
+    if (cfg->parallel_load_gbs > 0.0) c.activation.parallel_curve = curve(cfg->parallel_load_gbs);
+    if (cfg->naive_load_gbs > 0.0) c.activation.naive_curve = curve(cfg->naive_load_gbs);
+    c.tau_per_gb = cfg->tau_per_gb;
+    c.tick_s = cfg->tick_s;
+    c.idle_evict_s = cfg->idle_evict_s;
+    c.pressure_free_frac = cfg->pressure_free_frac;
+    c.buffer_target_pages = cfg->buffer_target_pages;
+    c.initial_placement = cfg->initial_placement != 0;
+    c.max_events = cfg->max_events;
+    if (cfg->local_scheduler < 0 || cfg->local_scheduler > 1) {
+        throw std::invalid_argument("prism_sim_run: unknown local scheduler");
+    }
+    c.local = static_cast<sc::LocalScheduler>(cfg->local_scheduler);
+    c.executor = executor;
+    for (std::size_t i = 0; i < n_models; ++i) {
+        sc::ModelEntry m;
+        m.spec = to_spec(specs[i]);
+        m.rate = rates ? rates[i] : 0.0;
+        sim->models.push_back(std::move(m));
+    }
+    std::vector<wl::TraceEvent> t;
+    t.reserve(n_trace);
+    for (std::size_t i = 0; i < n_trace; ++i) {
+        t.push_back(wl::TraceEvent{trace[i].arrival_s, trace[i].model_id, trace[i].prompt_tokens,
+                                   trace[i].output_tokens});
+    }
+    sim->metrics = sc::run(c, sim->models, t);
+}
+
+}  // namespace prism_capi_detail
+
+extern "C" {
+
 /* ------------------------------------------------------------------ simcore */
 
 void prism_default_sim_config(prism_sim_config* out) {
@@ -876,50 +925,9 @@ void prism_default_sim_config(prism_sim_config* out) {
 int prism_sim_run(const prism_sim_config* cfg, const prism_model_spec* specs, const double* rates, size_t n_models,
                   const prism_trace_event* trace, size_t n_trace, prism_sim** out) {
     return guard([&] {
-        need(cfg, "cfg");
         need(out, "out");
-        if (n_models) need(specs, "specs");
-        if (n_trace) need(trace, "trace");
-        sc::SimConfig c;
-        if (cfg->policy < 0 || cfg->policy > 3) throw std::invalid_argument("prism_sim_run: unknown policy");
-        c.policy = static_cast<sc::Policy>(cfg->policy);
-        c.n_gpus = cfg->n_gpus;
-        c.capacity_pages = cfg->capacity_pages;
-        c.page_bytes = cfg->page_bytes;
-        c.params = to_params(&cfg->params);
-        c.method = cfg->method ? me::ActivationMethod::parallel : me::ActivationMethod::naive;
-        const auto curve = [&](double gbs) {
-            std::vector<std::pair<double, double>> c2;
-            for (double b : {16e9, 28e9}) c2.emplace_back(b, cfg->load_fixed_s + b / (gbs * 1e9));
-            return c2;
-        };
-        if (cfg->parallel_load_gbs > 0.0) c.activation.parallel_curve = curve(cfg->parallel_load_gbs);
-        if (cfg->naive_load_gbs > 0.0) c.activation.naive_curve = curve(cfg->naive_load_gbs);
-        c.tau_per_gb = cfg->tau_per_gb;
-        c.tick_s = cfg->tick_s;
-        c.idle_evict_s = cfg->idle_evict_s;
-        c.pressure_free_frac = cfg->pressure_free_frac;
-        c.buffer_target_pages = cfg->buffer_target_pages;
-        c.initial_placement = cfg->initial_placement != 0;
-        c.max_events = cfg->max_events;
-        if (cfg->local_scheduler < 0 || cfg->local_scheduler > 1) {
-            throw std::invalid_argument("prism_sim_run: unknown local scheduler");
-        }
-        c.local = static_cast<sc::LocalScheduler>(cfg->local_scheduler);
         auto sim = std::make_unique<prism_sim>();
-        for (std::size_t i = 0; i < n_models; ++i) {
-            sc::ModelEntry m;
-            m.spec = to_spec(specs[i]);
-            m.rate = rates ? rates[i] : 0.0;
-            sim->models.push_back(std::move(m));
-        }
-        std::vector<wl::TraceEvent> t;
-        t.reserve(n_trace);
-        for (std::size_t i = 0; i < n_trace; ++i) {
-            t.push_back(wl::TraceEvent{trace[i].arrival_s, trace[i].model_id, trace[i].prompt_tokens,
-                                       trace[i].output_tokens});
-        }
-        sim->metrics = sc::run(c, sim->models, t);
+        prism_capi_detail::sim_run(cfg, specs, rates, n_models, trace, n_trace, nullptr, sim.get());
         *out = sim.release();
     });
 }
@@ -981,6 +989,15 @@ int prism_sim_attainment(const prism_sim* s, const char* model_id, double slo_sc
         if (tpot) *tpot = it->second.tpot;
         if (both) *both = it->second.both;
         if (n) *n = it->second.n;
+    });
+}
+
+int prism_sim_serving_get(const prism_sim* s, prism_serving_stats* out) {
+    return guard([&] {
+        need(s, "sim");
+        need(out, "out");
+        if (!s->device) throw msim::UsageError("prism_sim_serving_get: the run did not drive the GPU data path");
+        *out = s->serving;
     });
 }
 

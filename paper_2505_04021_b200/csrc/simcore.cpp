@@ -72,6 +72,9 @@ public:
             if (!index_.count(ev.model_id)) throw UsageError("simcore: trace names an unknown model: " + ev.model_id);
         }
         for (int g = 0; g < cfg.n_gpus; ++g) gpus_.emplace_back(g, cfg.capacity_pages, cfg.page_bytes);
+        if (cfg.executor) {
+            for (Gpu& g : gpus_) cfg.executor->gpu_created(g.gs.gpu_id, g.gs);
+        }
         state_.resize(models.size());
         cap_pages_.assign(models.size(), 0);
         m_.requests.resize(trace.size());
@@ -211,6 +214,7 @@ private:
         ModelState& s = state_[mi];
         Gpu& g = gpus_[static_cast<std::size_t>(s.gpu)];
         me::finish_activation(g.gs, s.engine);
+        if (cfg_.executor) cfg_.executor->attached(s.gpu, g.gs, s.engine);
         s.loading = false;
         me::Engine& e = g.gs.engines[static_cast<std::size_t>(s.engine)];
         if (cfg_.policy == Policy::static_partition) e.pools.front().set_mapped_page_cap(cap_pages_[mi]);
@@ -354,6 +358,7 @@ private:
             if (best == models_.size()) return;
             if (res >= 0) {
                 ModelState& r = state_[res];
+                if (cfg_.executor) cfg_.executor->detaching(g.gs.gpu_id, g.gs, r.engine);
                 me::deactivate(g.gs, r.engine);
                 r.gpu = -1;
                 r.engine = -1;
@@ -385,8 +390,12 @@ private:
             const std::size_t ei = (g.rr + k) % n;
             me::Engine& e = g.gs.engines[ei];
             if (!e.serving() || !e.has_runnable_work(ledgers)) continue;
+            if (cfg_.executor) cfg_.executor->before_step(gpu, g.gs, static_cast<int>(ei));
             const me::IterationOutcome o = me::step(e, ledgers, cfg_.params, now_);
-            const SimTime dur = std::max<SimTime>(o.duration_us, 1);
+            SimTime dur = std::max<SimTime>(o.duration_us, 1);
+            if (cfg_.executor) {
+                dur = std::max<SimTime>(cfg_.executor->iteration(gpu, g.gs, static_cast<int>(ei), o, dur), 1);
+            }
             const SimTime end = now_ + dur;
             for (std::uint64_t id : o.first_tokens) m_.requests[id - 1].first_token_us = end;
             for (std::uint64_t id : o.preemptions) {
@@ -446,6 +455,7 @@ private:
             Gpu& g = gpus_[static_cast<std::size_t>(s.gpu)];
             me::Engine& e = g.gs.engines[static_cast<std::size_t>(s.engine)];
             if (s.loading || !e.drained()) continue;
+            if (cfg_.executor) cfg_.executor->detaching(s.gpu, g.gs, s.engine);
             me::deactivate(g.gs, s.engine);
             s.gpu = -1;
             s.engine = -1;

@@ -1018,9 +1018,10 @@ class SimResult:
             self.h = None
 
 
-def simulate(cfg: SimConfig, models: Sequence, trace: Sequence[TraceEvent], lib=None) -> SimResult:
+def simulate(cfg: SimConfig, models: Sequence, trace: Sequence[TraceEvent], lib=None, serving=None) -> SimResult:
     """msim::simcore::run. models: (ModelSpec, rate) pairs; rate = demand
-    for the initial placement."""
+    for the initial placement. serving: a ServingConfig to drive the GPU data
+    path with the same event loop (prism_sim_run_device, product only)."""
     lib = _lib(lib)
     c = capi.SimConfig()
     lib.dll.prism_default_sim_config(C.byref(c))
@@ -1039,5 +1040,34 @@ def simulate(cfg: SimConfig, models: Sequence, trace: Sequence[TraceEvent], lib=
     for i, e in enumerate(trace):
         arr[i] = capi.TraceEvent(e.arrival_s, e.model_id.encode(), e.prompt_tokens, e.output_tokens)
     h = C.c_void_p()
-    lib.call("prism_sim_run", C.byref(c), specs, rates, len(models), arr, len(trace), C.byref(h))
-    return SimResult(lib, h)
+    if serving is None:
+        lib.call("prism_sim_run", C.byref(c), specs, rates, len(models), arr, len(trace), C.byref(h))
+        return SimResult(lib, h)
+    o = capi.ServingOptions()
+    o.measured = int(serving.measured)
+    o.seed = serving.seed
+    ords = (C.c_int32 * max(len(serving.ordinals), 1))(*serving.ordinals)
+    owned = (C.c_int32 * max(len(serving.owned), 1))(*serving.owned)
+    o.ordinals, o.n_ordinals = ords, len(serving.ordinals)
+    o.owned, o.n_owned = owned, len(serving.owned)
+    o.max_decode_batch, o.chunk_pages = serving.max_decode_batch, serving.chunk_pages
+    lib.call("prism_sim_run_device", C.byref(c), specs, rates, len(models), arr, len(trace), C.byref(o), C.byref(h))
+    res = SimResult(lib, h)
+    st = capi.ServingStats()
+    lib.call("prism_sim_serving_get", h, C.byref(st))
+    res.serving = {f: getattr(st, f) for f, _ in capi.ServingStats._fields_}
+    return res
+
+
+@dataclass
+class ServingConfig:
+    """prism_serving_options: simcore's event loop driving the GPU data path
+    (every iteration runs K1 / K2 / K4 / K3 on the device). measured=False:
+    iterations are charged their modelled duration (records equal the
+    host-only run); True: the measured GPU time of the iteration's kernels."""
+    measured: bool = False
+    seed: int = 20251017
+    ordinals: list = field(default_factory=lambda: [0])
+    owned: list = field(default_factory=list)  # simulated GPUs executed on a device (empty: all)
+    max_decode_batch: int = 512
+    chunk_pages: int = 0
