@@ -792,6 +792,73 @@ def slo_c5(copies=6, horizon=240.0):
     return out
 
 
+def serving_gpu():
+    """The two-level scheduler driving the B200 data path (north_star (4)):
+    simcore's event loop (place_models / eviction_tick / activate_on_arrival
+    globally, Algorithm 2 per GPU, engine::step) with every iteration running
+    K1 / K2 / K4 / K3 for all layers on pools backed by real VMM pages
+    (prism_sim_run_device). Per scenario:
+      * modelled clock: decisions must equal the host-only simulation's
+        (`decisions_equal_host_sim`), the device path only executes them;
+      * measured clock (C2, C4 shard): every iteration is charged the CUDA-
+        event time of its own kernels, so TTFT / TPOT come from B200 kernel
+        time. Attention path only — weight GEMMs are out of scope (SURVEY
+        §8), so these latencies are a lower bound on a full model's.
+    C5 at 1 GPU forces real swaps: weights exceed the ledger, idle models
+    are deactivated (pool VA freed, chunks recycled) and re-activated."""
+    from paper_2505_04021_b200 import msim
+    from paper_2505_04021_b200.configs import B200_LEDGER_PAGES, c2_case, c4_case, c5_case
+
+    def att(r):
+        return {str(k): {m: round(v, 4) for m, v in r.attainment(k).items() if m != "n"} for k in (1, 2, 4)}
+
+    def run(name, models, prof, n_gpus, capacity, owned=(), **kw):
+        trace = msim.synth_trace(prof, TRACE_SEED)
+        cfg = msim.SimConfig(n_gpus=n_gpus, capacity_pages=capacity, **kw)
+        host = msim.simulate(cfg, models, trace)
+        t0 = time.perf_counter()
+        dev = msim.simulate(cfg, models, trace, serving=msim.ServingConfig(owned=list(owned)))
+        wall_modelled = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        meas = msim.simulate(cfg, models, trace, serving=msim.ServingConfig(measured=True, owned=list(owned)))
+        wall_meas = time.perf_counter() - t0
+        s = meas.serving
+        it = max(s["iterations"], 1)
+        return {
+            "workload": name, "requests": len(trace), "gpus_simulated": n_gpus, "ledger_pages": capacity,
+            "gpus_on_device": list(owned) or list(range(n_gpus)),
+            "decisions_equal_host_sim": dev.summary == host.summary and dev.requests == host.requests,
+            "modelled": {"attainment": att(dev), "activations": dev.summary["activations"],
+                         "evictions": dev.summary["evictions"], "preemptions": dev.summary["preemptions"],
+                         "engine_attach": dev.serving["attached"], "engine_detach": dev.serving["detached"],
+                         "wall_s": round(wall_modelled, 2)},
+            "measured": {"attainment": att(meas), "iterations_on_device": s["iterations"],
+                         "gpu_us_per_iteration": round(s["gpu_us"] / it, 1),
+                         "modelled_us_per_iteration": round(s["modelled_us"] / it, 1),
+                         "k2_launches": s["k2_launches"], "k3_launches": s["k3_launches"],
+                         "k4_launches": s["k4_launches"], "decode_tokens": s["decode_tokens"],
+                         "prefill_tokens": s["prefill_tokens"], "activations": meas.summary["activations"],
+                         "evictions": meas.summary["evictions"], "vmm_maps": s["vmm_maps"],
+                         "vmm_unmaps": s["vmm_unmaps"], "wall_s": round(wall_meas, 2)},
+        }
+
+    out = {"note": "attainment = fraction of requests meeting both TTFT and TPOT SLOs at SLO scale k; "
+                   "measured clock = CUDA-event time of the iteration's attention-path kernels "
+                   "(K1+K2+K4+K3, no weight GEMMs)"}
+    models, prof = c2_case()
+    out["c2"] = run("C2: 8 shapes space-sharing 1 B200, 10 s on / 10 s off bursts", models, prof, 1,
+                    B200_LEDGER_PAGES)
+    models, prof = c4_case(horizon=60.0)
+    out["c4_shard"] = run("C4: 24 models (8 shapes x 3, Zipf 1.2, idle periods) placed over 8 simulated B200s; "
+                          "simulated GPU 0 (this rank's shard) on the device", models, prof, 8,
+                          B200_LEDGER_PAGES, owned=[0])
+    models, prof = c5_case(copies=6, horizon=30.0)
+    out["c5_1gpu"] = run("C5: 48 models, r / 5r swings, 30 s, 1 B200 (weights exceed the ledger: idle models "
+                         "evicted after 5 s, re-activated on arrival)", models, prof, 1, B200_LEDGER_PAGES,
+                         idle_evict_s=5.0, tick_s=2.0)
+    return out
+
+
 def loaded_native_libs():
     """In-repo / torch-extension shared objects mapped into this process."""
     out = set()
@@ -938,6 +1005,8 @@ def main():
     ap.add_argument("--no-churn", action="store_true", help="skip the C2 page map/unmap measurement")
     ap.add_argument("--no-prefill", action="store_true", help="skip the C3 chunked-prefill (K4) measurement")
     ap.add_argument("--no-slo", action="store_true", help="skip the C5 SLO-attainment sweep (simcore)")
+    ap.add_argument("--no-serving", action="store_true",
+                    help="skip the scheduler-driven device runs (C2 / C4 shard / C5 at 1 GPU)")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -992,6 +1061,11 @@ def main():
                 res["activation_f2"] = activation_f2()
             except Exception as e:
                 res["activation_f2"] = {"error": str(e)}
+        if world == 1 and not args.no_serving:
+            try:
+                res["serving"] = serving_gpu()
+            except Exception as e:
+                res["serving"] = {"error": str(e)}
         print(json.dumps(res))
     if world > 1:
         import torch.distributed as dist

@@ -59,3 +59,36 @@ def c5_case(copies=6, horizon=240.0, base_rate=0.25):
         profiles.append(msim.ModelProfile(spec.model_id, segs, 384.0, 0.6, 96.0, 0.6))
         models.append((spec, base_rate * 3.0))
     return models, profiles
+
+
+def c2_case(rate=3.0, horizon=80.0):
+    """Config 2 ("8 models (1B-8B shapes) space-sharing 1 B200 with bursty
+    trace forcing frequent page map/unmap across models"): one model per
+    shape, 10 s on / 10 s off with alternating phase. Returns ((spec,
+    demand rate) pairs, synth_trace profiles)."""
+    specs = slo_models(1)
+    prof = []
+    for i, s in enumerate(specs):
+        segs = [(float(t), float(t) + 10.0, rate) for t in range(10 * (i % 2), int(horizon), 20)]
+        prof.append(msim.ModelProfile(s.model_id, segs, 256.0, 0.6, 64.0, 0.6))
+    return [(s, rate / 2) for s in specs], prof
+
+
+def c4_case(copies=3, horizon=120.0, total_rate=24.0, zipf=1.2, idle_every=3):
+    """Config 4 ("24 models of mixed size placed across 8 x B200 by the
+    global scheduler, long-tail synthetic trace with idle periods"): every
+    shape x `copies`; model k (popularity rank) gets total_rate * k^-zipf /
+    H; every `idle_every`-th model alternates 20 s on / 20 s idle."""
+    specs = slo_models(copies)
+    w = [(k + 1) ** -zipf for k in range(len(specs))]
+    h = sum(w)
+    prof, models = [], []
+    for k, s in enumerate(specs):
+        r = total_rate * w[k] / h
+        if idle_every and k % idle_every == idle_every - 1:
+            segs = [(float(t), float(t) + 20.0, r) for t in range(0, int(horizon), 40)]
+        else:
+            segs = [(0.0, horizon, r)]
+        prof.append(msim.ModelProfile(s.model_id, segs, 384.0, 0.6, 96.0, 0.6))
+        models.append((s, r))
+    return models, prof

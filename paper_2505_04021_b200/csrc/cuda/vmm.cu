@@ -217,7 +217,7 @@ void VmmDevice::set_idle(std::uint64_t va, Chunk& c) {
 
 void VmmDevice::drop_if_empty(ChunkMap::iterator it) {
     const Chunk& c = it->second;
-    if (!c.mapped && !c.inflight && !c.queued && c.refs == 0 && c.handle == 0) chunks_.erase(it);
+    if (!c.mapped && !c.inflight && !c.queued && !c.owed && c.refs == 0 && c.handle == 0) chunks_.erase(it);
 }
 
 void VmmDevice::check_failed() const {
@@ -354,11 +354,11 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h, bool premap) {
                     v.inflight = false;
                     v.handle = handles[k];
                     v.mapped = true;
-                    if (v.refs == 0) {
-                        set_idle(va, v);
-                    } else {
-                        --unready_;  // a caller revived it meanwhile: still mapped
+                    if (v.owed) {
+                        --unready_;  // a caller mapped a page in it meanwhile: still mapped
+                        v.owed = false;
                     }
+                    if (v.refs == 0) set_idle(va, v);
                 }
                 failed_ = "cuMemUnmap failed (" + std::to_string(res) + ")";
                 done_cv_.notify_all();
@@ -379,7 +379,7 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h, bool premap) {
                 const auto vit = chunks_.find(va);
                 Chunk& v = vit->second;
                 v.inflight = false;
-                if (v.refs > 0) {
+                if (v.owed) {
                     // its pool mapped a page in it again meanwhile: map it back
                     if (!v.queued) {
                         urgent_.push_back(va);
@@ -446,22 +446,26 @@ bool VmmDevice::map_chunk(Lock& lk, std::uint64_t va, std::uint64_t h, bool urge
         cache_.push_back(h);
         if (urgent) {
             failed_ = "cuMemMap/cuMemSetAccess failed (" + std::to_string(r) + ")";
-        } else if (c.refs > 0 && !c.queued) {
+        } else if (c.owed && !c.queued) {
             // a caller mapped a page into this look-ahead chunk meanwhile and
             // counts it in unready_: retry it as an urgent map
             urgent_.push_back(va);
             c.queued = true;
         }
         hints_.clear();
-        if (c.refs == 0) drop_if_empty(it);
+        drop_if_empty(it);
         return false;
     }
     c.mapped = true;
-    if (c.refs > 0) {
+    const bool owed = c.owed;
+    if (owed) {
         --unready_;
+        c.owed = false;
+    }
+    if (c.refs > 0) {
         c.clean = false;
     } else {
-        c.clean = !urgent;  // an urgent chunk whose pages all left meanwhile keeps its release epoch
+        c.clean = !owed;  // a chunk whose pages all left meanwhile keeps its release epoch
         set_idle(va, c);
     }
     if (urgent) {
@@ -477,7 +481,8 @@ void VmmDevice::worker_main() {
     const auto free_chunk = [&](std::uint64_t v) {
         const auto it = chunks_.find(v);
         return it == chunks_.end() ||
-               (!it->second.mapped && !it->second.inflight && !it->second.queued && it->second.refs == 0);
+               (!it->second.mapped && !it->second.inflight && !it->second.queued && !it->second.owed &&
+                it->second.refs == 0);
     };
     Lock lk(mu_);
     while (!stop_) {
@@ -488,7 +493,7 @@ void VmmDevice::worker_main() {
             const auto it = chunks_.find(va);
             Chunk& c = it->second;
             c.queued = false;
-            if (c.refs == 0 || c.mapped || c.inflight) {  // released, or mapped by the look-ahead
+            if (!c.owed || c.mapped || c.inflight) {  // mapped by the look-ahead, or in flight
                 drop_if_empty(it);
                 continue;
             }
@@ -529,7 +534,7 @@ void VmmDevice::worker_main() {
                 map_chunk(lk, va, h, false);
             } else {
                 it->second.inflight = false;
-                if (it->second.refs > 0 && !it->second.queued) {  // wanted meanwhile
+                if (it->second.owed && !it->second.queued) {  // wanted meanwhile
                     urgent_.push_back(va);
                     it->second.queued = true;
                 }
@@ -696,7 +701,7 @@ void VmmDevice::release(std::uint64_t va, std::uint64_t pages) {
                 synced = true;
             }
             unmap_chunk_caller(it);
-        } else if (c.refs > 0) {
+        } else if (c.owed) {
             --unready_;  // never mapped (worker failed): nothing to undo
         }
         it = chunks_.erase(it);
@@ -746,8 +751,9 @@ void VmmDevice::map_batch(const std::uint64_t* vas, std::size_t n, std::size_t n
                 }
             }
             ++stats_.revived;
-        } else if (c.refs == 0) {
+        } else if (!c.owed) {
             ++unready_;
+            c.owed = true;
             if (!c.inflight && !c.queued) {
                 urgent_.push_back(cv);
                 c.queued = true;
@@ -790,11 +796,9 @@ void VmmDevice::unmap(std::uint64_t va) {
     if (--c.refs == 0) {
         c.epoch = epoch_;  // kernels issued before the next fence may read it
         c.clean = false;
-        if (c.mapped) {
-            set_idle(it->first, c);
-        } else {
-            --unready_;  // queued / in flight: lands idle (or is skipped)
-        }
+        // not mapped yet: it stays owed (this step's kernels may touch its
+        // pages) and lands idle, with this epoch, once the worker mapped it
+        if (c.mapped) set_idle(it->first, c);
     }
     ++stats_.unmaps;
     const double ns = ns_since(t0);
@@ -903,6 +907,16 @@ VmmStats VmmDevice::stats() const {
 void VmmDevice::reset_stats() {
     Lock lk(mu_);
     stats_ = VmmStats{};
+}
+
+unsigned VmmDevice::debug_chunk_state(std::uint64_t page_va) const {
+    Lock lk(mu_);
+    const std::uint64_t cv = chunk_of(page_va);
+    const auto it = chunks_.find(cv);
+    if (it == chunks_.end()) return 0;
+    const Chunk& c = it->second;
+    return 1u | (c.mapped ? 2u : 0u) | (c.inflight ? 4u : 0u) | (c.queued ? 8u : 0u) | (c.refs > 0 ? 16u : 0u) |
+           (idle_.count(cv) ? 32u : 0u);
 }
 
 std::uint64_t VmmDevice::capacity_pages(std::uint64_t reserve_bytes) const {

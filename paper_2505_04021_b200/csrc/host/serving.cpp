@@ -23,9 +23,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <stdexcept>
 #include <string>
 
+#include "host/pool_state.hpp"
 #include "host/vmm.hpp"
 #include "msim/kvcache_device.hpp"
 
@@ -124,10 +126,43 @@ msim::SimTime DeviceExecutor::iteration(int gpu, msim::engine::GpuState& gs, int
     Buffers& b = bufs_.at({gpu, engine_index});
     const int n_tok = last_step_tokens(e), n_dec = last_step_decodes(e), n_pf = last_step_prefill_tokens(e);
     const float scale = 1.0f / std::sqrt(static_cast<float>(m.head_dim));
+    // PRISM_SERVE_SYNC=1 (diagnosis): synchronise after every launch group
+    // and name the one that failed
+    static const bool dbg_sync = std::getenv("PRISM_SERVE_SYNC") != nullptr;
+    const auto check = [&](const char* what, int layer) {
+        if (!dbg_sync) return;
+        const cudaError_t err = cudaStreamSynchronize(static_cast<cudaStream_t>(devs_.at(gpu)->stream()));
+        if (err != cudaSuccess) {
+            throw std::runtime_error(std::string("serving: ") + what + " layer " + std::to_string(layer) + " of " +
+                                     m.model_id + " (iteration " + std::to_string(stats_.iterations) + ", tokens " +
+                                     std::to_string(n_tok) + ", decodes " + std::to_string(n_dec) + ", prefill " +
+                                     std::to_string(n_pf) + "): " + cudaGetErrorString(err));
+        }
+    };
+    check("K1 (engine::step)", -1);
+    if (dbg_sync && n_tok > 0) {
+        // every slot K2 is about to write must lie in a mapped chunk (a page
+        // may already be free again: completions free in the same step)
+        const std::vector<std::int32_t> slots = last_step_slots(e);
+        const auto* st = e.pools.at(0).state();
+        for (const std::int32_t sid : slots) {
+            const std::uint64_t page = static_cast<std::uint64_t>(sid) / st->tpp;
+            const unsigned cs = devs_.at(gpu)->debug_chunk_state(st->va + page * gs.ledger.page_bytes());
+            if (sid < 0 || page >= st->vpages || (cs & 2u) == 0) {
+                throw std::runtime_error("serving: step slot " + std::to_string(sid) + " page " + std::to_string(page) +
+                                         " occ " + std::to_string(page < st->vpages ? st->occ[page] : 0) +
+                                         " chunk state " + std::to_string(cs) + " of " + m.model_id + " (iteration " +
+                                         std::to_string(stats_.iterations) + ")");
+            }
+        }
+    }
     if (n_tok > 0) append_step_kv_synthetic(e, 0, m.n_layers, opts_.seed);  // K2
+    check("K2", -1);
     for (int layer = 0; layer < m.n_layers; ++layer) {
         if (n_pf > 0) prefill_attention(e, layer, b.q, b.out, scale);  // K4
+        check("K4", layer);
         if (n_dec > 0) decode_attention(e, layer, b.q, b.out, scale);  // K3
+        check("K3", layer);
     }
     ++stats_.iterations;
     stats_.k2_launches += n_tok > 0;

@@ -140,6 +140,9 @@ public:
     void reset_stats();
 
     std::uint64_t capacity_pages(std::uint64_t reserve_bytes) const;
+    // Diagnosis: state of the chunk holding page_va (bit 0 known, 1 mapped,
+    // 2 inflight, 3 queued, 4 referenced, 5 idle).
+    unsigned debug_chunk_state(std::uint64_t page_va) const;
 
 private:
     VmmDevice() = default;
@@ -154,6 +157,11 @@ private:
         bool inflight = false;     // the worker is mapping / unmapping it now
         bool queued = false;       // in urgent_
         bool clean = false;        // mapped by the look-ahead, never referenced
+        // counted in unready_: a page of it was mapped while the chunk was
+        // not; it must be mapped before the step's kernels run even if its
+        // pages leave again in the same step (completion frees, preemption):
+        // K2 / K3 of that step still touch them
+        bool owed = false;
         std::chrono::steady_clock::time_point idle_at{};  // when it last became idle
     };
     using ChunkMap = std::map<std::uint64_t, Chunk>;

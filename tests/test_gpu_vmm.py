@@ -198,3 +198,54 @@ def test_startup_reservation_backs_later_maps(product):
         assert st["total_chunks"] * st["chunk_pages"] <= 600  # never past the physical budget
     finally:
         dev.close()
+
+
+_SAME_STEP_FREE = r"""
+import math, sys
+import torch
+from paper_2505_04021_b200 import msim
+from tests import scenarios as S
+dev = msim.Device(0, chunk_pages=1)          # one page per physical handle
+gpu = msim.GpuState(0, 64)
+gpu.ledger.attach_device(dev)
+spec = S.shape_spec("llama3.1-8b", "m", chunk=64, weight_scale=0.0)   # 16 tokens per page
+act = gpu.activate(spec)
+gpu.finish_activation(act.engine_index)
+eng = gpu.engine(act.engine_index)
+eng.attach_device()
+eng.push(1, 15, 2)    # prefill 15 (+1 first token) fills page 0 exactly
+eng.push(2, 47, 2)    # pages 1-3
+for step in range(10):
+    if not sum(eng.counts()):
+        break
+    eng.step()        # decode steps: each lands on a FRESH page and completes -> freed in the same step
+    eng.append_kv_synthetic(0, spec.n_layers, 7)
+    if eng.step_decode_ids():
+        q = torch.zeros((len(eng.step_decode_ids()), 32, 128), dtype=torch.bfloat16, device="cuda")
+        o = torch.empty_like(q)
+        for layer in range(spec.n_layers):
+            eng.decode_attention(layer, q.data_ptr(), o.data_ptr(), 1 / math.sqrt(128))
+    eng.synchronize()
+    torch.cuda.synchronize()
+assert sum(eng.counts()) == 0 and gpu.ledger.mapped_pages() == 0
+print("ok")
+"""
+
+
+def test_page_freed_in_its_allocating_step_is_still_mapped_for_the_kernels():
+    """A decode token that lands on a fresh page of a request completing in
+    the same step: the page is mapped and freed within one step (completion
+    frees run before the step's K2 / K3, reference engine.cpp:250-262), but
+    K2 still writes its K/V row and K3 reads it. With the look-ahead off
+    (PRISM_PREMAP=0) the chunk is still queued when the free arrives; it must
+    be mapped before the kernels run all the same (found by the scheduler-
+    driven C5 run: an illegal address in K2)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PRISM_PREMAP="0", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", _SAME_STEP_FREE], cwd=root, env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
