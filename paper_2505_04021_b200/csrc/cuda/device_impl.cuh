@@ -158,6 +158,9 @@ public:
     // stream-K K3 launch (no K1 / K2 / upload / other kernel since): the next
     // K3 may then be launched as a programmatic dependent (PDL) of it.
     bool k3_chain = false;
+    // K4: key-tile prefix over the Q-tile pairs of the last (first, chunk)
+    Staging<std::int32_t> pf_prefix;
+    int pf_first = -1, pf_chunk = -1, pf_per_head = 0;
 
     // host-buffer (end-to-end) path
     cudaStream_t copy_stream = nullptr;
@@ -206,6 +209,9 @@ struct PagedCtx final : PagedOp {
     int sk_total = 0, sk_per_cta = 1, sk_max_parts = 1;
     std::uint64_t sk_launches = 0;  // selects the CTA range counter (alternate launches)
     bool k3_chain = false;
+    // K4: key-tile prefix over the Q-tile pairs of the last (first, chunk)
+    Staging<std::int32_t> pf_prefix;
+    int pf_first = -1, pf_chunk = -1, pf_per_head = 0;
     float* workspace = nullptr;
     std::size_t workspace_floats = 0;
     int* counters = nullptr;

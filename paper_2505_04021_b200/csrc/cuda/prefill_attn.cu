@@ -8,31 +8,38 @@
 //   keys 0..p_i (causal), K/V read from the pool's pages through the block
 //   table, kv head h / G (GQA).
 //
-// One CTA = one (query tile, kv head) work item. The G q heads of a kv head
-// are packed into the MMA's M dimension: row r = token (r / G) x head (r % G),
-// 128 rows = floor(128 / G) tokens, so one K/V tile feeds all G heads.
-// Warp roles (256 threads = 2 warps per SM sub-partition, so up to 255
-// registers per thread; one CTA per SM):
-//   warps 0-3  softmax / correction / epilogue: thread r owns row r = TMEM
-//              lane r; reads S rows with tcgen05.ld, online softmax in the log2
-//              domain with lazy rescaling (O in TMEM is rescaled only when a
-//              row max grows by more than 2^8), writes P (bf16) to shared
-//              memory, final O / l to global;
-//   warps 4-6  loaders: gather the Q tile and each 64-key K/V tile from the
-//              pages with cp.async (16 B per thread-op) into 128B-swizzled
-//              K-major tiles (the UMMA canonical layout), 5-stage ring
-//              (64-key tiles: a deep ring hides the gather latency);
-//              cp.async.mbarrier.arrive signals a stage without blocking the
-//              loader (the MMA thread fences the generic->async proxy);
-//   warp 7     TMEM allocation, and one lane issues every tcgen05.mma:
-//              S = Q·Kᵀ (M=128, N=64, K=head_dim) into one of two TMEM S
-//              buffers, O += P·V (M=128, N=head_dim, K=64; V used MN-major)
-//              into the TMEM O accumulator; completion reaches the other
-//              roles through tcgen05.commit on mbarriers.
-// S(t+1) is issued before P(t)·V(t), so the tensor core computes the next
-// scores while the softmax warps work on the current ones; P is double
-// buffered, so the softmax of tile t+1 overlaps P(t)·V(t) (only a rare O
-// rescale waits for it).
+// Work decomposition. The G q heads of a kv head are packed into the MMA's M
+// dimension: Q-tile row r = token (r / G) x head (r % G), 128 rows =
+// floor(128 / G) tokens. A UNIT is a pair of consecutive Q tiles of one kv
+// head (256 rows) over the key tiles (128 keys) the pair may attend; each
+// K/V tile a CTA loads feeds BOTH Q tiles (half the K/V gather per FLOP of a
+// one-tile CTA). The units' key tiles are concatenated (kv head major) and
+// cut stream-K style into equal contiguous ranges, one per CTA (grid = SM
+// count, one CTA per SM): no wave tail, and causal units of unequal length
+// balance. A unit cut by range boundaries leaves one fp32 partial (O, m, l)
+// per CTA; the LAST CTA to publish its partial (ticket per unit) merges them
+// — no CTA ever waits for another, so any residency makes progress.
+//
+// Warp roles (512 threads, one CTA per SM, TMEM: S0 | S1 | O0 | O1; setmaxnreg
+// moves registers from the loader / MMA warpgroups to the softmax ones):
+//   warps 0-3   softmax warpgroup 0 (Q tile 0 of the unit): thread r owns
+//               row r = TMEM lane r; reads S0 with tcgen05.ld, online softmax
+//               in the log2 domain with lazy rescaling (O0 rescaled in TMEM
+//               only when a row max grows by more than 2^8), writes P0 (bf16)
+//               back into S0's columns, epilogue O0 / l (or a partial);
+//   warps 4-7   softmax warpgroup 1: the same for Q tile 1 (S1, O1);
+//   warps 8-11  loaders: Q pair once per unit segment, then each 128-key K
+//               and V tile gathered from the pages with cp.async (16 B per
+//               thread-op) into 128B-swizzled tiles (the UMMA canonical
+//               layout) through a ring of K|V halves; every thread owns two
+//               fixed tile rows and decodes their slot ids one tile ahead;
+//   warp 12     TMEM allocation; one lane issues every tcgen05.mma in the
+//               ping-pong order S0(0) S1(0) | PV0(t) S0(t+1) PV1(t) S1(t+1) |
+//               ..., so the tensor core computes one Q tile's scores / P·V
+//               while the other tile's warpgroup runs its softmax. P(t)
+//               aliases S(t) in TMEM: the MMAs of one thread execute in
+//               issue order, so S(t+1) overwrites P(t) only after P(t)·V(t)
+//               read it. Warps 13-15 only give their registers away.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -40,6 +47,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
+#include <vector>
 
 #include "cuda/attn_common.cuh"
 #include "cuda/device_impl.cuh"
@@ -58,14 +66,21 @@ struct PrefillArgs {
     int chunk;                // query tokens
     float scale_log2;
     float rescale_thr;        // lazy-rescale threshold (log2 units; 8)
-    unsigned long long* trace;  // PRISM_K4_TRACE: [5][1024] globaltimer stamps of CTA (0,0), else null
-    unsigned* dbg;            // PRISM_K4_DEBUG: host-mapped progress words (CTA (0,0) only), else null
+    int n_qp;                 // Q-tile pairs per kv head
+    const std::int32_t* qp_tiles;  // [n_qp + 1] key-tile prefix over the pairs (same for every kv head)
+    int per_cta;              // key tiles per CTA range
+    int total;                // key tiles of all units = n_kv * qp_tiles[n_qp]
+    float4* part_o;           // [2 * grid][D / 4][256] unnormalised O of cut units
+    float2* part_ml;          // [2 * grid][256] (m, l) of cut units
+    int* tickets;             // [n_kv * n_qp], zero between launches
+    unsigned long long* trace;  // PRISM_K4_TRACE: [5][1024] globaltimer stamps of CTA 0, else null
+    unsigned* dbg;            // PRISM_K4_DEBUG: host-mapped progress words (CTA 0 only), else null
 };
 
 // timeline stamp (no-op unless PRISM_K4_TRACE): role 0 loader issued tile t,
-// 1 S(t) issued, 2 P(t)·V(t) issued, 3 softmax has S(t), 4 softmax posted P(t)
+// 1 S0(t) issued, 2 P0(t)·V(t) issued, 3 warpgroup 0 has S0(t), 4 it posted P0(t)
 __device__ __forceinline__ void k4_stamp(unsigned long long* tr, int role, int t) {
-    if (tr && blockIdx.x == 0 && blockIdx.y == 0 && t < 1024) {
+    if (tr && blockIdx.x == 0 && t < 1024) {
         unsigned long long ns;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
         tr[role * 1024 + t] = ns;
@@ -74,7 +89,7 @@ __device__ __forceinline__ void k4_stamp(unsigned long long* tr, int role, int t
 
 // progress marker for hang diagnosis (no-op unless PRISM_K4_DEBUG)
 __device__ __forceinline__ void k4_mark(unsigned* dbg, int slot, unsigned v) {
-    if (dbg && blockIdx.x == 0 && blockIdx.y == 0) {
+    if (dbg && blockIdx.x == 0) {
         *reinterpret_cast<volatile unsigned*>(dbg + slot) = v;
         __threadfence_system();
     }
@@ -82,26 +97,29 @@ __device__ __forceinline__ void k4_mark(unsigned* dbg, int slot, unsigned v) {
 
 template <int D>
 struct PfShape {
-    static constexpr int kM = 128;            // MMA rows (packed token x head)
-    static constexpr int kN = 128;            // keys per K/V tile
-    static constexpr int kStages = 3;         // K/V ring depth
+    static constexpr int kM = 128;            // MMA rows per Q tile (packed token x head)
+    static constexpr int kN = 64;             // keys per K/V tile
     static constexpr int kSub = D / 64;       // 64-element (128 B) swizzle atoms along head_dim
-    static constexpr int kQB = kM * D * 2;    // Q tile bytes
-    static constexpr int kKB = kN * D * 2;    // K (or V) tile bytes
-    static constexpr int kStageB = 2 * kKB;   // K + V
-    static constexpr int kOffQ = 0;
-    static constexpr int kOffKV = kOffQ + kQB;
-    static constexpr int kOffRows = kOffKV + kStages * kStageB;  // [2][kN] K row offsets / 128 B (loaders)
-    static constexpr int kOffBar = kOffRows + 2 * kN * 4;
-    static constexpr int kBars = 2 * kStages + 8;
-    static constexpr int kSmem = kOffBar + kBars * 8 + 16 + 1024;  // + TMEM address slot + alignment slack
-    static constexpr int kThreads = 256;
-    static constexpr int kLoaders = 96;   // warps 4-6
-    static constexpr std::uint32_t kTmemCols = 512;  // S0 [0,128) S1 [128,256) O [256, 256+D)
-    // TMEM columns: S(t & 1) [kN each] | P(t & 1) [kN / 2 each: bf16 pairs] | O [D]
-    static constexpr std::uint32_t kColP = 2 * kN;
-    static constexpr std::uint32_t kColO = kColP + kN;
+    static constexpr int kQB = kM * D * 2;    // one Q tile
+    static constexpr int kHalfB = kN * D * 2;  // one K (or V) tile
+    static constexpr int kHalves = D == 128 ? 10 : 16;  // ring slots of K|V halves
+    static constexpr int kOffQ = 0;           // Q tiles 0 and 1
+    static constexpr int kOffKV = 2 * kQB;
+    static constexpr int kOffBar = kOffKV + kHalves * kHalfB;
+    // q_full | q_empty | kv_full[H] | kv_empty[H] | s_full[2][2] | p_full[2][2] | pv_done[2][2] | o_free[2]
+    static constexpr int kBars = 2 + 2 * kHalves + 14;
+    static constexpr int kOffMisc = kOffBar + kBars * 8;  // TMEM address, merge flag
+    static constexpr int kSmem = kOffMisc + 16 + 1024;    // + alignment slack
+    static constexpr int kThreads = 512;
+    static constexpr int kLoaders = 128;      // warps 8-11
+    // setmaxnreg split of the 64K registers: softmax warpgroups 0-1 grow,
+    // loader warpgroup 2 and the MMA warpgroup 3 shrink (2 x 128 x (168 + 88))
+    static constexpr int kRegsSoftmax = 168;
+    static constexpr int kRegsLoad = 88;
+    static constexpr std::uint32_t kTmemCols = 512;
+    static constexpr std::uint32_t kColO = 256;  // S0 buffers 0/1, S1 buffers 0/1 (kN each), O0, O1
 };
+static_assert(PfShape<128>::kSmem <= 232448, "K4 shared memory");
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ std::uint32_t saddr(const void* p) {
@@ -133,6 +151,10 @@ __device__ __forceinline__ void mb_arrive(std::uint32_t bar) {
 __device__ __forceinline__ void cp_async_arrive(std::uint32_t bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(bar) : "memory");
 }
+// 16-byte cp.async to a shared-window address (src_bytes 0: zero fill)
+__device__ __forceinline__ void cp_async16_s(std::uint32_t dst, const void* src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
+}
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -147,6 +169,30 @@ __device__ __forceinline__ void tc_mma(std::uint32_t d_tmem, std::uint64_t a_des
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
         " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
         "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// Warp-wide variants: every lane executes them with the same operands, one
+// elected lane issues (no divergent single-lane region around the uniform ops)
+__device__ __forceinline__ void tc_commit_e(std::uint32_t bar) {
+    asm volatile(
+        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_e(std::uint32_t d_tmem, std::uint64_t a_desc, std::uint64_t b_desc,
+                                         std::uint32_t idesc, std::uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ __forceinline__ void tc_mma_ts_e(std::uint32_t d_tmem, std::uint32_t a_tmem, std::uint64_t b_desc,
+                                            std::uint32_t idesc, std::uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 // 32 consecutive fp32 columns of this thread's TMEM lane
@@ -184,6 +230,31 @@ __device__ __forceinline__ void tc_st32(std::uint32_t taddr, const float (&v)[32
     asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
 }
 
+// 64 consecutive fp32 columns of this thread's TMEM lane, one load + wait
+// (the outputs are defined by the same asm statement as the wait)
+__device__ __forceinline__ void tc_ld64(std::uint32_t taddr, float (&v)[64]) {
+    std::uint32_t r[64];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x64.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32, %33, %34, %35, %36, %37, %38, %39, %40, %41, %42, %43, %44, %45, %46, %47, %48, %49, %50, %51, %52, %53, %54, %55, %56, %57, %58, %59, %60, %61, %62, %63}, [%64];\n"
+        "tcgen05.wait::ld.sync.aligned;\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31]), "=r"(r[32]), "=r"(r[33]), "=r"(r[34]), "=r"(r[35]), "=r"(r[36]), "=r"(r[37]), "=r"(r[38]), "=r"(r[39]), "=r"(r[40]), "=r"(r[41]), "=r"(r[42]), "=r"(r[43]), "=r"(r[44]), "=r"(r[45]), "=r"(r[46]), "=r"(r[47]), "=r"(r[48]), "=r"(r[49]), "=r"(r[50]), "=r"(r[51]), "=r"(r[52]), "=r"(r[53]), "=r"(r[54]), "=r"(r[55]), "=r"(r[56]), "=r"(r[57]), "=r"(r[58]), "=r"(r[59]), "=r"(r[60]), "=r"(r[61]), "=r"(r[62]), "=r"(r[63])
+        : "r"(taddr)
+        : "memory");
+#pragma unroll
+    for (int i = 0; i < 64; ++i) v[i] = __uint_as_float(r[i]);
+}
+// 32 consecutive 32-bit columns of this thread's TMEM lane (no wait)
+__device__ __forceinline__ void tc_st32_nowait(std::uint32_t taddr, const std::uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};\n" ::"r"(taddr),
+        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+        "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+        "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+
 // D[tmem] (+)= A[tmem] · B[smem]: the A operand (P) read from tensor memory,
 // lane = row, two bf16 K-elements per 32-bit column (8 columns per K=16 step)
 __device__ __forceinline__ void tc_mma_ts(std::uint32_t d_tmem, std::uint32_t a_tmem, std::uint64_t b_desc,
@@ -218,6 +289,17 @@ __device__ __forceinline__ std::uint64_t sw128_desc(std::uint32_t addr, std::uin
     d |= static_cast<std::uint64_t>(2) << 61;  // SWIZZLE_128B
     return d;
 }
+// The same descriptor split in two words: the low word (start address >> 4,
+// LBO >> 4) varies per operand tile and K step and never carries into the
+// high word (shared addresses < 256 KB), the high word (SBO 1024 B, version,
+// SWIZZLE_128B) is a constant. Offsets are added to the low word as >> 4.
+__device__ __forceinline__ std::uint32_t desc_lo(std::uint32_t addr, std::uint32_t lbo_bytes) {
+    return ((addr >> 4) & 0x3fffu) | (((lbo_bytes >> 4) & 0x3fffu) << 16);
+}
+__device__ __forceinline__ std::uint64_t desc_of(std::uint32_t lo) {
+    constexpr std::uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
+    return (static_cast<std::uint64_t>(kHi) << 32) | lo;
+}
 // Instruction descriptor, kind::f16: bf16 A/B, fp32 D, M x N, K-major A,
 // B K-major (b_mn = 0) or MN-major (b_mn = 1).
 __host__ __device__ constexpr std::uint32_t f16_idesc(int m, int n, int b_mn) {
@@ -231,48 +313,72 @@ __device__ __forceinline__ std::uint32_t sw_off(int r, int c) {
     return static_cast<std::uint32_t>((c >> 3) * (ROWS * 128) + r * 128 + (((c & 7) ^ (r & 7)) << 4));
 }
 
+// One unit segment of a CTA's key-tile range: unit (kv head h, Q-tile pair
+// qp) owns global key tiles [ustart, uend); the segment is [g0, g1).
+struct Seg {
+    int h, qp, ustart, uend, g0, g1;
+};
+
+__device__ __forceinline__ Seg seg_at(const PrefillArgs& a, int g, int g_end) {
+    const int per_head = __ldg(a.qp_tiles + a.n_qp);
+    Seg s;
+    s.h = g / per_head;
+    const int r = g - s.h * per_head;
+    int lo = 0, hi = a.n_qp;  // largest qp with qp_tiles[qp] <= r
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (__ldg(a.qp_tiles + mid) <= r) lo = mid;
+        else hi = mid;
+    }
+    s.qp = lo;
+    s.ustart = s.h * per_head + __ldg(a.qp_tiles + lo);
+    s.uend = s.h * per_head + __ldg(a.qp_tiles + lo + 1);
+    s.g0 = g;
+    s.g1 = min(s.uend, g_end);
+    return s;
+}
+
 template <int D, int G>
-__global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
+__global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
     using S = PfShape<D>;
     extern __shared__ unsigned char smem_raw[];
     // 1024-byte aligned base (SW128 atoms), derived by pointer arithmetic on
     // the shared array so accesses through it stay LDS / STS
     unsigned char* smem = smem_raw + ((1024u - (saddr(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    constexpr int kTQ = S::kM / G;  // query tokens per tile
-    const int h = blockIdx.y;       // kv head
-    const int i0 = blockIdx.x * kTQ;
-    const int tq = min(kTQ, a.chunk - i0);  // valid query tokens of this tile
-    if (tq <= 0) return;
+    constexpr int kTQ = S::kM / G;  // query tokens per Q tile
+    const int g_begin = blockIdx.x * a.per_cta;
+    const int g_end = min(a.total, g_begin + a.per_cta);
+    if (g_begin >= g_end) return;
     const int n_kv = a.g.n_kv, n_q = n_kv * G;
-    const int kv_len = a.first + i0 + tq;  // keys any row of the tile may attend
-    const int n_tiles = (kv_len + S::kN - 1) / S::kN;
 
     const std::uint32_t sQ = saddr(smem + S::kOffQ);
     const std::uint32_t sKV = saddr(smem + S::kOffKV);
     const std::uint32_t bar = saddr(smem + S::kOffBar);
-    // mbarriers: q | kv_full[kStages] | kv_empty[kStages] | s_full[2] | s_free[2] | p_full | pv_done[2]
-    const std::uint32_t b_q = bar, b_kvfull = bar + 8, b_kvempty = b_kvfull + 8 * S::kStages,
-                        b_sfull = b_kvempty + 8 * S::kStages, b_sfree = b_sfull + 16, b_pfull = b_sfree + 16,
-                        b_pvdone = b_pfull + 8;
-    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(smem + S::kOffBar + S::kBars * 8);
+    // q_full | q_empty | kv_full[H] | kv_empty[H] | s_full[2][2] | p_full[2][2] | pv_done[2][2] | o_free[2]
+    // ([j][b]: Q tile j, tile parity b)
+    const std::uint32_t b_qfull = bar, b_qempty = bar + 8, b_kvfull = bar + 16,
+                        b_kvempty = b_kvfull + 8 * S::kHalves, b_sfull = b_kvempty + 8 * S::kHalves,
+                        b_pfull = b_sfull + 32, b_pvdone = b_pfull + 32, b_ofree = b_pvdone + 32;
+    std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(smem + S::kOffMisc);
+    volatile int* merge_flag = reinterpret_cast<volatile int*>(smem + S::kOffMisc + 4);
 
     if (tid == 0) {
-        mb_init(b_q, S::kLoaders);
-        for (int s = 0; s < S::kStages; ++s) {
+        mb_init(b_qfull, S::kLoaders);
+        mb_init(b_qempty, 1);
+        for (int s = 0; s < S::kHalves; ++s) {
             mb_init(b_kvfull + 8 * s, S::kLoaders);
             mb_init(b_kvempty + 8 * s, 1);
         }
-        for (int s = 0; s < 2; ++s) {
-            mb_init(b_sfull + 8 * s, 1);
-            mb_init(b_sfree + 8 * s, 128);
+        for (int j = 0; j < 4; ++j) {
+            mb_init(b_sfull + 8 * j, 1);
+            mb_init(b_pfull + 8 * j, 128);
+            mb_init(b_pvdone + 8 * j, 1);
         }
-        mb_init(b_pfull, 128);
-        mb_init(b_pvdone, 1);
-        mb_init(b_pvdone + 8, 1);
+        for (int j = 0; j < 2; ++j) mb_init(b_ofree + 8 * j, 128);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
-    if (warp == 7) {
+    if (warp == 12) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(saddr(tmem_slot)),
                      "n"(S::kTmemCols)
                      : "memory");
@@ -282,257 +388,368 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
     __syncthreads();
     tc_fence_after();
     const std::uint32_t tmem = *tmem_slot;
+    // K half of local tile k is ring half 2k, its V half 2k + 1
+    auto half_slot = [](int idx) { return idx % S::kHalves; };
+    auto half_phase = [](int idx) { return static_cast<std::uint32_t>((idx / S::kHalves) & 1); };
 
-    if (warp >= 4 && warp < 7) {
+    if (warp >= 8 && warp < 12) {
         // ------------------------------------------------------------ loaders
-        const int lt = tid - 128;
-        constexpr int kCpr = D / 8;            // 16-byte chunks per row
-        constexpr int kRowsPerPass = S::kLoaders / kCpr;
-        const int c = lt % kCpr;
-        const int r0 = lt / kCpr;
-        // Q tile: row r = token (r / G) x head (r % G); padding rows zero
-        for (int r = r0; r < S::kM; r += kRowsPerPass) {
-            const int tok = r / G, g = r % G;
-            const bool ok = tok < tq && r < kTQ * G;
-            const __nv_bfloat16* src =
-                ok ? a.q + (static_cast<std::size_t>(i0 + tok) * n_q + static_cast<std::size_t>(h) * G + g) * D + c * 8
-                   : a.q;
-            cp_async16(smem + S::kOffQ + sw_off<S::kM>(r, c), src, ok ? 16 : 0);
-        }
-        cp_async_arrive(b_q);
-        if (lt == 0) k4_mark(a.dbg, 0, 1);
-
-        // Slot ids -> row byte offsets are decoded one tile ahead into shared
-        // memory (each loader owns keys lt and lt + 96 of a tile), so the
-        // block-table latency never sits between two cp.async issues.
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(S::kRegsLoad));
+        // Fixed rows per thread: lanes 2i and 2i+1 share a row (one 32-byte
+        // sector per lane pair and instruction), lane parity h picks the odd
+        // or even 16-byte chunks; loader warp w owns K/V tile row 16w + i (and
+        // rows 64m + 16w + i of the Q pair), so a thread decodes its own
+        // row's slot id one tile ahead in registers and each cp.async is one
+        // add + LDGSTS.
+        const int w = warp - 8, h = lane & 1;
+        const int ra = 16 * w + (lane >> 1);
+        constexpr int kCpl = D / 16;  // chunks per lane per row
         const char* base = reinterpret_cast<const char*>(a.g.base);
-        const std::uint64_t kblock = static_cast<std::uint64_t>(a.layer * 2 * n_kv + h) * a.g.tpp;
         const std::uint64_t v_delta = static_cast<std::uint64_t>(n_kv) * a.g.tpp * (D * 2);
-        // row start offsets in 128-byte units (rows are 128 / 256 B aligned;
-        // < 2^32 units for a 180 GB pool), kNone past the keys
-        std::uint32_t* offs = reinterpret_cast<std::uint32_t*>(smem + S::kOffRows);  // [2][kN]
-        constexpr std::uint32_t kNone = ~0u;
-        auto load_sid = [&](int t, int r) -> std::int32_t {
-            const int key = t * S::kN + r;
-            return (r < S::kN && key < kv_len) ? __ldg(a.row + key) : -1;
+        const int keys = a.first + a.chunk;  // the request's block-table row length
+        std::uint32_t dsw_kv[kCpl], dsw_q[kCpl];  // swizzled chunk offsets within a row
+#pragma unroll
+        for (int i = 0; i < kCpl; ++i) {
+            const int c = 2 * i + h;
+            dsw_kv[i] = static_cast<std::uint32_t>((c >> 3) * (S::kN * 128) + (((c & 7) ^ (ra & 7)) << 4));
+            dsw_q[i] = static_cast<std::uint32_t>((c >> 3) * (S::kM * 128) + (((c & 7) ^ (ra & 7)) << 4));
+        }
+        // src_bytes 0 (zero fill) reads nothing; q is a valid placeholder address
+        const char* dummy = reinterpret_cast<const char*>(a.q);
+        auto copy_row = [&](std::uint32_t dst_row, const std::uint32_t (&dsw)[kCpl], const char* src, bool ok) {
+            const char* p = (ok ? src : dummy) + h * 16;
+            const int bytes = ok ? 16 : 0;
+#pragma unroll
+            for (int i = 0; i < kCpl; ++i) cp_async16_s(dst_row + dsw[i], p + i * 32, bytes);
         };
-        auto decode = [&](std::int32_t sid_raw) -> std::uint32_t {
-            if (sid_raw < 0) return kNone;
+        auto load_sid = [&](int kt) -> std::int32_t {
+            const int key = kt * S::kN + ra;
+            return key < keys ? __ldg(a.row + key) : -1;
+        };
+        // byte offset of the row from the pool base, head block excluded; ~0: past the keys
+        auto decode = [&](std::int32_t sid_raw) -> std::uint64_t {
+            if (sid_raw < 0) return ~0ull;
             const std::uint32_t sid = static_cast<std::uint32_t>(sid_raw);
             const std::uint32_t page = slot_page(sid, a.g.magic);
             const std::uint32_t slot = sid - page * a.g.tpp;
-            return static_cast<std::uint32_t>(
-                (static_cast<std::uint64_t>(page) * a.g.page_bytes + (kblock + slot) * (D * 2)) >> 7);
+            return static_cast<std::uint64_t>(page) * a.g.page_bytes + static_cast<std::uint64_t>(slot) * (D * 2);
         };
-        auto store_offs = [&](int t, std::int32_t s0, std::int32_t s1) {
-            offs[(t & 1) * S::kN + lt] = decode(s0);
-            if (lt + S::kLoaders < S::kN) offs[(t & 1) * S::kN + lt + S::kLoaders] = decode(s1);
-        };
-        store_offs(0, load_sid(0, lt), load_sid(0, lt + S::kLoaders));
-        asm volatile("bar.sync 2, %0;\n" ::"n"(S::kLoaders) : "memory");
-        for (int t = 0; t < n_tiles; ++t) {
-            const int s = t % S::kStages;
-            std::int32_t n0 = -1, n1 = -1;
-            if (t + 1 < n_tiles) {
-                n0 = load_sid(t + 1, lt);
-                n1 = load_sid(t + 1, lt + S::kLoaders);
+        Seg la = seg_at(a, g_begin, g_end);  // look-ahead cursor (tile g + 1)
+        std::uint64_t oa = decode(load_sid(g_begin - la.ustart));
+        int g = g_begin, s_idx = 0;
+        while (g < g_end) {
+            const Seg sg = seg_at(a, g, g_end);
+            // Q pair of the unit: rows of tile j = token (r / G) x head (r % G), padding rows zero
+            if (s_idx > 0) mb_wait(b_qempty, (s_idx - 1) & 1);
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                const int r = ra + 64 * m, j = r >> 7, rr = r & 127;
+                const int tok = (2 * sg.qp + j) * kTQ + rr / G;
+                const bool ok = rr < kTQ * G && tok < a.chunk;
+                const char* src = reinterpret_cast<const char*>(
+                    a.q + (static_cast<std::size_t>(ok ? tok : 0) * n_q + static_cast<std::size_t>(sg.h) * G + rr % G) * D);
+                copy_row(sQ + j * S::kQB + rr * 128, dsw_q, src, ok);
             }
-            if (t >= S::kStages) mb_wait(b_kvempty + 8 * s, ((t / S::kStages) - 1) & 1);
-            unsigned char* kt = smem + S::kOffKV + s * S::kStageB;
-            unsigned char* vt = kt + S::kKB;
-            const std::uint32_t* to = offs + (t & 1) * S::kN;
-            for (int r = r0; r < S::kN; r += kRowsPerPass) {
-                const std::uint32_t off = to[r];
-                const char* srck = base;
-                int bytes = 0;
-                if (off != kNone) {
-                    srck = base + (static_cast<std::uint64_t>(off) << 7) + c * 16;
-                    bytes = 16;
+            cp_async_arrive(b_qfull);
+            const std::uint64_t kb = static_cast<std::uint64_t>(a.layer * 2 * n_kv + sg.h) * a.g.tpp * (D * 2);
+            for (; g < sg.g1; ++g) {
+                const int k = g - g_begin;
+                std::int32_t na = -1;
+                if (g + 1 < g_end) {
+                    if (g + 1 >= la.g1) la = seg_at(a, g + 1, g_end);
+                    na = load_sid(g + 1 - la.ustart);
                 }
-                cp_async16(kt + sw_off<S::kN>(r, c), srck, bytes);
-                cp_async16(vt + sw_off<S::kN>(r, c), bytes ? srck + v_delta : srck, bytes);
+#pragma unroll
+                for (int kv = 0; kv < 2; ++kv) {
+                    const int idx = 2 * k + kv;
+                    const int hs = half_slot(idx);
+                    if (idx >= S::kHalves) mb_wait(b_kvempty + 8 * hs, half_phase(idx) ^ 1u);
+                    copy_row(sKV + hs * S::kHalfB + ra * 128, dsw_kv, base + kb + (kv ? v_delta : 0) + oa, oa != ~0ull);
+                    cp_async_arrive(b_kvfull + 8 * hs);
+                }
+                if (lane == 0 && w == 0) k4_stamp(a.trace, 0, k);
+                oa = decode(na);
             }
-            cp_async_arrive(b_kvfull + 8 * s);
-            if (lt == 0) k4_mark(a.dbg, 1, 100 + t);
-            if (lt == 0) k4_stamp(a.trace, 0, t);
-            if (t + 1 < n_tiles) {
-                store_offs(t + 1, n0, n1);
-                asm volatile("bar.sync 2, %0;\n" ::"n"(S::kLoaders) : "memory");
-            }
+            ++s_idx;
         }
-    } else if (warp == 7) {
-        // ------------------------------------------------------------ MMA issue
-        if (lane == 0) {
+    } else if (warp >= 12) {
+        // ------------------------------------------------------------ MMA issue (warp 12)
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(S::kRegsLoad));
+        // the whole warp runs the issue loop (uniform control flow and operands
+        // in uniform registers); one elected lane issues each tcgen05 op
+        if (warp == 12) {
             constexpr std::uint32_t idesc_s = f16_idesc(S::kM, S::kN, 0);
             constexpr std::uint32_t idesc_o = f16_idesc(S::kM, D, 1);
-            mb_wait(b_q, 0);
-            fence_proxy_async();  // cp.async (generic proxy) data -> tcgen05.mma (async proxy)
-            k4_mark(a.dbg, 2, 1);
-            auto issue_s = [&](int t) {
-                const int s = t & 1, ks = t % S::kStages;  // S buffer, K/V stage
-                mb_wait(b_kvfull + 8 * ks, (t / S::kStages) & 1);
-                if (t >= 2) mb_wait(b_sfree + 8 * s, ((t >> 1) - 1) & 1);
-                fence_proxy_async();
+            const int n = g_end - g_begin;
+            auto wait_half = [&](int idx) {
+                mb_wait(b_kvfull + 8 * half_slot(idx), half_phase(idx));
+                fence_proxy_async();  // cp.async (generic proxy) data -> tcgen05.mma (async proxy)
                 tc_fence_after();
-                const std::uint32_t kt = sKV + ks * S::kStageB;
-#pragma unroll
-                for (int k = 0; k < D / 16; ++k) {
-                    const std::uint32_t offq = (k >> 2) * (S::kM * 128) + (k & 3) * 32;
-                    const std::uint32_t offk = (k >> 2) * (S::kN * 128) + (k & 3) * 32;
-                    tc_mma(tmem + s * S::kN, sw128_desc(sQ + offq, 16), sw128_desc(kt + offk, 16), idesc_s, k > 0);
+            };
+            // S_j(k) = Q_j · K(k)ᵀ into S buffer (j, k & 1), for both Q tiles;
+            // runs two tiles ahead of the P·V MMAs
+            Seg sc = seg_at(a, g_begin, g_end);
+            int sc_idx = 0;
+            auto issue_s = [&](int k) {
+                const int g = g_begin + k;
+                if (g >= sc.g1) {  // a new unit segment: its Q pair
+                    sc = seg_at(a, g, g_end);
+                    ++sc_idx;
                 }
-                tc_commit(b_sfull + 8 * s);
-                k4_mark(a.dbg, 3, 100 + t);
-                k4_stamp(a.trace, 1, t);
+                if (g == sc.g0) {
+                    mb_wait(b_qfull, sc_idx & 1);
+                    fence_proxy_async();
+                }
+                wait_half(2 * k);
+                const std::uint32_t dk = desc_lo(sKV + half_slot(2 * k) * S::kHalfB, 16);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    const std::uint32_t dq = desc_lo(sQ + j * S::kQB, 16);
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        // +16 B >> 4 per K=16 step inside a 128-byte atom, next atom 128 rows on
+                        const std::uint32_t offq = ((kk >> 2) * (S::kM * 128) + (kk & 3) * 32) >> 4;
+                        const std::uint32_t offk = ((kk >> 2) * (S::kN * 128) + (kk & 3) * 32) >> 4;
+                        tc_mma_e(tmem + j * 2 * S::kN + (k & 1) * S::kN, desc_of(dq + offq), desc_of(dk + offk), idesc_s,
+                               kk > 0);
+                    }
+                    tc_commit_e(b_sfull + 8 * (2 * j + (k & 1)));
+                }
+                tc_commit_e(b_kvempty + 8 * half_slot(2 * k));
+                if (g + 1 == sc.g1) tc_commit_e(b_qempty);  // last S of the segment: Q may be replaced
+                if (lane == 0) k4_stamp(a.trace, 1, k);
             };
             issue_s(0);
-            for (int t = 0; t < n_tiles; ++t) {
-                if (t + 1 < n_tiles) issue_s(t + 1);
-                mb_wait(b_pfull, t & 1);
-                tc_fence_after();
-                const std::uint32_t vt = sKV + (t % S::kStages) * S::kStageB + S::kKB;
-#pragma unroll
-                for (int k = 0; k < S::kN / 16; ++k) {
-                    tc_mma_ts(tmem + S::kColO, tmem + S::kColP + (t & 1) * (S::kN / 2) + k * 8,
-                              sw128_desc(vt + k * 2048, S::kN * 128), idesc_o, (t > 0 || k > 0) ? 1u : 0u);
+            if (n > 1) issue_s(1);
+            Seg pc = seg_at(a, g_begin, g_end);
+            int pc_idx = 0;
+            for (int k = 0; k < n; ++k) {
+                const int g = g_begin + k;
+                if (g >= pc.g1) {
+                    pc = seg_at(a, g, g_end);
+                    ++pc_idx;
                 }
-                tc_commit(b_pvdone + 8 * (t & 1));
-                tc_commit(b_kvempty + 8 * (t % S::kStages));
-                k4_mark(a.dbg, 4, 100 + t);
-                k4_stamp(a.trace, 2, t);
+                const bool fresh = g == pc.g0;
+                wait_half(2 * k + 1);
+                const std::uint32_t dv = desc_lo(sKV + half_slot(2 * k + 1) * S::kHalfB, S::kN * 128);
+#pragma unroll
+                for (int j = 0; j < 2; ++j) {
+                    // O_j (+)= P_j(k) · V(k), P_j in S buffer (j, k & 1)
+                    mb_wait(b_pfull + 8 * (2 * j + (k & 1)), (k >> 1) & 1);
+                    if (fresh && pc_idx > 0) mb_wait(b_ofree + 8 * j, (pc_idx - 1) & 1);
+                    tc_fence_after();
+#pragma unroll
+                    for (int kk = 0; kk < S::kN / 16; ++kk) {
+                        tc_mma_ts_e(tmem + S::kColO + j * D, tmem + j * 2 * S::kN + (k & 1) * S::kN + kk * 8,
+                                  desc_of(dv + kk * (2048 >> 4)), idesc_o, (!fresh || kk > 0) ? 1u : 0u);
+                    }
+                    tc_commit_e(b_pvdone + 8 * (2 * j + (k & 1)));
+                    if (j == 0 && lane == 0) k4_stamp(a.trace, 2, k);
+                }
+                tc_commit_e(b_kvempty + 8 * half_slot(2 * k + 1));
+                if (k + 2 < n) issue_s(k + 2);
             }
         }
         __syncwarp();
     } else {
-        // ------------------------------------------------------------ softmax
-        const int r = tid;                      // row = TMEM lane
-        const std::uint32_t lane_base = static_cast<std::uint32_t>(warp * 32) << 16;
-        const int tok = r / G;
-        const bool row_ok = tok < tq && r < kTQ * G;
-        const int pos = row_ok ? a.first + i0 + tok : -1;  // last key this row may attend
-        float m_run = -INFINITY, l_run = 0.f;
-        // PV(j) completes phase j >> 1 of pv_done[j & 1] (one barrier per P
-        // buffer): PV(j + 2) needs this warpgroup's P(j + 2), so a barrier is
-        // never two phases ahead of a wait here and parity waits are exact
-        auto ensure_pv = [&](int j) {
-            mb_wait(b_pvdone + 8 * (j & 1), (j >> 1) & 1);
+        // ------------------------------------------------------------ softmax warpgroups
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(S::kRegsSoftmax));
+        const int j = warp >> 2;  // Q tile of the unit
+        const int r = tid & 127;  // row = TMEM lane
+        const std::uint32_t lane_base = static_cast<std::uint32_t>((warp & 3) * 32) << 16;
+        const std::uint32_t tO = tmem + lane_base + S::kColO + j * D;
+        const int tq = r / G;
+        const int row = j * S::kM + r;  // row of the unit (partials)
+        int k = 0, g = g_begin;
+        // PV_j(k) completes phase k >> 1 of pv_done[j][k & 1]. Whenever this
+        // warpgroup waits for PV_j(k) (k = its current tile - 1 or its last
+        // tile), PV_j(k-2) is complete (it was issued before S_j(k), and MMAs
+        // and their commits complete in issue order) and PV_j(k+2) cannot
+        // be issued yet (it needs this warpgroup's P_j(k+2)): the parity
+        // wait is exact.
+        auto wait_pv = [&](int kk) {
+            mb_wait(b_pvdone + 8 * (2 * j + (kk & 1)), (kk >> 1) & 1);
             tc_fence_after();
         };
-        for (int t = 0; t < n_tiles; ++t) {
-            const int s = t & 1;
-            mb_wait(b_sfull + 8 * s, (t >> 1) & 1);
-            tc_fence_after();
-            if (r == 0) k4_mark(a.dbg, 5, 100 + t);
-            if (r == 0) k4_stamp(a.trace, 3, t);
-            const std::uint32_t ts = tmem + lane_base + s * S::kN;
-            const int k0 = t * S::kN;
-            // pass 1: row max of this tile (scaled, log2 domain)
-            // (8 independent partial maxima / sums: one warp per scheduler, so
-            // the reductions must not be one serial dependency chain; tiles
-            // entirely below the diagonal skip the causal mask)
-            const bool full = k0 + S::kN - 1 <= pos;
-            const int lim = pos - k0;  // last visible column of this tile
-            float mx[8];
+        while (g < g_end) {
+            const Seg sg = seg_at(a, g, g_end);
+            const int tok = (2 * sg.qp + j) * kTQ + tq;
+            const bool row_ok = r < kTQ * G && tok < a.chunk;
+            const int pos = row_ok ? a.first + tok : -1;  // last key this row may attend
+            float m_run = -INFINITY, l_run = 0.f;
+            for (; g < sg.g1; ++g, ++k) {
+                const int b = k & 1;
+                mb_wait(b_sfull + 8 * (2 * j + b), (k >> 1) & 1);
+                tc_fence_after();
+                if (j == 0 && r == 0) k4_stamp(a.trace, 3, k);
+                const std::uint32_t tS = tmem + lane_base + j * 2 * S::kN + b * S::kN;
+                const int k0 = (g - sg.ustart) * S::kN;
+                // the tile's S row in registers (one tcgen05.ld wait), row max
+                // with 8 independent partial maxima; tiles entirely below the
+                // diagonal skip the causal mask
+                const bool full = k0 + S::kN - 1 <= pos;
+                const int lim = pos - k0;  // last visible column of this tile
+                static_assert(S::kN == 64, "one x64 TMEM load per S row");
+                float v[S::kN];
+                tc_ld64(tS, v);
+                if (!full) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
-#pragma unroll
-            for (int cc = 0; cc < S::kN / 32; ++cc) {
-                float v[32];
-                tc_ld32(ts + cc * 32, v);
-                if (full) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) mx[j & 7] = fmaxf(mx[j & 7], v[j]);
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) mx[j & 7] = fmaxf(mx[j & 7], cc * 32 + j <= lim ? v[j] : -INFINITY);
+                    for (int q = 0; q < S::kN; ++q) v[q] = q <= lim ? v[q] : -INFINITY;
                 }
-            }
-            float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])), fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-            mt *= a.scale_log2;  // scale > 0: max commutes with the scaling
-            // lazy rescale (threshold 2^8): only when the max grows a lot
-            bool rescale = false;
-            float alpha = 1.f;
-            if (mt > m_run + a.rescale_thr) {
-                if (m_run != -INFINITY) {
-                    alpha = fast_exp2(m_run - mt);
-                    rescale = true;
-                }
-                m_run = mt;
-                l_run *= alpha;
-            }
-            const float m_use = m_run == -INFINITY ? 0.f : m_run;
-            // P(t) goes to P buffer t & 1, last read by PV(t-2)
-            if (t >= 2) ensure_pv(t - 2);
-            // pass 2: p = exp2(s - m), row sum, bf16 P into the swizzled K-major P tile
-            float ls[8];
+                float mx[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) ls[j] = 0.f;
+                for (int q = 0; q < 8; ++q) mx[q] = v[q];
 #pragma unroll
-            for (int cc = 0; cc < S::kN / 32; ++cc) {
-                float v[32];
-                tc_ld32(ts + cc * 32, v);
-                std::uint32_t pk[16];
-#pragma unroll
-                for (int j = 0; j < 32; j += 2) {
-                    float p0 = fast_exp2(fmaf(v[j], a.scale_log2, -m_use));
-                    float p1 = fast_exp2(fmaf(v[j + 1], a.scale_log2, -m_use));
-                    if (!full) {
-                        p0 = cc * 32 + j <= lim ? p0 : 0.f;
-                        p1 = cc * 32 + j + 1 <= lim ? p1 : 0.f;
+                for (int q = 8; q < S::kN; ++q) mx[q & 7] = fmaxf(mx[q & 7], v[q]);
+                float mt = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+                mt *= a.scale_log2;  // scale > 0: max commutes with the scaling
+                bool rescale = false;
+                float alpha = 1.f;
+                if (mt > m_run + a.rescale_thr) {
+                    if (m_run != -INFINITY) {
+                        alpha = fast_exp2(m_run - mt);
+                        rescale = true;
                     }
-                    ls[(j >> 1) & 7] += p0 + p1;
-                    pk[j >> 1] = pack_bf16(p0, p1);
+                    m_run = mt;
+                    l_run *= alpha;
                 }
-                // P straight into tensor memory (the P·V MMA reads A from TMEM)
-                tc_st16_nowait(tmem + lane_base + S::kColP + (t & 1) * (S::kN / 2) + cc * 16, pk);
+                const float m_use = m_run == -INFINITY ? 0.f : m_run;
+                // O_j *= alpha for the rows whose max moved (warp-collective
+                // TMEM access; rare with the 2^8 threshold): PV_j(k-1) must be
+                // complete (never needed on a unit's first tile: m was -inf)
+                if (__any_sync(0xffffffffu, rescale)) {
+                    wait_pv(k - 1);
+#pragma unroll
+                    for (int cc = 0; cc < D / 32; ++cc) {
+                        float o[32];
+                        tc_ld32(tO + cc * 32, o);
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) o[q] *= alpha;
+                        tc_st32(tO + cc * 32, o);
+                    }
+                }
+                // p = exp2(s - m) (masked s = -inf -> 0), row sum, bf16 P over
+                // the buffer's first columns (the S row is already in registers)
+                float ls[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) ls[q] = 0.f;
+                std::uint32_t pk[S::kN / 2];
+#pragma unroll
+                for (int q = 0; q < S::kN; q += 2) {
+                    const float p0 = fast_exp2(fmaf(v[q], a.scale_log2, -m_use));
+                    const float p1 = fast_exp2(fmaf(v[q + 1], a.scale_log2, -m_use));
+                    ls[(q >> 1) & 7] += p0 + p1;
+                    pk[q >> 1] = pack_bf16(p0, p1);
+                }
+                tc_st32_nowait(tS, pk);
+                asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+                l_run += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+                tc_fence_before();
+                mb_arrive(b_pfull + 8 * (2 * j + b));
+                if (j == 0 && r == 0) k4_stamp(a.trace, 4, k);
             }
-            asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-            l_run += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
-            tc_fence_before();
-            mb_arrive(b_sfree + 8 * s);
-            // O *= alpha for the rows whose max moved (warp-collective TMEM
-            // access; rare with the 2^8 threshold): O must be settled, PV(t-1) done
-            if (__any_sync(0xffffffffu, rescale)) {
-                ensure_pv(t - 1);
+            // ---- epilogue of the unit segment: O_j complete after PV_j(last)
+            wait_pv(k - 1);
+            const int u = sg.h * a.n_qp + sg.qp;
+            const int first_cta = sg.ustart / a.per_cta, last_cta = (sg.uend - 1) / a.per_cta;
+            const int parts = last_cta - first_cta + 1;
+            __nv_bfloat16* dst =
+                row_ok ? a.out + (static_cast<std::size_t>(tok) * n_q + static_cast<std::size_t>(sg.h) * G + r % G) * D
+                       : nullptr;
+            if (parts == 1) {
+                const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll
                 for (int cc = 0; cc < D / 32; ++cc) {
-                    float v[32];
-                    const std::uint32_t to = tmem + lane_base + S::kColO + cc * 32;
-                    tc_ld32(to, v);
+                    float o[32];
+                    tc_ld32(tO + cc * 32, o);
+                    if (row_ok) {
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] *= alpha;
-                    tc_st32(to, v);
+                        for (int q = 0; q < 32; q += 8) {
+                            *reinterpret_cast<uint4*>(dst + cc * 32 + q) =
+                                make_uint4(pack_bf16(o[q] * inv, o[q + 1] * inv), pack_bf16(o[q + 2] * inv, o[q + 3] * inv),
+                                           pack_bf16(o[q + 4] * inv, o[q + 5] * inv),
+                                           pack_bf16(o[q + 6] * inv, o[q + 7] * inv));
+                        }
+                    }
                 }
-            }
-            tc_fence_before();
-            mb_arrive(b_pfull);
-            if (r == 0) k4_mark(a.dbg, 6, 100 + t);
-            if (r == 0) k4_stamp(a.trace, 4, t);
-        }
-        // epilogue: O / l -> bf16 -> out[token][h*G + g][:]
-        ensure_pv(n_tiles - 1);
-        if (r == 0) k4_mark(a.dbg, 7, 1);
-        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        __nv_bfloat16* dst =
-            row_ok ? a.out + (static_cast<std::size_t>(i0 + tok) * n_q + static_cast<std::size_t>(h) * G + r % G) * D
-                   : nullptr;
+                tc_fence_before();
+                mb_arrive(b_ofree + 8 * j);
+            } else {
+                // publish this CTA's partial of the unit (slot 2c: the range's
+                // first segment, 2c + 1: its last), then the last publisher merges
+                const int slot = 2 * static_cast<int>(blockIdx.x) + (sg.g0 == g_begin ? 0 : 1);
 #pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) {
-            float v[32];
-            tc_ld32(tmem + lane_base + S::kColO + cc * 32, v);
-            if (row_ok) {
+                for (int cc = 0; cc < D / 32; ++cc) {
+                    float o[32];
+                    tc_ld32(tO + cc * 32, o);
 #pragma unroll
-                for (int j = 0; j < 32; j += 8) {
-                    *reinterpret_cast<uint4*>(dst + cc * 32 + j) =
-                        make_uint4(pack_bf16(v[j] * inv, v[j + 1] * inv), pack_bf16(v[j + 2] * inv, v[j + 3] * inv),
-                                   pack_bf16(v[j + 4] * inv, v[j + 5] * inv), pack_bf16(v[j + 6] * inv, v[j + 7] * inv));
+                    for (int q = 0; q < 8; ++q)
+                        a.part_o[(static_cast<std::size_t>(slot) * (D / 4) + cc * 8 + q) * 256 + row] =
+                            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                }
+                a.part_ml[static_cast<std::size_t>(slot) * 256 + row] = make_float2(m_run, l_run);
+                tc_fence_before();
+                mb_arrive(b_ofree + 8 * j);
+                __threadfence();
+                asm volatile("bar.sync 1, 256;\n" ::: "memory");
+                if (tid == 0) {
+                    const int prev = atomicAdd(a.tickets + u, 1);
+                    const int last = prev == parts - 1;
+                    if (last) a.tickets[u] = 0;  // no other CTA touches it again in this launch
+                    __threadfence();
+                    *merge_flag = last;
+                }
+                asm volatile("bar.sync 1, 256;\n" ::: "memory");
+                if (*merge_flag) {
+                    __threadfence();
+                    // online combination of the parts' (m, l, O) rows
+                    auto slot_of = [&](int cta) { return 2 * cta + (cta * a.per_cta >= sg.ustart ? 0 : 1); };
+                    float mm = -INFINITY;
+                    for (int cta = first_cta; cta <= last_cta; ++cta)
+                        mm = fmaxf(mm, __ldcg(a.part_ml + static_cast<std::size_t>(slot_of(cta)) * 256 + row).x);
+                    float ll = 0.f;
+                    for (int cta = first_cta; cta <= last_cta; ++cta) {
+                        const float2 ml = __ldcg(a.part_ml + static_cast<std::size_t>(slot_of(cta)) * 256 + row);
+                        ll += ml.x == -INFINITY ? 0.f : ml.y * fast_exp2(ml.x - mm);
+                    }
+                    const float inv = ll > 0.f ? 1.f / ll : 0.f;
+#pragma unroll 1
+                    for (int cg = 0; cg < D / 32; ++cg) {
+                        float4 acc[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        for (int cta = first_cta; cta <= last_cta; ++cta) {
+                            const int sl = slot_of(cta);
+                            const float pm = __ldcg(a.part_ml + static_cast<std::size_t>(sl) * 256 + row).x;
+                            const float wt = pm == -INFINITY ? 0.f : fast_exp2(pm - mm) * inv;
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const float4 o4 =
+                                    __ldcg(a.part_o + (static_cast<std::size_t>(sl) * (D / 4) + cg * 8 + q) * 256 + row);
+                                acc[q].x += wt * o4.x;
+                                acc[q].y += wt * o4.y;
+                                acc[q].z += wt * o4.z;
+                                acc[q].w += wt * o4.w;
+                            }
+                        }
+                        if (row_ok) {
+#pragma unroll
+                            for (int q = 0; q < 8; q += 2) {
+                                *reinterpret_cast<uint4*>(dst + cg * 32 + 4 * q) =
+                                    make_uint4(pack_bf16(acc[q].x, acc[q].y), pack_bf16(acc[q].z, acc[q].w),
+                                               pack_bf16(acc[q + 1].x, acc[q + 1].y),
+                                               pack_bf16(acc[q + 1].z, acc[q + 1].w));
+                            }
+                        }
+                    }
                 }
             }
         }
         tc_fence_before();
     }
     __syncthreads();
-    if (warp == 7) {
+    if (warp == 12) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(S::kTmemCols)
                      : "memory");
@@ -540,30 +757,28 @@ __global__ void __launch_bounds__(256, 1) k4_prefill(PrefillArgs a) {
 }
 
 template <int D, int G>
-void launch_pf(const PrefillArgs& a, cudaStream_t stream) {
+void launch_pf(const PrefillArgs& a, int grid, cudaStream_t stream) {
     using S = PfShape<D>;
     static bool init = false;
     if (!init) {
         PRISM_CUDA(cudaFuncSetAttribute(k4_prefill<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmem));
         init = true;
     }
-    constexpr int kTQ = S::kM / G;
-    const dim3 grid(static_cast<unsigned>((a.chunk + kTQ - 1) / kTQ), static_cast<unsigned>(a.g.n_kv));
     k4_prefill<D, G><<<grid, S::kThreads, S::kSmem, stream>>>(a);
     PRISM_CUDA(cudaGetLastError());
 }
 
 template <int D>
-void launch_pf_d(int group, const PrefillArgs& a, cudaStream_t stream) {
+void launch_pf_d(int group, const PrefillArgs& a, int grid, cudaStream_t stream) {
     switch (group) {
-        case 1: launch_pf<D, 1>(a, stream); break;
-        case 2: launch_pf<D, 2>(a, stream); break;
-        case 3: launch_pf<D, 3>(a, stream); break;
-        case 4: launch_pf<D, 4>(a, stream); break;
-        case 5: launch_pf<D, 5>(a, stream); break;
-        case 6: launch_pf<D, 6>(a, stream); break;
-        case 7: launch_pf<D, 7>(a, stream); break;
-        case 8: launch_pf<D, 8>(a, stream); break;
+        case 1: launch_pf<D, 1>(a, grid, stream); break;
+        case 2: launch_pf<D, 2>(a, grid, stream); break;
+        case 3: launch_pf<D, 3>(a, grid, stream); break;
+        case 4: launch_pf<D, 4>(a, grid, stream); break;
+        case 5: launch_pf<D, 5>(a, grid, stream); break;
+        case 6: launch_pf<D, 6>(a, grid, stream); break;
+        case 7: launch_pf<D, 7>(a, grid, stream); break;
+        case 8: launch_pf<D, 8>(a, grid, stream); break;
         default: throw std::runtime_error("prefill_attention: unsupported GQA group");
     }
 }
@@ -583,7 +798,7 @@ static unsigned* k4_debug_words() {
     return dev;
 }
 
-// Progress words of the last K4 launch's CTA (0,0) (PRISM_K4_DEBUG), readable
+// Progress words of the last K4 launch's CTA 0 (PRISM_K4_DEBUG), readable
 // while the kernel runs; 0 words when debugging is off.
 static unsigned long long* k4_trace_buf() {
     static unsigned long long* dev = [] {
@@ -613,11 +828,60 @@ int k4_debug_read(unsigned* out, int n) {
     return m;
 }
 
+// Host side of the launch, shared by the engine path (EngineDeviceImpl) and
+// the pool-level op (PagedCtx): the key-tile prefix over the Q-tile pairs
+// depends only on (first, chunk), so it is uploaded once per chunk, not per
+// layer; the stream-K cut uses one CTA per SM.
+template <class Ctx>
+void launch_k4(Ctx& d, PrefillArgs a) {
+    constexpr int kN = 64;
+    static const int sms = [] {
+        int dev = 0, n = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (const char* e = std::getenv("PRISM_K4_SMS")) n = std::max(1, std::min(n, std::atoi(e)));  // experiments
+        return n;
+    }();
+    const int tq = 128 / d.group;
+    const int n_qp = ((a.chunk + tq - 1) / tq + 1) / 2;
+    if (d.pf_first != a.first || d.pf_chunk != a.chunk) {
+        d.pf_prefix.ensure(static_cast<std::size_t>(n_qp) + 1);
+        std::int32_t acc = 0;
+        for (int qp = 0; qp < n_qp; ++qp) {
+            d.pf_prefix.host[qp] = acc;
+            const int kv_len = a.first + std::min(a.chunk, (2 * qp + 2) * tq);
+            acc += (kv_len + kN - 1) / kN;
+        }
+        d.pf_prefix.host[n_qp] = acc;
+        d.pf_prefix.upload(static_cast<std::size_t>(n_qp) + 1, d.stream);
+        d.pf_first = a.first;
+        d.pf_chunk = a.chunk;
+        d.pf_per_head = acc;
+    }
+    a.n_qp = n_qp;
+    a.qp_tiles = d.pf_prefix.dev;
+    a.total = d.n_kv * d.pf_per_head;
+    a.per_cta = std::max(4, (a.total + sms - 1) / sms);
+    const int grid = (a.total + a.per_cta - 1) / a.per_cta;
+    const std::size_t slots = 2 * static_cast<std::size_t>(grid);
+    float* ws = d.attn_workspace(slots * 256 * d.head_dim + slots * 256 * 2);
+    a.part_o = reinterpret_cast<float4*>(ws);
+    a.part_ml = reinterpret_cast<float2*>(ws + slots * 256 * d.head_dim);
+    a.tickets = d.attn_counters(static_cast<std::size_t>(d.n_kv) * n_qp);
+    a.dbg = k4_debug_words();
+    a.trace = k4_trace_buf();
+    d.k3_chain = false;
+    if (d.head_dim == 128) {
+        launch_pf_d<128>(d.group, a, grid, d.stream);
+    } else {
+        launch_pf_d<64>(d.group, a, grid, d.stream);
+    }
+}
+
 void launch_prefill_attention(EngineDeviceImpl& d, int layer, const void* q, void* out, float scale) {
     if (layer < 0 || layer >= d.n_layers) throw std::runtime_error("prefill_attention: bad layer");
     if (d.prefill_chunk <= 0) return;
     if (d.head_dim != 64 && d.head_dim != 128) throw std::runtime_error("prefill_attention: head_dim must be 64 or 128");
-    d.k3_chain = false;
     PrefillArgs a{};
     a.g = d.geom;
     a.layer = layer;
@@ -627,18 +891,12 @@ void launch_prefill_attention(EngineDeviceImpl& d, int layer, const void* q, voi
     a.first = d.prefill_first;
     a.chunk = d.prefill_chunk;
     a.scale_log2 = scale * 1.4426950408889634f;
-    a.dbg = k4_debug_words();
-    a.trace = k4_trace_buf();
     static const float thr = [] {
         const char* e = std::getenv("PRISM_K4_RESCALE_THR");
         return e ? static_cast<float>(std::atof(e)) : 8.f;
     }();
     a.rescale_thr = thr;
-    if (d.head_dim == 128) {
-        launch_pf_d<128>(d.group, a, d.stream);
-    } else {
-        launch_pf_d<64>(d.group, a, d.stream);
-    }
+    launch_k4(d, a);
 }
 
 void prefill_attention(msim::engine::Engine& eng, int layer, const void* q, void* out, float scale) {
@@ -652,7 +910,6 @@ void PagedCtx::prefill_attention(int layer, const std::int32_t* slot_ids, int fi
     if (first < 0) throw std::invalid_argument("paged prefill_attention: first must be >= 0");
     if (!slot_ids || !q || !out) throw std::invalid_argument("paged prefill_attention: null pointer");
     PRISM_CUDA(cudaSetDevice(vmm->ordinal()));
-    k3_chain = false;
     PrefillArgs a{};
     a.g = geom;
     a.layer = layer;
@@ -662,14 +919,8 @@ void PagedCtx::prefill_attention(int layer, const std::int32_t* slot_ids, int fi
     a.first = first;
     a.chunk = n_tokens;
     a.scale_log2 = scale * 1.4426950408889634f;
-    a.dbg = k4_debug_words();
-    a.trace = k4_trace_buf();
     a.rescale_thr = 8.f;
-    if (head_dim == 128) {
-        launch_pf_d<128>(group, a, stream);
-    } else {
-        launch_pf_d<64>(group, a, stream);
-    }
+    launch_k4(*this, a);
 }
 
 int last_step_prefill_tokens(const msim::engine::Engine& eng) { return impl_of(eng).prefill_chunk; }
