@@ -11,7 +11,7 @@
 // Work decomposition. The G q heads of a kv head are packed into the MMA's M
 // dimension: Q-tile row r = token (r / G) x head (r % G), 128 rows =
 // floor(128 / G) tokens. A UNIT is a pair of consecutive Q tiles of one kv
-// head (256 rows) over the key tiles (128 keys) the pair may attend; each
+// head (256 rows) over the key tiles (64 keys) the pair may attend; each
 // K/V tile a CTA loads feeds BOTH Q tiles (half the K/V gather per FLOP of a
 // one-tile CTA). The units' key tiles are concatenated (kv head major) and
 // cut stream-K style into equal contiguous ranges, one per CTA (grid = SM
@@ -20,26 +20,30 @@
 // per CTA; the LAST CTA to publish its partial (ticket per unit) merges them
 // — no CTA ever waits for another, so any residency makes progress.
 //
-// Warp roles (512 threads, one CTA per SM, TMEM: S0 | S1 | O0 | O1; setmaxnreg
-// moves registers from the loader / MMA warpgroups to the softmax ones):
+// Warp roles (512 threads, one CTA per SM; TMEM: S0 buffers 0/1 | S1 buffers
+// 0/1 (64 columns each) | O0 | O1; setmaxnreg moves registers from the loader
+// / MMA warpgroups to the softmax ones):
 //   warps 0-3   softmax warpgroup 0 (Q tile 0 of the unit): thread r owns
-//               row r = TMEM lane r; reads S0 with tcgen05.ld, online softmax
-//               in the log2 domain with lazy rescaling (O0 rescaled in TMEM
-//               only when a row max grows by more than 2^8), writes P0 (bf16)
-//               back into S0's columns, epilogue O0 / l (or a partial);
+//               row r = TMEM lane r; reads an S0 buffer with one tcgen05.ld,
+//               online softmax in the log2 domain with lazy rescaling (O0
+//               rescaled in TMEM only when a row max grows by more than 2^8),
+//               writes P0 (bf16) back into the buffer's columns, epilogue
+//               O0 / l (or a partial);
 //   warps 4-7   softmax warpgroup 1: the same for Q tile 1 (S1, O1);
-//   warps 8-11  loaders: Q pair once per unit segment, then each 128-key K
+//   warps 8-11  loaders: Q pair once per unit segment, then each 64-key K
 //               and V tile gathered from the pages with cp.async (16 B per
 //               thread-op) into 128B-swizzled tiles (the UMMA canonical
-//               layout) through a ring of K|V halves; every thread owns two
-//               fixed tile rows and decodes their slot ids one tile ahead;
-//   warp 12     TMEM allocation; one lane issues every tcgen05.mma in the
-//               ping-pong order S0(0) S1(0) | PV0(t) S0(t+1) PV1(t) S1(t+1) |
-//               ..., so the tensor core computes one Q tile's scores / P·V
-//               while the other tile's warpgroup runs its softmax. P(t)
-//               aliases S(t) in TMEM: the MMAs of one thread execute in
-//               issue order, so S(t+1) overwrites P(t) only after P(t)·V(t)
-//               read it. Warps 13-15 only give their registers away.
+//               layout) through a ring of K|V halves; every thread owns a
+//               fixed tile row and decodes its slot id one tile ahead, and
+//               publishes its copies itself (cp.async group wait, proxy
+//               fence, mbarrier arrive, a few groups behind the issue);
+//   warps 12-13 TMEM allocation (12); warp 12 + j issues every tcgen05.mma of
+//               Q tile j: S_j(t) into one of two S buffers, two tiles ahead
+//               of O_j += P_j(t)·V(t), so the softmax of tile t+1 never
+//               waits for the MMAs of tile t. P(t) aliases its S buffer in
+//               TMEM: the MMAs of one thread execute in issue order, so
+//               S(t+2) overwrites P(t) only after P(t)·V(t) read it. Warps
+//               14-15 only give their registers away.
 #include <cuda_bf16.h>
 
 #include <algorithm>
@@ -73,12 +77,13 @@ struct PrefillArgs {
     float4* part_o;           // [2 * grid][D / 4][256] unnormalised O of cut units
     float2* part_ml;          // [2 * grid][256] (m, l) of cut units
     int* tickets;             // [n_kv * n_qp], zero between launches
-    unsigned long long* trace;  // PRISM_K4_TRACE: [5][1024] globaltimer stamps of CTA 0, else null
+    unsigned long long* trace;  // PRISM_K4_TRACE: [8][1024] globaltimer stamps of CTA 0, else null
     unsigned* dbg;            // PRISM_K4_DEBUG: host-mapped progress words (CTA 0 only), else null
 };
 
 // timeline stamp (no-op unless PRISM_K4_TRACE): role 0 loader issued tile t,
-// 1 S0(t) issued, 2 P0(t)·V(t) issued, 3 warpgroup 0 has S0(t), 4 it posted P0(t)
+// 1 S(t) issued (both Q tiles), 2 / 7 P0(t)·V(t) / P1(t)·V(t) issued,
+// 3 / 5 warpgroup 0 / 1 has S(t), 4 / 6 it posted P(t)
 __device__ __forceinline__ void k4_stamp(unsigned long long* tr, int role, int t) {
     if (tr && blockIdx.x == 0 && t < 1024) {
         unsigned long long ns;
@@ -122,6 +127,9 @@ struct PfShape {
 static_assert(PfShape<128>::kSmem <= 232448, "K4 shared memory");
 
 // ---------------------------------------------------------------- PTX helpers
+// High word of every shared-memory matrix descriptor used here: SBO 1024 B
+// (8-row groups), descriptor version 1 (sm_100), SWIZZLE_128B.
+constexpr std::uint32_t kDescHi = (1024u >> 4) | (1u << 14) | (2u << 29);
 __device__ __forceinline__ std::uint32_t saddr(const void* p) {
     return static_cast<std::uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -193,6 +201,70 @@ __device__ __forceinline__ void tc_mma_ts_e(std::uint32_t d_tmem, std::uint32_t 
         "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
         " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
         "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// One tile's MMAs from one asm statement (the operands reach the uniform
+// datapath once; per-MMA descriptors are 64-bit adds of the low word inside):
+// S_j = Q_j · K(k)ᵀ over head_dim in K=16 steps (+32 B inside a 128-byte
+// atom, next atom 128 Q rows / 64 K rows further), fresh accumulator.
+template <int D>
+__device__ __forceinline__ void tc_mma_s_tile(std::uint32_t d_tmem, std::uint64_t dq, std::uint64_t dk,
+                                              std::uint32_t idesc) {
+    static_assert(D == 64 || D == 128, "head_dim");
+    if constexpr (D == 128) {
+        asm volatile(
+        "{\n .reg .pred e, f, t;\n .reg .b64 a, b;\n setp.ne.b32 t, 1, 0;\n setp.ne.b32 f, 1, 1;\n elect.sync _|e, 0xffffffff;\n"
+        " add.s64 a, %1, 0;\n add.s64 b, %2, 0;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, f;\n"
+        " add.s64 a, %1, 2;\n add.s64 b, %2, 2;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        " add.s64 a, %1, 4;\n add.s64 b, %2, 4;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        " add.s64 a, %1, 6;\n add.s64 b, %2, 6;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        " add.s64 a, %1, 1024;\n add.s64 b, %2, 512;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        " add.s64 a, %1, 1026;\n add.s64 b, %2, 514;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        " add.s64 a, %1, 1028;\n add.s64 b, %2, 516;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        " add.s64 a, %1, 1030;\n add.s64 b, %2, 518;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "}\n"
+        ::"r"(d_tmem), "l"(dq), "l"(dk), "r"(idesc)
+        : "memory");
+    } else {
+        asm volatile(
+        "{\n .reg .pred e, f, t;\n .reg .b64 a, b;\n setp.ne.b32 t, 1, 0;\n setp.ne.b32 f, 1, 1;\n elect.sync _|e, 0xffffffff;\n"
+        " add.s64 a, %1, 0;\n add.s64 b, %2, 0;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, f;\n"
+        " add.s64 a, %1, 2;\n add.s64 b, %2, 2;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        " add.s64 a, %1, 4;\n add.s64 b, %2, 4;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        " add.s64 a, %1, 6;\n add.s64 b, %2, 6;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, t;\n"
+        "}\n"
+        ::"r"(d_tmem), "l"(dq), "l"(dk), "r"(idesc)
+        : "memory");
+    }
+}
+// O_j (+)= P_j · V(k) over the tile's 64 keys in K=16 steps: P from TMEM (+8
+// columns per step), V MN-major (+16 rows = 2048 B per step).
+__device__ __forceinline__ void tc_mma_pv_tile(std::uint32_t d_tmem, std::uint32_t p_tmem, std::uint64_t dv,
+                                               std::uint32_t idesc, std::uint32_t accumulate) {
+    asm volatile(
+        "{\n .reg .pred e, p, t;\n .reg .b64 b;\n .reg .b32 a;\n setp.ne.b32 t, 1, 0;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
+        " add.s32 a, %1, 0;\n add.s64 b, %2, 0;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, p;\n"
+        " add.s32 a, %1, 8;\n add.s64 b, %2, 128;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n"
+        " add.s32 a, %1, 16;\n add.s64 b, %2, 256;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n"
+        " add.s32 a, %1, 24;\n add.s64 b, %2, 384;\n"
+        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [a], b, %3, t;\n"
+        "}\n"
+        ::"r"(d_tmem), "r"(p_tmem), "l"(dv), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 // 32 consecutive fp32 columns of this thread's TMEM lane
@@ -289,16 +361,15 @@ __device__ __forceinline__ std::uint64_t sw128_desc(std::uint32_t addr, std::uin
     d |= static_cast<std::uint64_t>(2) << 61;  // SWIZZLE_128B
     return d;
 }
-// The same descriptor split in two words: the low word (start address >> 4,
-// LBO >> 4) varies per operand tile and K step and never carries into the
-// high word (shared addresses < 256 KB), the high word (SBO 1024 B, version,
-// SWIZZLE_128B) is a constant. Offsets are added to the low word as >> 4.
+// The low word of that descriptor (start address >> 4, LBO >> 4): it varies
+// per operand tile and K step and never carries into the high word (shared
+// addresses < 256 KB), which is the constant kDescHi. Offsets are added to the
+// low word as >> 4.
 __device__ __forceinline__ std::uint32_t desc_lo(std::uint32_t addr, std::uint32_t lbo_bytes) {
     return ((addr >> 4) & 0x3fffu) | (((lbo_bytes >> 4) & 0x3fffu) << 16);
 }
 __device__ __forceinline__ std::uint64_t desc_of(std::uint32_t lo) {
-    constexpr std::uint32_t kHi = (1024u >> 4) | (1u << 14) | (2u << 29);
-    return (static_cast<std::uint64_t>(kHi) << 32) | lo;
+    return (static_cast<std::uint64_t>(kDescHi) << 32) | lo;
 }
 // Instruction descriptor, kind::f16: bf16 A/B, fp32 D, M x N, K-major A,
 // B K-major (b_mn = 0) or MN-major (b_mn = 1).
@@ -365,10 +436,10 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
 
     if (tid == 0) {
         mb_init(b_qfull, S::kLoaders);
-        mb_init(b_qempty, 1);
+        mb_init(b_qempty, 2);  // one commit per MMA issuer
         for (int s = 0; s < S::kHalves; ++s) {
             mb_init(b_kvfull + 8 * s, S::kLoaders);
-            mb_init(b_kvempty + 8 * s, 1);
+            mb_init(b_kvempty + 8 * s, 2);
         }
         for (int j = 0; j < 4; ++j) {
             mb_init(b_sfull + 8 * j, 1);
@@ -434,13 +505,36 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
             const std::uint32_t slot = sid - page * a.g.tpp;
             return static_cast<std::uint64_t>(page) * a.g.page_bytes + static_cast<std::uint64_t>(slot) * (D * 2);
         };
+        // The loaders make their own copies visible to the tensor core: each
+        // ring half is one cp.async group; kLag groups after issuing it, a
+        // thread waits for it, fences the generic -> async proxy and arrives
+        // on the half's full barrier (and on q_full for the group that also
+        // carried the unit's Q pair), so the MMA warps only wait on barriers.
+        constexpr int kLag = 4;
+        static_assert(kLag + 4 < S::kHalves, "MMA progress must not need a half held back by the lag");
+        int pend = 0, last_idx = -1;
+        unsigned qbits = 0;  // bit i: the group of half last_idx - i carried Q
+        auto arrive_half = [&](int hidx, bool q) {
+            if (q) mb_arrive(b_qfull);
+            mb_arrive(b_kvfull + 8 * half_slot(hidx));
+        };
+        auto flush = [&]() {
+            cp_async_wait<0>();
+            fence_proxy_async();
+            for (int i = pend - 1; i >= 0; --i) arrive_half(last_idx - i, (qbits >> i) & 1u);
+            pend = 0;
+        };
         Seg la = seg_at(a, g_begin, g_end);  // look-ahead cursor (tile g + 1)
         std::uint64_t oa = decode(load_sid(g_begin - la.ustart));
         int g = g_begin, s_idx = 0;
         while (g < g_end) {
             const Seg sg = seg_at(a, g, g_end);
-            // Q pair of the unit: rows of tile j = token (r / G) x head (r % G), padding rows zero
-            if (s_idx > 0) mb_wait(b_qempty, (s_idx - 1) & 1);
+            // Q pair of the unit: rows of tile j = token (r / G) x head (r % G),
+            // padding rows zero; committed with the segment's first K half
+            if (s_idx > 0) {
+                flush();  // the MMA warps need every issued half to release Q
+                mb_wait(b_qempty, (s_idx - 1) & 1);
+            }
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 const int r = ra + 64 * m, j = r >> 7, rr = r & 127;
@@ -450,7 +544,6 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                     a.q + (static_cast<std::size_t>(ok ? tok : 0) * n_q + static_cast<std::size_t>(sg.h) * G + rr % G) * D);
                 copy_row(sQ + j * S::kQB + rr * 128, dsw_q, src, ok);
             }
-            cp_async_arrive(b_qfull);
             const std::uint64_t kb = static_cast<std::uint64_t>(a.layer * 2 * n_kv + sg.h) * a.g.tpp * (D * 2);
             for (; g < sg.g1; ++g) {
                 const int k = g - g_begin;
@@ -465,29 +558,41 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                     const int hs = half_slot(idx);
                     if (idx >= S::kHalves) mb_wait(b_kvempty + 8 * hs, half_phase(idx) ^ 1u);
                     copy_row(sKV + hs * S::kHalfB + ra * 128, dsw_kv, base + kb + (kv ? v_delta : 0) + oa, oa != ~0ull);
-                    cp_async_arrive(b_kvfull + 8 * hs);
+                    cp_async_commit();
+                    last_idx = idx;
+                    qbits = (qbits << 1) | ((kv == 0 && g == sg.g0) ? 1u : 0u);
+                    if (++pend > kLag) {
+                        cp_async_wait<kLag>();
+                        fence_proxy_async();
+                        arrive_half(idx - kLag, (qbits >> kLag) & 1u);
+                        --pend;
+                    }
                 }
                 if (lane == 0 && w == 0) k4_stamp(a.trace, 0, k);
                 oa = decode(na);
             }
             ++s_idx;
         }
+        flush();
     } else if (warp >= 12) {
         // ------------------------------------------------------------ MMA issue (warp 12)
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(S::kRegsLoad));
-        // the whole warp runs the issue loop (uniform control flow and operands
-        // in uniform registers); one elected lane issues each tcgen05 op
-        if (warp == 12) {
+        // Warp 12 + j issues every MMA of Q tile j (the two Q tiles' pipelines
+        // share only the K/V ring, whose slots are released by one commit of
+        // each issuer). The whole warp runs the issue loop (uniform control
+        // flow); one elected lane issues each tcgen05 op.
+        if (warp < 14) {
+            const int j = warp - 12;
             constexpr std::uint32_t idesc_s = f16_idesc(S::kM, S::kN, 0);
             constexpr std::uint32_t idesc_o = f16_idesc(S::kM, D, 1);
             const int n = g_end - g_begin;
             auto wait_half = [&](int idx) {
-                mb_wait(b_kvfull + 8 * half_slot(idx), half_phase(idx));
-                fence_proxy_async();  // cp.async (generic proxy) data -> tcgen05.mma (async proxy)
+                mb_wait(b_kvfull + 8 * half_slot(idx), half_phase(idx));  // the loaders fenced the proxy
                 tc_fence_after();
             };
-            // S_j(k) = Q_j · K(k)ᵀ into S buffer (j, k & 1), for both Q tiles;
-            // runs two tiles ahead of the P·V MMAs
+            const std::uint32_t dq = desc_lo(sQ + j * S::kQB, 16);
+            const std::uint32_t s_col = tmem + j * 2 * S::kN, o_col = tmem + S::kColO + j * D;
+            // S_j(k) = Q_j · K(k)ᵀ into S buffer (j, k & 1): two tiles ahead of P_j·V
             Seg sc = seg_at(a, g_begin, g_end);
             int sc_idx = 0;
             auto issue_s = [&](int k) {
@@ -496,28 +601,17 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                     sc = seg_at(a, g, g_end);
                     ++sc_idx;
                 }
-                if (g == sc.g0) {
-                    mb_wait(b_qfull, sc_idx & 1);
-                    fence_proxy_async();
-                }
+                if (g == sc.g0) mb_wait(b_qfull, sc_idx & 1);
+                if (j == 0 && lane == 0) k4_stamp(a.trace, 11, k);
                 wait_half(2 * k);
+                if (j == 0 && lane == 0) k4_stamp(a.trace, 12, k);
                 const std::uint32_t dk = desc_lo(sKV + half_slot(2 * k) * S::kHalfB, 16);
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    const std::uint32_t dq = desc_lo(sQ + j * S::kQB, 16);
-#pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        // +16 B >> 4 per K=16 step inside a 128-byte atom, next atom 128 rows on
-                        const std::uint32_t offq = ((kk >> 2) * (S::kM * 128) + (kk & 3) * 32) >> 4;
-                        const std::uint32_t offk = ((kk >> 2) * (S::kN * 128) + (kk & 3) * 32) >> 4;
-                        tc_mma_e(tmem + j * 2 * S::kN + (k & 1) * S::kN, desc_of(dq + offq), desc_of(dk + offk), idesc_s,
-                               kk > 0);
-                    }
-                    tc_commit_e(b_sfull + 8 * (2 * j + (k & 1)));
-                }
+                static_assert(S::kM * 128 / 16 == 1024 && S::kN * 128 / 16 == 512, "descriptor steps in tc_mma_s_tile");
+                tc_mma_s_tile<D>(s_col + (k & 1) * S::kN, desc_of(dq), desc_of(dk), idesc_s);
+                tc_commit_e(b_sfull + 8 * (2 * j + (k & 1)));
                 tc_commit_e(b_kvempty + 8 * half_slot(2 * k));
                 if (g + 1 == sc.g1) tc_commit_e(b_qempty);  // last S of the segment: Q may be replaced
-                if (lane == 0) k4_stamp(a.trace, 1, k);
+                if (j == 0 && lane == 0) k4_stamp(a.trace, 1, k);
             };
             issue_s(0);
             if (n > 1) issue_s(1);
@@ -530,23 +624,19 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                     ++pc_idx;
                 }
                 const bool fresh = g == pc.g0;
+                // O_j (+)= P_j(k) · V(k), P_j in S buffer (j, k & 1)
+                if (j == 0 && lane == 0) k4_stamp(a.trace, 8, k);
+                mb_wait(b_pfull + 8 * (2 * j + (k & 1)), (k >> 1) & 1);
+                if (fresh && pc_idx > 0) mb_wait(b_ofree + 8 * j, (pc_idx - 1) & 1);
+                if (j == 0 && lane == 0) k4_stamp(a.trace, 9, k);
                 wait_half(2 * k + 1);
+                if (j == 0 && lane == 0) k4_stamp(a.trace, 10, k);
                 const std::uint32_t dv = desc_lo(sKV + half_slot(2 * k + 1) * S::kHalfB, S::kN * 128);
-#pragma unroll
-                for (int j = 0; j < 2; ++j) {
-                    // O_j (+)= P_j(k) · V(k), P_j in S buffer (j, k & 1)
-                    mb_wait(b_pfull + 8 * (2 * j + (k & 1)), (k >> 1) & 1);
-                    if (fresh && pc_idx > 0) mb_wait(b_ofree + 8 * j, (pc_idx - 1) & 1);
-                    tc_fence_after();
-#pragma unroll
-                    for (int kk = 0; kk < S::kN / 16; ++kk) {
-                        tc_mma_ts_e(tmem + S::kColO + j * D, tmem + j * 2 * S::kN + (k & 1) * S::kN + kk * 8,
-                                  desc_of(dv + kk * (2048 >> 4)), idesc_o, (!fresh || kk > 0) ? 1u : 0u);
-                    }
-                    tc_commit_e(b_pvdone + 8 * (2 * j + (k & 1)));
-                    if (j == 0 && lane == 0) k4_stamp(a.trace, 2, k);
-                }
+                static_assert(S::kN == 64, "four K=16 steps in tc_mma_pv_tile");
+                tc_mma_pv_tile(o_col, s_col + (k & 1) * S::kN, desc_of(dv), idesc_o, fresh ? 0u : 1u);
+                tc_commit_e(b_pvdone + 8 * (2 * j + (k & 1)));
                 tc_commit_e(b_kvempty + 8 * half_slot(2 * k + 1));
+                if (lane == 0) k4_stamp(a.trace, j == 0 ? 2 : 7, k);
                 if (k + 2 < n) issue_s(k + 2);
             }
         }
@@ -581,7 +671,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 const int b = k & 1;
                 mb_wait(b_sfull + 8 * (2 * j + b), (k >> 1) & 1);
                 tc_fence_after();
-                if (j == 0 && r == 0) k4_stamp(a.trace, 3, k);
+                if (r == 0) k4_stamp(a.trace, j == 0 ? 3 : 5, k);
                 const std::uint32_t tS = tmem + lane_base + j * 2 * S::kN + b * S::kN;
                 const int k0 = (g - sg.ustart) * S::kN;
                 // the tile's S row in registers (one tcgen05.ld wait), row max
@@ -631,23 +721,28 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 }
                 // p = exp2(s - m) (masked s = -inf -> 0), row sum, bf16 P over
                 // the buffer's first columns (the S row is already in registers)
-                float ls[8];
+                // packed fp32x2 arithmetic (FFMA2 / FADD2) around the MUFU ex2
+                // (a polynomial exp2 on the FMA pipe for part of the pairs was
+                // measured: no gain, the MMA issue path bounds the tile rate)
+                const float2 sc2 = make_float2(a.scale_log2, a.scale_log2), nm2 = make_float2(-m_use, -m_use);
+                float2 ls[4];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) ls[q] = 0.f;
+                for (int q = 0; q < 4; ++q) ls[q] = make_float2(0.f, 0.f);
                 std::uint32_t pk[S::kN / 2];
 #pragma unroll
-                for (int q = 0; q < S::kN; q += 2) {
-                    const float p0 = fast_exp2(fmaf(v[q], a.scale_log2, -m_use));
-                    const float p1 = fast_exp2(fmaf(v[q + 1], a.scale_log2, -m_use));
-                    ls[(q >> 1) & 7] += p0 + p1;
-                    pk[q >> 1] = pack_bf16(p0, p1);
+                for (int i = 0; i < S::kN / 2; ++i) {
+                    const float2 x = __ffma2_rn(make_float2(v[2 * i], v[2 * i + 1]), sc2, nm2);
+                    const float2 pr = make_float2(fast_exp2(x.x), fast_exp2(x.y));
+                    ls[i & 3] = __fadd2_rn(ls[i & 3], pr);
+                    pk[i] = pack_bf16(pr.x, pr.y);
                 }
                 tc_st32_nowait(tS, pk);
                 asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-                l_run += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+                const float2 l2 = __fadd2_rn(__fadd2_rn(ls[0], ls[1]), __fadd2_rn(ls[2], ls[3]));
+                l_run += l2.x + l2.y;
                 tc_fence_before();
                 mb_arrive(b_pfull + 8 * (2 * j + b));
-                if (j == 0 && r == 0) k4_stamp(a.trace, 4, k);
+                if (r == 0) k4_stamp(a.trace, j == 0 ? 4 : 6, k);
             }
             // ---- epilogue of the unit segment: O_j complete after PV_j(last)
             wait_pv(k - 1);
@@ -804,8 +899,8 @@ static unsigned long long* k4_trace_buf() {
     static unsigned long long* dev = [] {
         if (!std::getenv("PRISM_K4_TRACE")) return static_cast<unsigned long long*>(nullptr);
         unsigned long long* p = nullptr;
-        PRISM_CUDA(cudaMalloc(&p, 5 * 1024 * sizeof(unsigned long long)));
-        PRISM_CUDA(cudaMemset(p, 0, 5 * 1024 * sizeof(unsigned long long)));
+        PRISM_CUDA(cudaMalloc(&p, 16 * 1024 * sizeof(unsigned long long)));
+        PRISM_CUDA(cudaMemset(p, 0, 16 * 1024 * sizeof(unsigned long long)));
         return p;
     }();
     return dev;
@@ -815,7 +910,7 @@ static unsigned long long* k4_trace_buf() {
 int k4_trace_read(unsigned long long* out, int n) {
     unsigned long long* d = k4_trace_buf();
     if (!d) return 0;
-    const int m = n < 5 * 1024 ? n : 5 * 1024;
+    const int m = n < 16 * 1024 ? n : 16 * 1024;
     PRISM_CUDA(cudaDeviceSynchronize());
     PRISM_CUDA(cudaMemcpy(out, d, m * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
     return m;

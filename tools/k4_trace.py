@@ -38,19 +38,27 @@ while True:
 for _ in range(3):
     eng.prefill_attention(0, q.data_ptr(), o.data_ptr(), 1 / math.sqrt(128))
 eng.synchronize()
-buf = (C.c_uint64 * (5 * 1024))()
+R = 13
+SHOW = [int(x) for x in os.environ.get('SHOW', '').split(',') if x]
+buf = (C.c_uint64 * (R * 1024))()
 got = C.c_int32()
-lib.call("prism_debug_k4_trace", buf, 5 * 1024, C.byref(got))
-tr = [list(buf[r * 1024:(r + 1) * 1024]) for r in range(5)]
+lib.call("prism_debug_k4_trace", buf, R * 1024, C.byref(got))
+tr = [list(buf[r * 1024:(r + 1) * 1024]) for r in range(R)]
 n_tiles = max(i for i in range(1024) if tr[1][i]) + 1
 t0 = min(x for row in tr for x in row[:n_tiles] if x)
-print("tile  load   S_iss  PV_iss  sm_S   sm_P   (us from first stamp)")
+names = ["load", "S_iss", "PV0_is", "w0_S", "w0_P", "w1_S", "w1_P", "PV1_is", "m_it", "m_P", "m_V", "s_beg", "s_K"]
+print("tile " + " ".join(f"{n:>7s}" for n in names) + "   (us from first stamp)")
 for t in range(n_tiles):
-    row = [(tr[r][t] - t0) / 1e3 if tr[r][t] else float("nan") for r in range(5)]
-    if t < 12 or t % 8 == 0 or t == n_tiles - 1:
-        print(f"{t:4d} " + " ".join(f"{x:6.2f}" for x in row))
+    row = [(tr[r][t] - t0) / 1e3 if tr[r][t] else float("nan") for r in range(R)]
+    if t < 12 or t % 8 == 0 or t == n_tiles - 1 or (SHOW and SHOW[0] <= t < SHOW[1]):
+        print(f"{t:4d} " + " ".join(f"{x:7.2f}" for x in row))
+mean = lambda xs: sum(xs) / max(len(xs), 1)
 d = [(tr[2][t + 1] - tr[2][t]) / 1e3 for t in range(n_tiles - 1)]
-sm = [(tr[4][t] - tr[3][t]) / 1e3 for t in range(n_tiles)]
-wait = [(tr[3][t + 1] - tr[4][t]) / 1e3 for t in range(n_tiles - 1)]
-print(f"tiles {n_tiles}; mean PV-to-PV {sum(d) / len(d):.3f} us; softmax busy per tile {sum(sm) / len(sm):.3f} us; "
-      f"softmax idle between tiles {sum(wait) / len(wait):.3f} us")
+for w, (rs, rp) in enumerate(((3, 4), (5, 6))):
+    sm = [(tr[rp][t] - tr[rs][t]) / 1e3 for t in range(n_tiles)]
+    wait = [(tr[rs][t + 1] - tr[rp][t]) / 1e3 for t in range(n_tiles - 1)]
+    print(f"warpgroup {w}: softmax busy per tile {mean(sm):.3f} us, idle between tiles {mean(wait):.3f} us")
+p2pv = [(tr[2][t] - tr[4][t]) / 1e3 for t in range(n_tiles)]
+s_lat = [(tr[3][t] - tr[1][t]) / 1e3 for t in range(n_tiles)]
+print(f"tiles {n_tiles}; mean PV-to-PV {mean(d):.3f} us; P0 posted -> PV0 issued {mean(p2pv):.3f} us; "
+      f"S issued -> warpgroup 0 has it {mean(s_lat):.3f} us")
