@@ -19,6 +19,9 @@ from ctypes import c_uint64, c_void_p
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 PRODUCT_LIB = os.path.join(PKG_DIR, "libprism_b200.so")
+# A/B timing of two builds on one box (tools only): PRISM_PRODUCT_LIB names
+# another build of the same sources; unset, the in-tree product is loaded.
+PRODUCT_LIB = os.environ.get("PRISM_PRODUCT_LIB", PRODUCT_LIB)
 
 PRISM_OK = 0
 STATUS_NAMES = {0: "OK", 1: "USAGE", 2: "PARSE", 3: "CONFIG", 4: "PLACEMENT", 5: "CUDA", 6: "ARG", 7: "INTERNAL"}

@@ -47,6 +47,7 @@ struct SkShape {
 struct SkArgs {
     AttnArgs a;                       // geometry, q/out, table, desc, scale
     const std::int32_t* pair_tiles;   // [n_pairs + 1] prefix of tiles per pair
+    const std::int32_t* range_pair;   // [grid] first pair of each CTA range (host-computed)
     int n_pairs;
     int total_tiles;
     int per_cta;                      // W
@@ -104,16 +105,9 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
     if (g_begin >= g_end) return;
     k3_stamp(sk.trace, 0);  // CTA running
 
-    // first pair of the range: largest p with T[p] <= g_begin
-    auto pair_of = [&](int g) {
-        int lo = 0, hi = sk.n_pairs;
-        while (hi - lo > 1) {
-            const int mid = (lo + hi) >> 1;
-            if (__ldg(T + mid) <= g) lo = mid;
-            else hi = mid;
-        }
-        return lo;
-    };
+    // first pair of the range (host-computed once per step: one load instead
+    // of a binary search over the pair-tile prefix)
+    const int pair0 = __ldg(sk.range_pair + range);
 
     // ---------------- prefetch cursor: the row offsets of the next tile to
     // issue are decoded one tile ahead of its cp.async, crossing pair
@@ -130,7 +124,7 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
     // before it is decoded into a row offset (load_sid / decode_row), and the
     // end tile + descriptor of the pair after the cursor's are loaded when the
     // cursor enters a pair (crossing a boundary then needs no load).
-    int pf = pair_of(g_begin);
+    int pf = pair0;
     int pf_first = __ldg(T + pf), pf_end = __ldg(T + pf + 1);
     int pf_ctx = a.desc[pf / n_kv].ctx;
     std::int64_t pf_row = a.desc[pf / n_kv].row;
@@ -199,7 +193,7 @@ __global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
     };
 
     // ---------------- consumer state
-    int cp = pair_of(g_begin);  // pair being computed
+    int cp = pair0;  // pair being computed
     int cp_first = __ldg(T + cp), cp_end = __ldg(T + cp + 1);
     int ctx = 0;
     std::uint32_t qb[S::kKSteps][2];
@@ -600,6 +594,14 @@ void launch_k3_streamk_t(Ctx& d, AttnArgs a, int n_dec) {
         const int per_sm = std::min(per_sm_cap, d.head_dim == 128 ? occupancy_sk_d<128>(d.group) : occupancy_sk_d<64>(d.group));
         const int slots = sms * per_sm;
         d.sk_per_cta = std::max(1, (d.sk_total + slots - 1) / slots);
+        // the first pair of every CTA range
+        const int grid = (d.sk_total + d.sk_per_cta - 1) / d.sk_per_cta;
+        d.sk_range_pair.ensure(static_cast<std::size_t>(grid));
+        for (int c = 0, p = 0; c < grid; ++c) {
+            while (p + 1 < n_pairs && d.sk_prefix.host[p + 1] <= c * d.sk_per_cta) ++p;
+            d.sk_range_pair.host[c] = p;
+        }
+        d.sk_range_pair.upload(static_cast<std::size_t>(grid), d.stream);
         // partial slots per pair: CTAs a pair's tile range can touch
         int max_tiles = 0;
         for (int b = 0; b < n_dec; ++b) max_tiles = std::max(max_tiles, (d.decode_desc.host[b].ctx + kT - 1) / kT);
@@ -623,6 +625,7 @@ void launch_k3_streamk_t(Ctx& d, AttnArgs a, int n_dec) {
     ++launch_no;
     s.a = a;
     s.pair_tiles = d.sk_prefix.dev;
+    s.range_pair = d.sk_range_pair.dev;
     s.n_pairs = n_pairs;
     s.total_tiles = d.sk_total;
     s.per_cta = d.sk_per_cta;

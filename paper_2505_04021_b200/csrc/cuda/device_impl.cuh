@@ -100,6 +100,7 @@ struct DecodeDesc {
     std::uint64_t request;
 };
 
+
 class EngineDeviceImpl final : public EngineDevice {
 public:
     EngineDeviceImpl(msim::engine::Engine& eng, msim::pagealloc::PhysicalLedger& ledger,
@@ -152,6 +153,7 @@ public:
     std::uint64_t step_serial = 0;
     std::uint64_t sk_step = ~0ull;
     Staging<std::int32_t> sk_prefix;
+    Staging<std::int32_t> sk_range_pair;  // first pair of each stream-K CTA range
     int sk_total = 0, sk_per_cta = 1, sk_max_parts = 1;
     std::uint64_t sk_launches = 0;  // selects the CTA range counter (alternate launches)
     // true while the last operation this engine put on `stream` is a
@@ -205,6 +207,7 @@ struct PagedCtx final : PagedOp {
     Staging<DecodeDesc> decode_desc;
     Staging<TokenMeta> token_meta;  // all live (K2 skips dead tokens only in engine steps)
     Staging<std::int32_t> sk_prefix;
+    Staging<std::int32_t> sk_range_pair;  // first pair of each stream-K CTA range
     std::uint64_t step_serial = 0, sk_step = ~0ull;
     int sk_total = 0, sk_per_cta = 1, sk_max_parts = 1;
     std::uint64_t sk_launches = 0;  // selects the CTA range counter (alternate launches)

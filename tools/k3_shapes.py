@@ -5,6 +5,7 @@ import json
 import math
 import os
 import sys
+import time
 
 import torch
 
@@ -44,14 +45,17 @@ for name, (L, nq, nkv, d, _) in SHAPES.items():
     dev.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
+    t0 = time.perf_counter()
     for _ in range(3):
         for layer in range(L):
             eng.decode_attention(layer, q[layer].data_ptr(), o[layer].data_ptr(), sc)
+    host_us = (time.perf_counter() - t0) * 1e6 / (3 * L)  # host submission time per launch
     e.record()
     e.synchronize()
     ms = s.elapsed_time(e) / (3 * L)
     ctx = sum(r.live_slots() for r in eng.batch())
     nbytes = ctx * nkv * d * 4 + 2 * B * nq * d * 2
     print(json.dumps({"shape": name, "G": nq // nkv, "d": d, "n_kv": nkv, "ms": round(ms, 4),
-                      "GBps": round(nbytes / ms / 1e6, 1), "frac": round(nbytes / ms / 1e6 / peak, 4)}), flush=True)
+                      "GBps": round(nbytes / ms / 1e6, 1), "frac": round(nbytes / ms / 1e6 / peak, 4),
+                      "host_submit_us_per_launch": round(host_us, 2)}), flush=True)
     del eng, gpu
