@@ -303,13 +303,13 @@ def gpu_arm(args, rank, world):
     torch.cuda.set_device(int(os.environ.get("PRISM_BENCH_DEVICE", os.environ.get("LOCAL_RANK", 0))))
     steps, warm = args.steps, args.warmup
     mids = placement_for(world, rank)
-    dev, gpu, models = setup_gpu(rank, mids, steps * 2 + warm * 2 + 8)
+    dev, gpu, models = setup_gpu(rank, mids, steps * (1 + E2E_RUNS) + warm * (1 + E2E_RUNS) + 8)
     # startup reservation (as in page_churn_c2): physical handles for the KV
     # the warm-up, timed and e2e decode steps will append, plus each pool's
     # look-ahead window, so maps while serving are cuMemMap + cuMemSetAccess
     # only (no cuMemCreate behind them)
     tpp = (2 << 20) // (2 * L * NKV * D * 2)
-    dev.reserve(len(models) * (B_PER_MODEL * (2 * steps + 2 * warm + 8) // tpp + 2 * 256))
+    dev.reserve(len(models) * (B_PER_MODEL * ((1 + E2E_RUNS) * (steps + warm) + 8) // tpp + 2 * 256))
     dev.quiesce()
     stream = torch.cuda.ExternalStream(dev.stream())
     q_bufs, out_bufs = [], []
@@ -375,8 +375,14 @@ def gpu_arm(args, rank, world):
         tokens = int(n.item())
     value = tokens / (ms_max / 1e3)
 
-    # ---- e2e through the C-ABI with host buffers
-    e2e = e2e_arm(models, steps, warm, scale, dev, world)
+    # ---- e2e through the C-ABI with host buffers: E2E_RUNS passes, the
+    # median reported with every pass beside it (the VMM driver calls behind
+    # the decode growth vary ~10x run to run on one box)
+    passes = [e2e_arm(models, steps, warm, scale, dev, world) for _ in range(E2E_RUNS)]
+    order = sorted(range(len(passes)), key=lambda i: passes[i]["value"])
+    e2e = dict(passes[order[len(order) // 2]])
+    e2e["runs"] = [p["value"] for p in passes]
+    e2e["reported"] = f"median of {len(passes)} passes of {steps} steps (after {warm} warm-up steps each)"
 
     peak, peak_kind = measured_peaks()
     # per-launch algorithmic bytes (contexts grow by 1 per step; use the mean)
@@ -480,6 +486,8 @@ def e2e_arm(models, steps, warm, scale, dev, world):
                     "worker_ms": round(st["background_ns_total"] / 1e6, 3), "premaps": st["premaps"]}}
 
 
+E2E_RUNS = 3  # end-to-end passes (median reported)
+
 C2_SHAPES = {  # L, n_q, n_kv, d, weight GB
     "qwen2.5-0.5b": (24, 14, 2, 64, 0.99), "llama3.2-1b": (16, 32, 8, 64, 2.47),
     "qwen2.5-1.5b": (28, 12, 2, 128, 3.09), "qwen2.5-3b": (36, 16, 2, 128, 6.17),
@@ -488,19 +496,22 @@ C2_SHAPES = {  # L, n_q, n_kv, d, weight GB
 }
 
 
-def page_churn_c2(max_rounds=2500, kv_pages=6000, horizon_s=60.0):
+def page_churn_c2(max_rounds=2500, kv_pages=6000, horizon_s=60.0, chunk_pages=0, k3_layers=4):
     """BASELINE config 2 as a page map/unmap measurement: the 8 model shapes
     space-share one B200 ledger (weights accounted at their real size, KV
     budget `kv_pages`), bursty 10 s on / 10 s off arrivals in alternating
     phases (seeded Poisson, SURVEY Appendix A scenario 2), driven by the
     shared TraceDriver; every step runs K1 + K2 on the GPU, so every logical
-    map/unmap is real CUDA VMM work (park / revive / steal)."""
+    map/unmap is real CUDA VMM work (park / revive / steal), and K3 over
+    `k3_layers` layers of every engine that decodes, so the driver calls
+    compete with decode attention's HBM traffic. chunk_pages: logical 2 MiB
+    pages per physical VMM handle (0: the default 8 = 16 MiB)."""
     import torch
 
     from paper_2505_04021_b200 import msim
     from paper_2505_04021_b200.driver import TraceDriver
 
-    dev = msim.Device(torch.cuda.current_device())
+    dev = msim.Device(torch.cuda.current_device(), chunk_pages=chunk_pages)
     weight_pages = sum(math.ceil(s[4] * 1e9 / (2 << 20)) for s in C2_SHAPES.values())
     gpu = msim.GpuState(0, weight_pages + kv_pages)
     gpu.ledger.attach_device(dev)
@@ -524,13 +535,40 @@ def page_churn_c2(max_rounds=2500, kv_pages=6000, horizon_s=60.0):
     dev.reserve(kv_pages)
     dev.quiesce()
     dev.reset_stats()
+    max_dec = 1024
+    qbuf = {n: torch.zeros((max_dec, C2_SHAPES[n][1], C2_SHAPES[n][3]), dtype=torch.bfloat16, device="cuda")
+            for n in C2_SHAPES}
+    obuf = {n: torch.empty_like(q) for n, q in qbuf.items()}
+    k3 = [0]
+    resid = {"physical_pages_max": 0, "excess_pages_max": 0}
+    steps = [0]
+
+    def on_step(mid, e, o):
+        e.append_kv_synthetic(0, layers_of[mid], SEED)
+        n_dec = e.step_info()[1]
+        if k3_layers and n_dec:
+            sc = 1.0 / math.sqrt(C2_SHAPES[mid][3])
+            for layer in range(min(k3_layers, layers_of[mid])):
+                e.decode_attention(layer, qbuf[mid].data_ptr(), obuf[mid].data_ptr(), sc)
+                k3[0] += 1
+        steps[0] += 1
+        if steps[0] % 250 == 0:  # physical residency vs the ledger's KV pages
+            sd = dev.stats()
+            phys = sd["total_chunks"] * sd["chunk_pages"]
+            logical = gpu.ledger.mapped_pages() + gpu.ledger.buffer_pages()
+            resid["physical_pages_max"] = max(resid["physical_pages_max"], phys)
+            resid["excess_pages_max"] = max(resid["excess_pages_max"], phys - logical)
+
     t0 = time.perf_counter()
-    drv = TraceDriver(engines, trace, on_step=lambda mid, e, o: e.append_kv_synthetic(0, layers_of[mid], SEED))
+    drv = TraceDriver(engines, trace, on_step=on_step)
     drv.run(max_rounds)
     dev.synchronize()
     wall = time.perf_counter() - t0
     st = dev.stats()
     res = page_map_summary(st, len(drv.outcomes))
+    res["k3_launches"] = k3[0]
+    res["residency"] = dict(resid, note="physical = chunks held x chunk_pages (incl. parked / cached); excess = "
+                                        "physical - the ledger's KV + buffer pages, sampled every 250 steps")
     res.update({"workload": f"C2: 8 shapes on one ledger ({weight_pages} weight + {kv_pages} KV pages; physical "
                             f"handles for the KV budget reserved at startup), bursty "
                             f"10s on/off, {len(drv.outcomes)} engine steps, {drv.next} arrivals",
@@ -542,13 +580,13 @@ def page_churn_c2(max_rounds=2500, kv_pages=6000, horizon_s=60.0):
     return res
 
 
-def page_churn_c2_median(reps=3):
+def page_churn_c2_median(reps=3, **kw):
     """page_churn_c2 `reps` times in this process (a fresh device, ledger and
     engines each time; identical seeded trace, so identical logical and driver
     call counts): the per-call cost of the CUDA VMM driver calls varies up to
     ~10x between runs on the same box (tools/vmm_churn_repeat.py), so the
     median run is reported, with every run's amortised figure beside it."""
-    runs = [page_churn_c2() for _ in range(reps)]
+    runs = [page_churn_c2(**kw) for _ in range(reps)]
     order = sorted(range(reps), key=lambda i: runs[i]["amortised_us_per_page_op"])
     res = dict(runs[order[reps // 2]])
     res["amortised_us_per_page_op_runs"] = [r["amortised_us_per_page_op"] for r in runs]
@@ -583,6 +621,13 @@ def page_map_summary(st, steps):
                 "cuMemCreate": round(st["create_ns_total"] / 1e3 / ops, 2),
                 "cuMemUnmap_steals": round(st["steal_ns_total"] / 1e3 / ops, 2)},
             "steals_of_premapped": st["caller_steals_clean"],
+            "driver_call_us": {  # raw per-call latency, worker thread, per physical chunk
+                "map_and_access_p50": round(st["drv_map_ns_p50"] / 1e3, 1),
+                "map_and_access_p99": round(st["drv_map_ns_p99"] / 1e3, 1),
+                "create_p50": round(st["drv_create_ns_p50"] / 1e3, 1),
+                "create_p99": round(st["drv_create_ns_p99"] / 1e3, 1),
+                "steal_unmap_p50": round(st["drv_unmap_ns_p50"] / 1e3, 1),
+                "steal_unmap_p99": round(st["drv_unmap_ns_p99"] / 1e3, 1)},
             "note": "amortised = engine-thread time in the VMM layer (incl. waits); background = worker-thread driver time"}
 
 
@@ -839,7 +884,16 @@ def serving_gpu():
                          "k4_launches": s["k4_launches"], "decode_tokens": s["decode_tokens"],
                          "prefill_tokens": s["prefill_tokens"], "activations": meas.summary["activations"],
                          "evictions": meas.summary["evictions"], "vmm_maps": s["vmm_maps"],
-                         "vmm_unmaps": s["vmm_unmaps"], "wall_s": round(wall_meas, 2)},
+                         "vmm_unmaps": s["vmm_unmaps"], "wall_s": round(wall_meas, 2),
+                         # page map/unmap cost while the scheduler runs K1/K2/K4/K3 on the same GPU
+                         "page_map": {
+                             "caller_us_per_page_op": round(
+                                 s["vmm_caller_ns"] / 1e3 / max(s["vmm_maps"] + s["vmm_unmaps"], 1), 2),
+                             "worker_us_per_page_op": round(
+                                 s["vmm_worker_ns"] / 1e3 / max(s["vmm_maps"] + s["vmm_unmaps"], 1), 2),
+                             "revived": s["vmm_revived"], "urgent_chunks": s["vmm_urgent"],
+                             "driver_creates": s["vmm_creates"], "driver_unmaps": s["vmm_driver_unmaps"],
+                             "steals": s["vmm_steals"]}},
         }
 
     out = {"note": "attainment = fraction of requests meeting both TTFT and TPOT SLOs at SLO scale k; "
@@ -1043,6 +1097,16 @@ def main():
                 res["page_map_c2"] = page_churn_c2_median()
             except Exception as e:
                 res["page_map_c2"] = {"error": str(e)}
+            try:  # physical chunk size trade-off: one handle per 2 MiB page vs per 8 pages
+                small = page_churn_c2(chunk_pages=1)
+                big = res.get("page_map_c2", {})
+                keys = ("amortised_us_per_page_op", "caller_wait_us_per_page_op", "background_us_per_page_op",
+                        "urgent_chunks", "driver_creates", "steals", "access_calls", "driver_call_us", "residency")
+                res["page_map_c2_chunk_tradeoff"] = {
+                    "chunk_2MiB": {k: small.get(k) for k in keys},
+                    "chunk_16MiB": {k: big.get(k) for k in keys}}
+            except Exception as e:
+                res["page_map_c2_chunk_tradeoff"] = {"error": str(e)}
         if world == 1 and not args.no_prefill:
             try:
                 res["decode_c3"] = decode_c3()

@@ -434,6 +434,9 @@ typedef struct {
     uint64_t urgent;            /* chunks the worker mapped on demand (not anticipated by the look-ahead) */
     uint64_t total_chunks;      /* physical chunks held (mapped, cached, in flight) */
     uint64_t chunk_pages;       /* logical pages per chunk */
+    /* raw driver-call latency per physical chunk (worker thread, bounded sample):
+     * cuMemMap + cuMemSetAccess, cuMemCreate, cuMemUnmap of a steal */
+    double drv_map_ns_p50, drv_map_ns_p99, drv_create_ns_p50, drv_create_ns_p99, drv_unmap_ns_p50, drv_unmap_ns_p99;
 } prism_device_stats;
 int prism_device_stats_get(const prism_device* d, prism_device_stats* out);
 int prism_device_reset_stats(prism_device* d);

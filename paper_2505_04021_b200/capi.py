@@ -197,7 +197,9 @@ class DeviceStats(C.Structure):
         ("access_calls", c_uint64), ("steals", c_uint64), ("steal_ns_total", c_double),
         ("background_ns_total", c_double)] + [(n, c_uint64) for n in ("premaps", "premapped_hits", "over_budget",
                                                                  "caller_steals_clean")] + [
-        ("wait_ns_total", c_double), ("urgent", c_uint64), ("total_chunks", c_uint64), ("chunk_pages", c_uint64)]
+        ("wait_ns_total", c_double), ("urgent", c_uint64), ("total_chunks", c_uint64), ("chunk_pages", c_uint64)] + [
+        (n, c_double) for n in ("drv_map_ns_p50", "drv_map_ns_p99", "drv_create_ns_p50", "drv_create_ns_p99",
+                                "drv_unmap_ns_p50", "drv_unmap_ns_p99")]
 
 
 class EngineDeviceOptions(C.Structure):

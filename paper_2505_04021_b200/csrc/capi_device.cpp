@@ -140,6 +140,12 @@ int prism_device_stats_get(const prism_device* d, prism_device_stats* out) {
         out->urgent = s.urgent;
         out->total_chunks = d->dev->total_handles();
         out->chunk_pages = d->dev->chunk_pages();
+        out->drv_map_ns_p50 = percentile(s.drv_map_ns, 0.5);
+        out->drv_map_ns_p99 = percentile(s.drv_map_ns, 0.99);
+        out->drv_create_ns_p50 = percentile(s.drv_create_ns, 0.5);
+        out->drv_create_ns_p99 = percentile(s.drv_create_ns, 0.99);
+        out->drv_unmap_ns_p50 = percentile(s.drv_unmap_ns, 0.5);
+        out->drv_unmap_ns_p99 = percentile(s.drv_unmap_ns, 0.99);
     });
 }
 

@@ -260,6 +260,7 @@ bool VmmDevice::take_handle(Lock& lk, bool urgent, std::uint64_t& h) {
         ++mapped_;
         ++stats_.creates;
         stats_.create_ns_total += ns;
+        sample(stats_.drv_create_ns, ns);
         trace('C', 1, tc, ns);
         return true;
     };
@@ -367,6 +368,7 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h, bool premap) {
             ++stats_.driver_unmaps;
             stats_.steals += static_cast<std::uint64_t>(n);
             stats_.steal_ns_total += ns;
+            sample(stats_.drv_unmap_ns, ns);
             trace('U', n, t0, ns);
             // the pick's handle goes to the caller (keeps its mapped_ count);
             // the others become cached, unmapped handles
@@ -438,6 +440,7 @@ bool VmmDevice::map_chunk(Lock& lk, std::uint64_t va, std::uint64_t h, bool urge
     c.inflight = false;
     stats_.map_call_ns_total += map_ns;
     stats_.access_ns_total += acc_ns;
+    sample(stats_.drv_map_ns, map_ns + acc_ns);
     if (acc_ns > 0.0) ++stats_.access_calls;
     trace(urgent ? 'M' : 'P', 1, tm, map_ns + acc_ns);
     if (r != CUDA_SUCCESS) {

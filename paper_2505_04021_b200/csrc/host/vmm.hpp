@@ -75,6 +75,9 @@ struct VmmStats {
     double wait_ns_total = 0.0;       // caller time waiting for the worker (inside map_ns_total)
     std::vector<float> map_ns;        // per logical map, caller thread (bounded)
     std::vector<float> unmap_ns;      // per logical unmap, caller thread (bounded)
+    std::vector<float> drv_map_ns;    // per chunk cuMemMap + cuMemSetAccess, worker thread (bounded)
+    std::vector<float> drv_create_ns; // per cuMemCreate (bounded)
+    std::vector<float> drv_unmap_ns;  // per cuMemUnmap of a steal (bounded)
     double create_ns_total = 0.0;     // inside cuMemCreate
     double map_call_ns_total = 0.0;   // inside cuMemMap
     double access_ns_total = 0.0;     // inside cuMemSetAccess
