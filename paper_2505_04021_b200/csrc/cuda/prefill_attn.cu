@@ -107,12 +107,12 @@ struct PfShape {
     static constexpr int kSub = D / 64;       // 64-element (128 B) swizzle atoms along head_dim
     static constexpr int kQB = kM * D * 2;    // one Q tile
     static constexpr int kHalfB = kN * D * 2;  // one K (or V) tile
-    static constexpr int kHalves = D == 128 ? 10 : 16;  // ring slots of K|V halves
-    static constexpr int kOffQ = 0;           // Q tiles 0 and 1
-    static constexpr int kOffKV = 2 * kQB;
+    static constexpr int kHalves = D == 128 ? 6 : 16;  // ring slots of K|V halves
+    static constexpr int kOffQ = 0;           // Q pair buffers 0 and 1 (tiles 0, 1 each)
+    static constexpr int kOffKV = 4 * kQB;
     static constexpr int kOffBar = kOffKV + kHalves * kHalfB;
-    // q_full | q_empty | kv_full[H] | kv_empty[H] | s_full[2][2] | p_full[2][2] | pv_done[2][2] | o_free[2]
-    static constexpr int kBars = 2 + 2 * kHalves + 14;
+    // q_full[2] | q_empty[2] | kv_full[H] | kv_empty[H] | s_full[2][2] | p_full[2][2] | pv_done[2][2] | o_free[2]
+    static constexpr int kBars = 4 + 2 * kHalves + 14;
     static constexpr int kOffMisc = kOffBar + kBars * 8;  // TMEM address, merge flag
     static constexpr int kSmem = kOffMisc + 16 + 1024;    // + alignment slack
     static constexpr int kThreads = 512;
@@ -428,15 +428,17 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
     const std::uint32_t bar = saddr(smem + S::kOffBar);
     // q_full | q_empty | kv_full[H] | kv_empty[H] | s_full[2][2] | p_full[2][2] | pv_done[2][2] | o_free[2]
     // ([j][b]: Q tile j, tile parity b)
-    const std::uint32_t b_qfull = bar, b_qempty = bar + 8, b_kvfull = bar + 16,
+    const std::uint32_t b_qfull = bar, b_qempty = bar + 16, b_kvfull = bar + 32,
                         b_kvempty = b_kvfull + 8 * S::kHalves, b_sfull = b_kvempty + 8 * S::kHalves,
                         b_pfull = b_sfull + 32, b_pvdone = b_pfull + 32, b_ofree = b_pvdone + 32;
     std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(smem + S::kOffMisc);
     volatile int* merge_flag = reinterpret_cast<volatile int*>(smem + S::kOffMisc + 4);
 
     if (tid == 0) {
-        mb_init(b_qfull, S::kLoaders);
-        mb_init(b_qempty, 2);  // one commit per MMA issuer
+        for (int b = 0; b < 2; ++b) {
+            mb_init(b_qfull + 8 * b, S::kLoaders);
+            mb_init(b_qempty + 8 * b, 2);  // one commit per MMA issuer
+        }
         for (int s = 0; s < S::kHalves; ++s) {
             mb_init(b_kvfull + 8 * s, S::kLoaders);
             mb_init(b_kvempty + 8 * s, 2);
@@ -510,18 +512,20 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
         // thread waits for it, fences the generic -> async proxy and arrives
         // on the half's full barrier (and on q_full for the group that also
         // carried the unit's Q pair), so the MMA warps only wait on barriers.
-        constexpr int kLag = 4;
-        static_assert(kLag + 4 < S::kHalves, "MMA progress must not need a half held back by the lag");
+        // (a half of ring slot s is released once the MMA warps consumed it,
+        // which needs only halves issued before it: kLag < kHalves suffices)
+        constexpr int kLag = 2;
+        static_assert(kLag < S::kHalves, "MMA progress must not need a half held back by the lag");
         int pend = 0, last_idx = -1;
-        unsigned qbits = 0;  // bit i: the group of half last_idx - i carried Q
-        auto arrive_half = [&](int hidx, bool q) {
-            if (q) mb_arrive(b_qfull);
+        unsigned qbits = 0, qsel = 0;  // bit i: the group of half last_idx - i carried a Q pair, its buffer
+        auto arrive_half = [&](int hidx, bool q, unsigned qb) {
+            if (q) mb_arrive(b_qfull + 8 * qb);
             mb_arrive(b_kvfull + 8 * half_slot(hidx));
         };
         auto flush = [&]() {
             cp_async_wait<0>();
             fence_proxy_async();
-            for (int i = pend - 1; i >= 0; --i) arrive_half(last_idx - i, (qbits >> i) & 1u);
+            for (int i = pend - 1; i >= 0; --i) arrive_half(last_idx - i, (qbits >> i) & 1u, (qsel >> i) & 1u);
             pend = 0;
         };
         Seg la = seg_at(a, g_begin, g_end);  // look-ahead cursor (tile g + 1)
@@ -529,11 +533,14 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
         int g = g_begin, s_idx = 0;
         while (g < g_end) {
             const Seg sg = seg_at(a, g, g_end);
-            // Q pair of the unit: rows of tile j = token (r / G) x head (r % G),
-            // padding rows zero; committed with the segment's first K half
-            if (s_idx > 0) {
-                flush();  // the MMA warps need every issued half to release Q
-                mb_wait(b_qempty, (s_idx - 1) & 1);
+            // Q pair of the unit into buffer s_idx & 1 (the next segment's Q
+            // loads while this one computes): rows of tile j = token (r / G) x
+            // head (r % G), padding rows zero; committed with the segment's
+            // first K half
+            const unsigned qb = static_cast<unsigned>(s_idx & 1);
+            if (s_idx > 1) {
+                flush();  // the MMA warps need every issued half to release that buffer
+                mb_wait(b_qempty + 8 * qb, ((s_idx - 2) >> 1) & 1);
             }
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
@@ -542,7 +549,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 const bool ok = rr < kTQ * G && tok < a.chunk;
                 const char* src = reinterpret_cast<const char*>(
                     a.q + (static_cast<std::size_t>(ok ? tok : 0) * n_q + static_cast<std::size_t>(sg.h) * G + rr % G) * D);
-                copy_row(sQ + j * S::kQB + rr * 128, dsw_q, src, ok);
+                copy_row(sQ + (2 * qb + j) * S::kQB + rr * 128, dsw_q, src, ok);
             }
             const std::uint64_t kb = static_cast<std::uint64_t>(a.layer * 2 * n_kv + sg.h) * a.g.tpp * (D * 2);
             for (; g < sg.g1; ++g) {
@@ -561,10 +568,11 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                     cp_async_commit();
                     last_idx = idx;
                     qbits = (qbits << 1) | ((kv == 0 && g == sg.g0) ? 1u : 0u);
+                    qsel = (qsel << 1) | qb;
                     if (++pend > kLag) {
                         cp_async_wait<kLag>();
                         fence_proxy_async();
-                        arrive_half(idx - kLag, (qbits >> kLag) & 1u);
+                        arrive_half(idx - kLag, (qbits >> kLag) & 1u, (qsel >> kLag) & 1u);
                         --pend;
                     }
                 }
@@ -590,7 +598,6 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 mb_wait(b_kvfull + 8 * half_slot(idx), half_phase(idx));  // the loaders fenced the proxy
                 tc_fence_after();
             };
-            const std::uint32_t dq = desc_lo(sQ + j * S::kQB, 16);
             const std::uint32_t s_col = tmem + j * 2 * S::kN, o_col = tmem + S::kColO + j * D;
             // S_j(k) = Q_j · K(k)ᵀ into S buffer (j, k & 1): two tiles ahead of P_j·V
             Seg sc = seg_at(a, g_begin, g_end);
@@ -601,7 +608,9 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                     sc = seg_at(a, g, g_end);
                     ++sc_idx;
                 }
-                if (g == sc.g0) mb_wait(b_qfull, sc_idx & 1);
+                const unsigned qb = static_cast<unsigned>(sc_idx & 1);
+                if (g == sc.g0) mb_wait(b_qfull + 8 * qb, (sc_idx >> 1) & 1);
+                const std::uint32_t dq = desc_lo(sQ + (2 * qb + j) * S::kQB, 16);
                 if (j == 0 && lane == 0) k4_stamp(a.trace, 11, k);
                 wait_half(2 * k);
                 if (j == 0 && lane == 0) k4_stamp(a.trace, 12, k);
@@ -610,7 +619,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 tc_mma_s_tile<D>(s_col + (k & 1) * S::kN, desc_of(dq), desc_of(dk), idesc_s);
                 tc_commit_e(b_sfull + 8 * (2 * j + (k & 1)));
                 tc_commit_e(b_kvempty + 8 * half_slot(2 * k));
-                if (g + 1 == sc.g1) tc_commit_e(b_qempty);  // last S of the segment: Q may be replaced
+                if (g + 1 == sc.g1) tc_commit_e(b_qempty + 8 * qb);  // last S of the segment: its Q buffer is free
                 if (j == 0 && lane == 0) k4_stamp(a.trace, 1, k);
             };
             issue_s(0);
@@ -956,7 +965,9 @@ void launch_k4(Ctx& d, PrefillArgs a) {
     a.n_qp = n_qp;
     a.qp_tiles = d.pf_prefix.dev;
     a.total = d.n_kv * d.pf_per_head;
-    a.per_cta = std::max(4, (a.total + sms - 1) / sms);
+    // one CTA per SM; a small launch (a short prefill chunk) spreads its
+    // tiles over as many CTAs as there are tiles (latency, not throughput)
+    a.per_cta = std::max(1, (a.total + sms - 1) / sms);
     const int grid = (a.total + a.per_cta - 1) / a.per_cta;
     const std::size_t slots = 2 * static_cast<std::size_t>(grid);
     float* ws = d.attn_workspace(slots * 256 * d.head_dim + slots * 256 * 2);
