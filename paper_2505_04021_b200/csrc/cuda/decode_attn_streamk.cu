@@ -69,8 +69,10 @@ __device__ __forceinline__ int swz_sk(int row, int chunk) {
     return (row * (D / 8) + (chunk ^ (row & 7))) * 16;
 }
 
+// d = 64: registers capped for 4 CTAs per SM (no spills; +5% on the d = 64
+// shapes); d = 128 keeps 3 (its smem allows 2-3, and the cap costs 2-3%).
 template <int D, int G>
-__global__ void __launch_bounds__(128, 3) k3_decode_streamk(SkArgs sk) {
+__global__ void __launch_bounds__(128, D == 64 ? 4 : 3) k3_decode_streamk(SkArgs sk) {
     using S = SkShape<D, G>;
     extern __shared__ __align__(128) unsigned char smem[];
     const AttnArgs& a = sk.a;
