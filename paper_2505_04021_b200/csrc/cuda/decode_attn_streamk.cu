@@ -102,6 +102,14 @@ __global__ void __launch_bounds__(128, D == 64 ? 4 : 3) k3_decode_streamk(SkArgs
     }
     __syncthreads();
     const int range = s_range;
+    // The next K3 of the chain may launch as soon as every CTA of this one has
+    // drawn its range (it then streams into the SMs this launch's CTAs leave).
+    // Safe: the next launch draws from the other counter, and the launch after
+    // it (this counter again) launches only once every CTA of the next one has
+    // drawn, i.e. after this launch's last drawer reset the counter; every
+    // write of the next launch waits for this launch's completion
+    // (griddepcontrol.wait before its first write, finish_pair).
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const int g_begin = range * sk.per_cta;
     const int g_end = min(sk.total_tiles, g_begin + sk.per_cta);
     if (g_begin >= g_end) return;
@@ -235,8 +243,17 @@ __global__ void __launch_bounds__(128, D == 64 ? 4 : 3) k3_decode_streamk(SkArgs
     float* red_m = red_o + S::kWarps * G * D;                  // [warps][8]
     float* red_l = red_m + S::kWarps * 8;                      // [warps][8]
 
+    bool pdl_waited = false;
+    auto pdl_wait = [&]() {
+        if (pdl_waited) return;
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
+        pdl_waited = true;
+        k3_stamp(sk.trace, 2);  // previous kernel complete
+    };
+
     // finish pair cp: merge warps, write out or a partial (+ merge if last)
     auto finish_pair = [&](int seg_first) {
+        pdl_wait();
         float ll0 = l0, ll1 = l1;
 #pragma unroll
         for (int off = 4; off < 32; off <<= 1) {
@@ -363,15 +380,15 @@ __global__ void __launch_bounds__(128, D == 64 ? 4 : 3) k3_decode_streamk(SkArgs
     if (g_begin + S::kStages - 1 < g_end) rows = load_rows(g_begin + S::kStages - 1);
     std::uint32_t blk_p = 0;  // raw slot id / block of tile g + kStages (decoded one iteration later)
     std::int32_t sid_p = g_begin + S::kStages < g_end ? load_sid(g_begin + S::kStages, blk_p) : -1;
-    // Programmatic dependent launch: everything above reads only state that
+    // Programmatic dependent launch: this launch only READS state that
     // predates the previous kernel on the stream (block table, decode
-    // descriptors, tile prefix, K/V pages — see EngineDeviceImpl::k3_chain),
-    // so it overlaps that kernel's tail. q, out and the split-K workspace
-    // (shared with the previous K3) are touched only after it completed.
+    // descriptors, tile prefix, K/V pages, and q: a K3 is chained only behind
+    // our own K3, which does not write q — see EngineDeviceImpl::k3_chain and
+    // INTEGRATION.md), so it streams and computes while the previous K3's
+    // last CTAs finish. Its WRITES (partials, tickets, out: the workspace and
+    // tickets are shared with the previous K3) wait for that kernel to
+    // complete: griddepcontrol.wait before the first one (finish_pair).
     k3_stamp(sk.trace, 1);  // prologue copies issued
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-    k3_stamp(sk.trace, 2);  // previous kernel complete
     ctx = a.desc[cp / n_kv].ctx;
     start_pair();
     const int wrow = warp * 16;
