@@ -315,3 +315,46 @@ def test_per_layer_append_then_attend_matches_batched(product, device):
     assert len(outs[0]) == len(outs[1]) > 5
     for a, b in zip(*outs):
         assert torch.equal(a.view(torch.int16), b.view(torch.int16))
+
+
+@pytest.mark.parametrize("shape", ["qwen2.5-1.5b", "llama3.1-8b"])
+def test_chained_launches_write_in_order(product, device, shape):
+    """A step's K3 launches form a programmatic-dependent chain in which a
+    launch streams K/V and q before its predecessor has completed and only
+    its writes (partials, tickets, out) wait for it. Chains of back-to-back
+    launches, with no synchronisation in between: (a) every layer into its
+    own out buffer, each equal to its layer's oracle; (b) every layer into
+    ONE shared out buffer, which must end up holding the last layer's
+    result (write-after-write order across chained launches)."""
+    gpu, spec, eng = _engine(product, device, shape, cap_pages=4000, chunk=1024)
+    for i in range(24):
+        eng.push(i + 1, 700 + 37 * i, 64)
+    while eng.counts()[1] or any(r.prompt_done < r.prompt_tokens for r in eng.batch()):
+        eng.step()
+        eng.append_kv_synthetic(0, spec.n_layers, SEED)
+    eng.step()
+    eng.append_kv_synthetic(0, spec.n_layers, SEED)
+    n_tok, n_dec = eng.step_info()
+    assert n_dec == 24
+    ids = eng.step_decode_ids()
+    live = {r.id: r.live_slots() for r in eng.batch()}
+    L, nq, nkv, d = spec.n_layers, spec.n_q_heads, spec.n_kv_heads, spec.head_dim
+    scale = 1.0 / math.sqrt(d)
+    q = torch.empty((L, n_dec, nq, d), dtype=torch.bfloat16, device="cuda")
+    for layer in range(L):
+        eng.synth_q(layer, SEED, 4.0, q[layer].data_ptr())
+    outs = torch.full_like(q, float("nan"))
+    shared = torch.full_like(q[0], float("nan"))
+    for layer in range(L):  # (a) one chain, distinct outputs
+        eng.decode_attention(layer, q[layer].data_ptr(), outs[layer].data_ptr(), scale)
+    for _ in range(3):  # (b) chains into one buffer, repeated
+        for layer in range(L):
+            eng.decode_attention(layer, q[layer].data_ptr(), shared.data_ptr(), scale)
+    eng.synchronize()
+    for layer in (0, L // 2, L - 1):
+        ref = oracle.synth_attention(SEED, layer, ids, [live[i] for i in ids], nq, nkv, d, 4.0, scale)
+        _close(outs[layer].float().cpu().numpy(), ref)
+        if layer == L - 1:
+            _close(shared.float().cpu().numpy(), ref)
+    # all layers' outputs are complete (no NaN left by a skipped write)
+    assert not torch.isnan(outs.float()).any()
