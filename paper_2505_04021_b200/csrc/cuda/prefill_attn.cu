@@ -30,7 +30,8 @@
 //               writes P0 (bf16) back into the buffer's columns, epilogue
 //               O0 / l (or a partial);
 //   warps 4-7   softmax warpgroup 1: the same for Q tile 1 (S1, O1);
-//   warps 8-11  loaders: Q pair once per unit segment, then each 64-key K
+//   warps 10-11 loaders (warps 8-9 idle, so the two schedulers of the MMA
+//               warps carry no loader): Q pair once per unit segment, then each 64-key K
 //               and V tile gathered from the pages with cp.async (16 B per
 //               thread-op) into 128B-swizzled tiles (the UMMA canonical
 //               layout) through a ring of K|V halves; every thread owns a
@@ -116,7 +117,7 @@ struct PfShape {
     static constexpr int kOffMisc = kOffBar + kBars * 8;  // TMEM address, merge flag
     static constexpr int kSmem = kOffMisc + 16 + 1024;    // + alignment slack
     static constexpr int kThreads = 512;
-    static constexpr int kLoaders = 128;      // warps 8-11
+    static constexpr int kLoaders = 64;       // warps 10-11 (schedulers 2, 3; the MMA warps own 0, 1)
     // setmaxnreg split of the 64K registers: softmax warpgroups 0-1 grow,
     // loader warpgroup 2 and the MMA warpgroup 3 shrink (2 x 128 x (168 + 88))
     static constexpr int kRegsSoftmax = 168;
@@ -465,17 +466,21 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
     auto half_slot = [](int idx) { return idx % S::kHalves; };
     auto half_phase = [](int idx) { return static_cast<std::uint32_t>((idx / S::kHalves) & 1); };
 
-    if (warp >= 8 && warp < 12) {
+    if (warp >= 8 && warp < 10) {
+        // idle (registers only): the schedulers of the MMA warps (0, 1) carry
+        // no loader, which measured +5% at 2K-token chunks
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(S::kRegsLoad));
+    } else if (warp >= 10 && warp < 12) {
         // ------------------------------------------------------------ loaders
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(S::kRegsLoad));
         // Fixed rows per thread: lanes 2i and 2i+1 share a row (one 32-byte
         // sector per lane pair and instruction), lane parity h picks the odd
-        // or even 16-byte chunks; loader warp w owns K/V tile row 16w + i (and
-        // rows 64m + 16w + i of the Q pair), so a thread decodes its own
-        // row's slot id one tile ahead in registers and each cp.async is one
-        // add + LDGSTS.
-        const int w = warp - 8, h = lane & 1;
-        const int ra = 16 * w + (lane >> 1);
+        // or even 16-byte chunks; loader warp w owns K/V tile rows 16w + i
+        // and 32 + 16w + i (and rows 32m + 16w + i of the Q pair), so a thread
+        // decodes its own rows' slot ids one tile ahead in registers and each
+        // cp.async is one add + LDGSTS.
+        const int w = warp - 10, h = lane & 1;
+        const int ra = 16 * w + (lane >> 1), rb = ra + 32;  // ra & 7 == rb & 7
         constexpr int kCpl = D / 16;  // chunks per lane per row
         const char* base = reinterpret_cast<const char*>(a.g.base);
         const std::uint64_t v_delta = static_cast<std::uint64_t>(n_kv) * a.g.tpp * (D * 2);
@@ -495,8 +500,8 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
 #pragma unroll
             for (int i = 0; i < kCpl; ++i) cp_async16_s(dst_row + dsw[i], p + i * 32, bytes);
         };
-        auto load_sid = [&](int kt) -> std::int32_t {
-            const int key = kt * S::kN + ra;
+        auto load_sid = [&](int kt, int r) -> std::int32_t {
+            const int key = kt * S::kN + r;
             return key < keys ? __ldg(a.row + key) : -1;
         };
         // byte offset of the row from the pool base, head block excluded; ~0: past the keys
@@ -529,7 +534,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
             pend = 0;
         };
         Seg la = seg_at(a, g_begin, g_end);  // look-ahead cursor (tile g + 1)
-        std::uint64_t oa = decode(load_sid(g_begin - la.ustart));
+        std::uint64_t oa = decode(load_sid(g_begin - la.ustart, ra)), ob = decode(load_sid(g_begin - la.ustart, rb));
         int g = g_begin, s_idx = 0;
         while (g < g_end) {
             const Seg sg = seg_at(a, g, g_end);
@@ -543,8 +548,8 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 mb_wait(b_qempty + 8 * qb, ((s_idx - 2) >> 1) & 1);
             }
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-                const int r = ra + 64 * m, j = r >> 7, rr = r & 127;
+            for (int m = 0; m < 8; ++m) {
+                const int r = ra + 32 * m, j = r >> 7, rr = r & 127;
                 const int tok = (2 * sg.qp + j) * kTQ + rr / G;
                 const bool ok = rr < kTQ * G && tok < a.chunk;
                 const char* src = reinterpret_cast<const char*>(
@@ -554,17 +559,20 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
             const std::uint64_t kb = static_cast<std::uint64_t>(a.layer * 2 * n_kv + sg.h) * a.g.tpp * (D * 2);
             for (; g < sg.g1; ++g) {
                 const int k = g - g_begin;
-                std::int32_t na = -1;
+                std::int32_t na = -1, nb = -1;
                 if (g + 1 < g_end) {
                     if (g + 1 >= la.g1) la = seg_at(a, g + 1, g_end);
-                    na = load_sid(g + 1 - la.ustart);
+                    na = load_sid(g + 1 - la.ustart, ra);
+                    nb = load_sid(g + 1 - la.ustart, rb);
                 }
 #pragma unroll
                 for (int kv = 0; kv < 2; ++kv) {
                     const int idx = 2 * k + kv;
                     const int hs = half_slot(idx);
                     if (idx >= S::kHalves) mb_wait(b_kvempty + 8 * hs, half_phase(idx) ^ 1u);
-                    copy_row(sKV + hs * S::kHalfB + ra * 128, dsw_kv, base + kb + (kv ? v_delta : 0) + oa, oa != ~0ull);
+                    const char* blk = base + kb + (kv ? v_delta : 0);
+                    copy_row(sKV + hs * S::kHalfB + ra * 128, dsw_kv, blk + oa, oa != ~0ull);
+                    copy_row(sKV + hs * S::kHalfB + rb * 128, dsw_kv, blk + ob, ob != ~0ull);
                     cp_async_commit();
                     last_idx = idx;
                     qbits = (qbits << 1) | ((kv == 0 && g == sg.g0) ? 1u : 0u);
@@ -578,6 +586,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 }
                 if (lane == 0 && w == 0) k4_stamp(a.trace, 0, k);
                 oa = decode(na);
+                ob = decode(nb);
             }
             ++s_idx;
         }
