@@ -804,9 +804,12 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 a.part_ml[static_cast<std::size_t>(slot) * 256 + row] = make_float2(m_run, l_run);
                 tc_fence_before();
                 mb_arrive(b_ofree + 8 * j);
-                __threadfence();
+                // the barrier orders every thread's partial stores before
+                // thread 0's gpu-scope release (fence + ticket), which is
+                // cumulative over them (the usual semaphore pattern)
                 asm volatile("bar.sync 1, 256;\n" ::: "memory");
                 if (tid == 0) {
+                    __threadfence();
                     const int prev = atomicAdd(a.tickets + u, 1);
                     const int last = prev == parts - 1;
                     if (last) a.tickets[u] = 0;  // no other CTA touches it again in this launch
