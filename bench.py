@@ -1130,6 +1130,14 @@ def main():
                 res["serving"] = serving_gpu()
             except Exception as e:
                 res["serving"] = {"error": str(e)}
+        if world == 1 and isinstance(res.get("serving"), dict) and "c2" in res["serving"]:
+            # the same C2 page churn served by the two-level scheduler with all
+            # kernels (K1/K2/K4/K3 every iteration): the maps' driver calls then
+            # overlap real kernel time instead of an attention-only engine loop
+            m = res["serving"]["c2"].get("measured", {})
+            res["page_map_c2_served"] = dict(m.get("page_map", {}), note=(
+                "scheduler-driven C2 run (bench serving.c2, kernel-timed clock): engine-thread and worker "
+                "time per logical page op; page_map_c2 above is the attention-only stress loop"))
         print(json.dumps(res))
     if world > 1:
         import torch.distributed as dist
