@@ -150,3 +150,48 @@ def test_k4_c3_32k_prefix(product, device):
         if first + n >= ctx:
             break
     assert checked >= 8
+
+
+@pytest.mark.parametrize("n_q,n_kv,chunk", [(14, 2, 1024), (32, 8, 384)])
+def test_k4_head_dim_64_long_prefix(product, device, n_q, n_kv, chunk):
+    """K4 on the head_dim-64 path (16-half K/V ring, two Q buffers) at long
+    prefixes: qwen2.5-0.5b (GQA 7, padded Q-tile rows) and llama3.2-1b
+    (GQA 4) shapes prefilled to 8K keys; at the chunks ending at 4K and 8K
+    keys, sampled query tokens against the fp64 oracle (cut units, partials
+    and merges all exercised: the grid spreads each launch over the SMs)."""
+    ctx, layer, q_scale, d = 8192, 3, 4.0, 64
+    gpu = msim.GpuState(0, ctx // 64 + 64, lib=product)
+    gpu.ledger.attach_device(device)
+    spec = msim.ModelSpec.llm("k4-d64", 16, n_q, n_kv, d, chunk_size=chunk)
+    act = gpu.activate(spec)
+    gpu.finish_activation(act.engine_index)
+    eng = gpu.engine(act.engine_index)
+    eng.attach_device(max_step_tokens=chunk + 8)
+    eng.push(1, ctx, 2)
+    scale = 1 / math.sqrt(d)
+    rng = random.Random(n_q)
+    checked = 0
+    while True:
+        eng.step()
+        eng.append_kv_synthetic(0, 16, SEED)
+        n, first, rid = eng.prefill_info()
+        if n == 0:
+            break
+        if first < ctx // 2 <= first + n or first + n >= ctx:
+            picks = sorted({0, n - 1, *[rng.randrange(n) for _ in range(5)]})
+            qh = np.random.default_rng(first).integers(0x3c00, 0x3f80, size=(n, n_q, d), dtype=np.uint16)
+            qh[picks] = _synth_q_rows(rid, [first + i for i in picks], layer, n_q, d, q_scale)
+            q = torch.from_numpy(qh.view(np.int16)).view(torch.bfloat16).cuda()
+            o = torch.full_like(q, float("nan"))
+            torch.cuda.current_stream().synchronize()
+            eng.prefill_attention(layer, q.data_ptr(), o.data_ptr(), scale)
+            eng.synchronize()
+            oc = o.float().cpu().numpy()
+            assert not np.isnan(oc).any()
+            ref = oracle.synth_attention(SEED, layer, [rid] * len(picks), [first + i + 1 for i in picks], n_q, n_kv, d,
+                                         q_scale, scale)
+            _close(oc[picks], ref)
+            checked += len(picks)
+        if first + n >= ctx:
+            break
+    assert checked >= 8
