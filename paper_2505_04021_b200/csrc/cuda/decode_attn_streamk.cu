@@ -40,7 +40,9 @@ struct SkShape {
     static constexpr int kKSteps = D / 16;
     static constexpr int kMTiles = D / 16;
     static constexpr int kRingB = kStages * kStageB;
-    static constexpr int kMergeB = (kWarps * G * D + 2 * kWarps * 8) * 4;  // separate from the ring
+    // warp partials [warps][G][D] + (m, l) [warps][8], then the stash of the
+    // range's first segment [G][D] + [G][2]; separate from the ring
+    static constexpr int kMergeB = (kWarps * G * D + 2 * kWarps * 8 + G * D + 2 * G) * 4;
     static constexpr int kSmem = kRingB + kMergeB;
 };
 
@@ -251,9 +253,18 @@ __global__ void __launch_bounds__(128, D == 64 ? 4 : 3) k3_decode_streamk(SkArgs
         k3_stamp(sk.trace, 2);  // previous kernel complete
     };
 
-    // finish pair cp: merge warps, write out or a partial (+ merge if last)
-    auto finish_pair = [&](int seg_first) {
-        pdl_wait();
+    // The range's FIRST pair segment is stashed — its CTA-combined (m, l, O)
+    // kept in shared memory — and written at the next segment's end (or the
+    // kernel's): a chained launch's writes wait for the previous launch
+    // (griddepcontrol.wait), and a range's first segment usually ends after a
+    // few tiles, so writing it at once stalled the CTA's streaming.
+    float* stash_o = red_l + S::kWarps * 8;  // [G][D]
+    float* stash_ml = stash_o + G * D;       // [G][2]
+    bool stashed = false, first_segment = true;
+    int st_cp = 0, st_first = 0, st_end = 0;
+
+    // the CTA-combined (m, l, O) of pair cp's segment into stash_o / stash_ml
+    auto combine = [&]() {
         float ll0 = l0, ll1 = l1;
 #pragma unroll
         for (int off = 4; off < 32; off <<= 1) {
@@ -279,26 +290,7 @@ __global__ void __launch_bounds__(128, D == 64 ? 4 : 3) k3_decode_streamk(SkArgs
             red_l[warp * 8 + qc + 1] = ll1;
         }
         __syncthreads();
-        const int b = cp / n_kv, h = cp % n_kv;
-        // CTAs whose ranges intersect this pair
-        const int first_cta = cp_first / sk.per_cta;
-        const int last_cta = (cp_end - 1) / sk.per_cta;
-        const int parts = last_cta - first_cta + 1;
-        const int part = range - first_cta;
-        __nv_bfloat16* out = a.out + (static_cast<std::size_t>(b) * n_q + static_cast<std::size_t>(h) * G) * D;
-        const std::size_t pslot = static_cast<std::size_t>(cp) * sk.max_parts + part;
-        // A cut pair is merged by its FIRST CTA (part 0): that CTA reaches the
-        // pair at the end of its range, after the later parts (computed at
-        // the start of the next CTAs' ranges) were published. It keeps its
-        // own (m, l, O) in registers, waits for the ticket to count the other
-        // parts (almost never an actual wait) and combines; the other parts
-        // write a partial, fence once and bump the ticket.
-        constexpr int kPer = (G * D + S::kThreads - 1) / S::kThreads;
-        float own_m[kPer], own_l[kPer], own_o[kPer];
-#pragma unroll
-        for (int k = 0; k < kPer; ++k) {
-            const int idx = tid + k * S::kThreads;
-            if (idx >= G * D) break;
+        for (int idx = tid; idx < G * D; idx += S::kThreads) {
             const int g = idx / D, d = idx % D;
             float mm = -INFINITY;
 #pragma unroll
@@ -311,43 +303,69 @@ __global__ void __launch_bounds__(128, D == 64 ? 4 : 3) k3_decode_streamk(SkArgs
                 ll += red_l[w * 8 + g] * f;
                 oo += red_o[(w * G + g) * D + d] * f;
             }
-            own_m[k] = mm;
-            own_l[k] = ll;
-            own_o[k] = oo;
-            if (parts == 1) {
-                out[idx] = __float2bfloat16_rn(oo / ll);
-            } else if (part > 0) {
-                a.part_o[pslot * G * D + idx] = oo;
-                if (d == 0) {
-                    a.part_ml[(pslot * G + g) * 2] = mm;
-                    a.part_ml[(pslot * G + g) * 2 + 1] = ll;
-                }
+            stash_o[idx] = oo;
+            if (d == 0) {
+                stash_ml[2 * g] = mm;
+                stash_ml[2 * g + 1] = ll;
             }
         }
-        if (parts > 1 && part > 0) {
-            __syncthreads();  // all of this CTA's partial stores precede the fence
-            if (tid == 0) {
-                __threadfence();
-                atomicAdd(&a.tickets[cp], 1);
+        __syncthreads();  // stash complete; red_* free for the next pair
+    };
+
+    // the writes of pair pc's segment from the stash: out, or a partial +
+    // ticket, or (first part of a cut pair) the merge of the later parts
+    auto emit = [&](int pc, int pc_first, int pc_end) {
+        pdl_wait();
+        const int b = pc / n_kv, h = pc % n_kv;
+        // CTAs whose ranges intersect this pair
+        const int first_cta = pc_first / sk.per_cta;
+        const int last_cta = (pc_end - 1) / sk.per_cta;
+        const int parts = last_cta - first_cta + 1;
+        const int part = range - first_cta;
+        __nv_bfloat16* out = a.out + (static_cast<std::size_t>(b) * n_q + static_cast<std::size_t>(h) * G) * D;
+        const std::size_t pslot = static_cast<std::size_t>(pc) * sk.max_parts + part;
+        // A cut pair is merged by its FIRST CTA (part 0): that CTA reaches the
+        // pair at the end of its range, after the later parts (computed at
+        // the start of the next CTAs' ranges) were published. It combines its
+        // own (m, l, O) from the stash with theirs after the ticket counts
+        // them (almost never an actual wait); the other parts write a
+        // partial, fence once and bump the ticket.
+        if (parts == 1 || part > 0) {
+            for (int idx = tid; idx < G * D; idx += S::kThreads) {
+                const int g = idx / D, d = idx % D;
+                const float oo = stash_o[idx];
+                if (parts == 1) {
+                    out[idx] = __float2bfloat16_rn(oo / stash_ml[2 * g + 1]);
+                } else {
+                    a.part_o[pslot * G * D + idx] = oo;
+                    if (d == 0) {
+                        a.part_ml[(pslot * G + g) * 2] = stash_ml[2 * g];
+                        a.part_ml[(pslot * G + g) * 2 + 1] = stash_ml[2 * g + 1];
+                    }
+                }
             }
-        } else if (parts > 1) {
+            if (parts > 1) {
+                __syncthreads();  // all of this CTA's partial stores precede the fence
+                if (tid == 0) {
+                    __threadfence();
+                    atomicAdd(&a.tickets[pc], 1);
+                }
+            }
+        } else {
             if (tid == 0) {
-                const int* tk = &a.tickets[cp];
+                const int* tk = &a.tickets[pc];
                 int seen;
                 do {
                     asm volatile("ld.acquire.gpu.global.s32 %0, [%1];\n" : "=r"(seen) : "l"(tk) : "memory");
                 } while (seen < parts - 1);
             }
             __syncthreads();
-            const std::size_t p0 = static_cast<std::size_t>(cp) * sk.max_parts;
-#pragma unroll
-            for (int k = 0; k < kPer; ++k) {
-                const int idx = tid + k * S::kThreads;
-                if (idx >= G * D) break;
+            const std::size_t p0 = static_cast<std::size_t>(pc) * sk.max_parts;
+            for (int idx = tid; idx < G * D; idx += S::kThreads) {
                 const int g = idx / D;
                 // one pass, online combination: each part's (m, l, o) loads are
                 // independent of the running state, so they go out together
-                float mm = own_m[k], ll = own_l[k], oo = own_o[k];
+                float mm = stash_ml[2 * g], ll = stash_ml[2 * g + 1], oo = stash_o[idx];
 #pragma unroll 2
                 for (int sp = 1; sp < parts; ++sp) {
                     const float pm = __ldcg(&a.part_ml[((p0 + sp) * G + g) * 2]);
@@ -361,10 +379,27 @@ __global__ void __launch_bounds__(128, D == 64 ? 4 : 3) k3_decode_streamk(SkArgs
                 }
                 out[idx] = __float2bfloat16_rn(oo / ll);
             }
-            if (tid == 0) a.tickets[cp] = 0;  // next launch touches tickets only after its PDL wait
+            if (tid == 0) a.tickets[pc] = 0;  // the next launch touches tickets only after its PDL wait
         }
-        __syncthreads();  // red_* reused by the next pair
-        (void)seg_first;
+        __syncthreads();  // stash free
+    };
+
+    // end of pair cp's segment inside the range
+    auto finish_pair = [&]() {
+        if (stashed) {  // the range's first segment: its writes, now
+            emit(st_cp, st_first, st_end);
+            stashed = false;
+        }
+        combine();
+        if (first_segment) {
+            first_segment = false;
+            stashed = true;
+            st_cp = cp;
+            st_first = cp_first;
+            st_end = cp_end;
+            return;
+        }
+        emit(cp, cp_first, cp_end);
     };
 
     // ---------------- pipeline over the CTA's tile range
@@ -470,7 +505,7 @@ __global__ void __launch_bounds__(128, D == 64 ? 4 : 3) k3_decode_streamk(SkArgs
         if (g + 1 == g_end) k3_stamp(sk.trace, 4);  // last tile computed
         // end of this pair's segment inside the range?
         if (g + 1 == cp_end || g + 1 == g_end) {
-            finish_pair(cp_first);
+            finish_pair();
             if (g + 1 < g_end) {
                 ++cp;
                 cp_first = cp_end;
@@ -480,6 +515,7 @@ __global__ void __launch_bounds__(128, D == 64 ? 4 : 3) k3_decode_streamk(SkArgs
             }
         }
     }
+    if (stashed) emit(st_cp, st_first, st_end);  // a single-segment range
     cp_async_wait<0>();
     k3_stamp(sk.trace, 5);  // done (incl. the last pair's merge)
     if (sk.trace && threadIdx.x == 0) sk.trace[blockIdx.x * 8 + 6] = static_cast<unsigned long long>(g_end - g_begin);
