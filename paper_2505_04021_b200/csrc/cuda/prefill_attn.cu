@@ -46,6 +46,7 @@
 //               S(t+2) overwrites P(t) only after P(t)·V(t) read it. Warps
 //               14-15 only give their registers away.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdint>
@@ -75,7 +76,7 @@ struct PrefillArgs {
     const std::int32_t* qp_tiles;  // [n_qp + 1] key-tile prefix over the pairs (same for every kv head)
     int per_cta;              // key tiles per CTA range
     int total;                // key tiles of all units = n_kv * qp_tiles[n_qp]
-    float4* part_o;           // [2 * grid][D / 4][256] unnormalised O of cut units
+    uint2* part_o;            // [2 * grid][D / 4][256] O / l of cut units, fp16 x 4
     float2* part_ml;          // [2 * grid][256] (m, l) of cut units
     int* tickets;             // [n_kv * n_qp], zero between launches
     unsigned long long* trace;  // PRISM_K4_TRACE: [8][1024] globaltimer stamps of CTA 0, else null
@@ -346,6 +347,14 @@ __device__ __forceinline__ void tc_st16_nowait(std::uint32_t taddr, const std::u
         "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
         "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
         : "memory");
+}
+
+__device__ __forceinline__ std::uint32_t pack_f16(float lo, float hi) {
+    const __half2 p = __floats2half2_rn(lo, hi);
+    return *reinterpret_cast<const std::uint32_t*>(&p);
+}
+__device__ __forceinline__ float2 unpack_f16(std::uint32_t w) {
+    return __half22float2(*reinterpret_cast<const __half2*>(&w));
 }
 
 // Shared-memory matrix descriptor (sm_100 "version 1"), 128-byte swizzle.
@@ -792,6 +801,9 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 // publish this CTA's partial of the unit (slot 2c: the range's
                 // first segment, 2c + 1: its last), then the last publisher merges
                 const int slot = 2 * static_cast<int>(blockIdx.x) + (sg.g0 == g_begin ? 0 : 1);
+                // O / l: |values| <= max |V|, so fp16 keeps 2^-11 relative
+                // precision in half the bytes of an fp32 partial
+                const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll
                 for (int cc = 0; cc < D / 32; ++cc) {
                     float o[32];
@@ -799,7 +811,8 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
 #pragma unroll
                     for (int q = 0; q < 8; ++q)
                         a.part_o[(static_cast<std::size_t>(slot) * (D / 4) + cc * 8 + q) * 256 + row] =
-                            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+                            make_uint2(pack_f16(o[4 * q] * inv_l, o[4 * q + 1] * inv_l),
+                                       pack_f16(o[4 * q + 2] * inv_l, o[4 * q + 3] * inv_l));
                 }
                 a.part_ml[static_cast<std::size_t>(slot) * 256 + row] = make_float2(m_run, l_run);
                 tc_fence_before();
@@ -837,16 +850,18 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                         for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
                         for (int cta = first_cta; cta <= last_cta; ++cta) {
                             const int sl = slot_of(cta);
-                            const float pm = __ldcg(a.part_ml + static_cast<std::size_t>(sl) * 256 + row).x;
-                            const float wt = pm == -INFINITY ? 0.f : fast_exp2(pm - mm) * inv;
+                            const float2 pml = __ldcg(a.part_ml + static_cast<std::size_t>(sl) * 256 + row);
+                            // the partial is O / l: weight by l
+                            const float wt = pml.x == -INFINITY ? 0.f : fast_exp2(pml.x - mm) * pml.y * inv;
 #pragma unroll
                             for (int q = 0; q < 8; ++q) {
-                                const float4 o4 =
+                                const uint2 h4 =
                                     __ldcg(a.part_o + (static_cast<std::size_t>(sl) * (D / 4) + cg * 8 + q) * 256 + row);
-                                acc[q].x += wt * o4.x;
-                                acc[q].y += wt * o4.y;
-                                acc[q].z += wt * o4.z;
-                                acc[q].w += wt * o4.w;
+                                const float2 lo = unpack_f16(h4.x), hi = unpack_f16(h4.y);
+                                acc[q].x += wt * lo.x;
+                                acc[q].y += wt * lo.y;
+                                acc[q].z += wt * hi.x;
+                                acc[q].w += wt * hi.y;
                             }
                         }
                         if (row_ok) {
@@ -983,7 +998,7 @@ void launch_k4(Ctx& d, PrefillArgs a) {
     const int grid = (a.total + a.per_cta - 1) / a.per_cta;
     const std::size_t slots = 2 * static_cast<std::size_t>(grid);
     float* ws = d.attn_workspace(slots * 256 * d.head_dim + slots * 256 * 2);
-    a.part_o = reinterpret_cast<float4*>(ws);
+    a.part_o = reinterpret_cast<uint2*>(ws);
     a.part_ml = reinterpret_cast<float2*>(ws + slots * 256 * d.head_dim);
     a.tickets = d.attn_counters(static_cast<std::size_t>(d.n_kv) * n_qp);
     a.dbg = k4_debug_words();
