@@ -106,7 +106,6 @@ template <int D>
 struct PfShape {
     static constexpr int kM = 128;            // MMA rows per Q tile (packed token x head)
     static constexpr int kN = 64;             // keys per K/V tile
-    static constexpr int kSub = D / 64;       // 64-element (128 B) swizzle atoms along head_dim
     static constexpr int kQB = kM * D * 2;    // one Q tile
     static constexpr int kHalfB = kN * D * 2;  // one K (or V) tile
     static constexpr int kHalves = D == 128 ? 6 : 16;  // ring slots of K|V halves
@@ -168,41 +167,13 @@ __device__ __forceinline__ void cp_async16_s(std::uint32_t dst, const void* src,
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
-__device__ __forceinline__ void tc_commit(std::uint32_t bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(bar)
-                 : "memory");
-}
-// D[tmem] (+)= A[smem] · B[smem], kind::f16 (bf16 in, fp32 accumulate)
-__device__ __forceinline__ void tc_mma(std::uint32_t d_tmem, std::uint64_t a_desc, std::uint64_t b_desc,
-                                       std::uint32_t idesc, std::uint32_t accumulate) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-// Warp-wide variants: every lane executes them with the same operands, one
-// elected lane issues (no divergent single-lane region around the uniform ops)
+// tcgen05 ops issued warp-wide: every lane executes them with the same
+// operands and one elected lane issues (no divergent single-lane region
+// around the uniform ops). MMAs are kind::f16: bf16 in, fp32 accumulate.
 __device__ __forceinline__ void tc_commit_e(std::uint32_t bar) {
     asm volatile(
         "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
         " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(bar)
-        : "memory");
-}
-__device__ __forceinline__ void tc_mma_e(std::uint32_t d_tmem, std::uint64_t a_desc, std::uint64_t b_desc,
-                                         std::uint32_t idesc, std::uint32_t accumulate) {
-    asm volatile(
-        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
-        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-__device__ __forceinline__ void tc_mma_ts_e(std::uint32_t d_tmem, std::uint32_t a_tmem, std::uint64_t b_desc,
-                                            std::uint32_t idesc, std::uint32_t accumulate) {
-    asm volatile(
-        "{\n .reg .pred p, e;\n setp.ne.b32 p, %4, 0;\n elect.sync _|e, 0xffffffff;\n"
-        " @e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
 // One tile's MMAs from one asm statement (the operands reach the uniform
@@ -251,8 +222,9 @@ __device__ __forceinline__ void tc_mma_s_tile(std::uint32_t d_tmem, std::uint64_
         : "memory");
     }
 }
-// O_j (+)= P_j · V(k) over the tile's 64 keys in K=16 steps: P from TMEM (+8
-// columns per step), V MN-major (+16 rows = 2048 B per step).
+// O_j (+)= P_j · V(k) over the tile's 64 keys in K=16 steps: P (the A
+// operand) from tensor memory, lane = row, two bf16 K-elements per 32-bit
+// column (+8 columns per step); V MN-major (+16 rows = 2048 B per step).
 __device__ __forceinline__ void tc_mma_pv_tile(std::uint32_t d_tmem, std::uint32_t p_tmem, std::uint64_t dv,
                                                std::uint32_t idesc, std::uint32_t accumulate) {
     asm volatile(
@@ -329,26 +301,6 @@ __device__ __forceinline__ void tc_st32_nowait(std::uint32_t taddr, const std::u
         : "memory");
 }
 
-// D[tmem] (+)= A[tmem] · B[smem]: the A operand (P) read from tensor memory,
-// lane = row, two bf16 K-elements per 32-bit column (8 columns per K=16 step)
-__device__ __forceinline__ void tc_mma_ts(std::uint32_t d_tmem, std::uint32_t a_tmem, std::uint64_t b_desc,
-                                          std::uint32_t idesc, std::uint32_t accumulate) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-        " tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-// 16 consecutive 32-bit columns of this thread's TMEM lane (no wait)
-__device__ __forceinline__ void tc_st16_nowait(std::uint32_t taddr, const std::uint32_t (&v)[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
-        "%14, %15, %16};\n" ::"r"(taddr),
-        "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
-        "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-        : "memory");
-}
-
 __device__ __forceinline__ std::uint32_t pack_f16(float lo, float hi) {
     const __half2 p = __floats2half2_rn(lo, hi);
     return *reinterpret_cast<const std::uint32_t*>(&p);
@@ -362,16 +314,9 @@ __device__ __forceinline__ float2 unpack_f16(std::uint32_t w) {
 // 8-row groups 1024 B apart (SBO), LBO unused (1). MN-major canonical layout
 // ((T,8,n),(8,k)):((1,T,LBO),(8T,SBO)): 64-element atoms along MN `lbo` bytes
 // apart, 8-row K groups 1024 B apart.
-__device__ __forceinline__ std::uint64_t sw128_desc(std::uint32_t addr, std::uint32_t lbo_bytes) {
-    std::uint64_t d = 0;
-    d |= static_cast<std::uint64_t>((addr >> 4) & 0x3fff);
-    d |= static_cast<std::uint64_t>((lbo_bytes >> 4) & 0x3fff) << 16;
-    d |= static_cast<std::uint64_t>((1024u >> 4) & 0x3fff) << 32;
-    d |= static_cast<std::uint64_t>(1) << 46;  // version (sm_100)
-    d |= static_cast<std::uint64_t>(2) << 61;  // SWIZZLE_128B
-    return d;
-}
-// The low word of that descriptor (start address >> 4, LBO >> 4): it varies
+// Fields: start address >> 4 (bits 0-13), LBO >> 4 (16-29), SBO >> 4 = 64
+// (32-45), version 1 (46), SWIZZLE_128B (61-63).
+// Its low word (start address >> 4, LBO >> 4) varies
 // per operand tile and K step and never carries into the high word (shared
 // addresses < 256 KB), which is the constant kDescHi. Offsets are added to the
 // low word as >> 4.
@@ -565,6 +510,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                     a.q + (static_cast<std::size_t>(ok ? tok : 0) * n_q + static_cast<std::size_t>(sg.h) * G + rr % G) * D);
                 copy_row(sQ + (2 * qb + j) * S::kQB + rr * 128, dsw_q, src, ok);
             }
+            if (lane == 0 && w == 0) k4_mark(a.dbg, 0, 1 + s_idx);  // loader: Q pair of segment issued
             const std::uint64_t kb = static_cast<std::uint64_t>(a.layer * 2 * n_kv + sg.h) * a.g.tpp * (D * 2);
             for (; g < sg.g1; ++g) {
                 const int k = g - g_begin;
@@ -593,7 +539,10 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                         --pend;
                     }
                 }
-                if (lane == 0 && w == 0) k4_stamp(a.trace, 0, k);
+                if (lane == 0 && w == 0) {
+                    k4_stamp(a.trace, 0, k);
+                    k4_mark(a.dbg, 1, 100 + k);  // loader: tile issued
+                }
                 oa = decode(na);
                 ob = decode(nb);
             }
@@ -638,7 +587,10 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 tc_commit_e(b_sfull + 8 * (2 * j + (k & 1)));
                 tc_commit_e(b_kvempty + 8 * half_slot(2 * k));
                 if (g + 1 == sc.g1) tc_commit_e(b_qempty + 8 * qb);  // last S of the segment: its Q buffer is free
-                if (j == 0 && lane == 0) k4_stamp(a.trace, 1, k);
+                if (lane == 0) {
+                    if (j == 0) k4_stamp(a.trace, 1, k);
+                    k4_mark(a.dbg, 2 + j, 100 + k);  // MMA warp j: S(k) issued
+                }
             };
             issue_s(0);
             if (n > 1) issue_s(1);
@@ -663,7 +615,10 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 tc_mma_pv_tile(o_col, s_col + (k & 1) * S::kN, desc_of(dv), idesc_o, fresh ? 0u : 1u);
                 tc_commit_e(b_pvdone + 8 * (2 * j + (k & 1)));
                 tc_commit_e(b_kvempty + 8 * half_slot(2 * k + 1));
-                if (lane == 0) k4_stamp(a.trace, j == 0 ? 2 : 7, k);
+                if (lane == 0) {
+                    k4_stamp(a.trace, j == 0 ? 2 : 7, k);
+                    if (j == 0) k4_mark(a.dbg, 4, 100 + k);  // MMA warp 0: P·V(k) issued
+                }
                 if (k + 2 < n) issue_s(k + 2);
             }
         }
@@ -698,7 +653,10 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 const int b = k & 1;
                 mb_wait(b_sfull + 8 * (2 * j + b), (k >> 1) & 1);
                 tc_fence_after();
-                if (r == 0) k4_stamp(a.trace, j == 0 ? 3 : 5, k);
+                if (r == 0) {
+                    k4_stamp(a.trace, j == 0 ? 3 : 5, k);
+                    if (j == 0) k4_mark(a.dbg, 5, 100 + k);  // softmax 0: has S(k)
+                }
                 const std::uint32_t tS = tmem + lane_base + j * 2 * S::kN + b * S::kN;
                 const int k0 = (g - sg.ustart) * S::kN;
                 // the tile's S row in registers (one tcgen05.ld wait), row max
@@ -769,10 +727,14 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 l_run += l2.x + l2.y;
                 tc_fence_before();
                 mb_arrive(b_pfull + 8 * (2 * j + b));
-                if (r == 0) k4_stamp(a.trace, j == 0 ? 4 : 6, k);
+                if (r == 0) {
+                    k4_stamp(a.trace, j == 0 ? 4 : 6, k);
+                    if (j == 0) k4_mark(a.dbg, 6, 100 + k);  // softmax 0: posted P(k)
+                }
             }
             // ---- epilogue of the unit segment: O_j complete after PV_j(last)
             wait_pv(k - 1);
+            if (j == 0 && r == 0) k4_mark(a.dbg, 7, 100 + k);  // softmax 0: epilogue
             const int u = sg.h * a.n_qp + sg.qp;
             const int first_cta = sg.ustart / a.per_cta, last_cta = (sg.uend - 1) / a.per_cta;
             const int parts = last_cta - first_cta + 1;

@@ -43,7 +43,8 @@ def watchdog():
         w = (C.c_uint32 * 16)()
         got = C.c_int32()
         lib.call("prism_debug_k4_progress", w, 16, C.byref(got))
-        print("K4 progress (loader q, loader t, mma q, mma S t, mma PV t, sm S t, sm P t, sm epi):",
+        print("K4 progress of CTA 0 (loader Q segment, loader tile, S issued by MMA warp 0 / 1, P.V issued, "
+              "softmax 0 has S, posted P, epilogue):",
               list(w)[:8], flush=True)
 
 
