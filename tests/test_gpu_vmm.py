@@ -249,3 +249,39 @@ def test_page_freed_in_its_allocating_step_is_still_mapped_for_the_kernels():
     r = subprocess.run([sys.executable, "-c", _SAME_STEP_FREE], cwd=root, env=env, capture_output=True, text=True,
                        timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_released_pool_hands_its_memory_to_the_next_pool(product):
+    """free_kvcache of a pool with mapped chunks (a model's eviction): its
+    chunks go back as cached handles and its VA range is freed. A pool
+    created right after, on a ledger too tight for both, maps all its pages
+    without creating handles past the physical budget; when it is released
+    too, every handle is cached and nothing stays mapped."""
+    cap = 32
+    dev = msim.Device(0, lib=product)
+    try:
+        K = dev.chunk_pages()
+        gpu = msim.GpuState(0, cap, lib=product)
+        gpu.ledger.attach_device(dev)
+        a = msim.alloc_kvcache(gpu.ledger, "old", 131072, 400)  # 16 tokens per page
+        held = msim.alloc_kv(a, gpu.ledger, cap * 16).handles
+        assert len({h.page for h in held}) == cap
+        dev.quiesce()
+        mapped_before = dev.stats()["total_chunks"] - dev.stats()["cached"]
+        assert mapped_before >= cap // K
+        msim.free_kv(a, gpu.ledger, held)
+        dev.reset_stats()
+        msim.free_kvcache(gpu.ledger, a)
+        b = msim.alloc_kvcache(gpu.ledger, "new", 131072, 400)
+        got = msim.alloc_kv(b, gpu.ledger, cap * 16)
+        assert got.shortfall_pages == 0
+        dev.quiesce()
+        st = dev.stats()
+        assert st["total_chunks"] * K <= cap + K, st      # nothing created past the budget
+        msim.free_kv(b, gpu.ledger, got.handles)
+        msim.free_kvcache(gpu.ledger, b)
+        dev.quiesce()  # waits for the retired ranges too
+        st = dev.stats()
+        assert st["pending"] == 0 and st["cached"] == st["total_chunks"], st
+    finally:
+        dev.close()
