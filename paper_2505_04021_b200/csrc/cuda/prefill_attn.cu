@@ -364,6 +364,40 @@ __device__ __forceinline__ Seg seg_at(const PrefillArgs& a, int g, int g_end) {
     return s;
 }
 
+// Key tile (unit-local) that global position g of segment s computes. A unit
+// cut across CTA ranges is shared by up to a few CTAs at the same time; ranked
+// by (local time t = g - x * per_cta, CTA x), its positions take the unit's
+// key tiles in ascending order, so every unit sweeps its keys from the start
+// at the rate of the CTAs on it. The units of one kv head (the Q-tile pairs)
+// then read nearby keys at any moment and each K/V tile is re-read from L2
+// within a short window, instead of the cuts scattering the readers over the
+// whole context (late 32K-key chunks: the kv heads' 134 MB of K/V do not fit
+// the 126 MB L2). Online softmax and the part merge are order-free: only the
+// causal mask needs the tile, and it takes it from here. Units inside one
+// range keep the identity order.
+// (per segment constants: the CTA is x = blockIdx.x, its local time is g - x * per_cta)
+struct UnitOrder {
+    int ustart, base, af, bl, nm, extra;  // base = x * per_cta; nm < 0: identity order
+    __device__ __forceinline__ int tile(int g) const {
+        if (nm < 0) return g - ustart;
+        const int t = g - base;
+        return max(0, t - af) + min(t, bl) + nm * t + (extra >= 0 ? extra + (t >= af ? 1 : 0) : 0);
+    }
+};
+
+__device__ __forceinline__ UnitOrder unit_order(const PrefillArgs& a, const Seg& s) {
+    const int P = a.per_cta, x = static_cast<int>(blockIdx.x);
+    const int f = s.ustart / P, l = (s.uend - 1) / P;
+    UnitOrder o;
+    o.ustart = s.ustart;
+    o.base = x * P;
+    o.af = s.ustart - f * P;  // CTA f holds local times [af, P) of the unit
+    o.bl = s.uend - l * P;    // CTA l holds [0, bl)
+    o.nm = f == l ? -1 : l - f - 1;  // CTAs whose whole range lies in the unit
+    o.extra = x > f ? min(x, l) - f - 1 : -1;  // lower CTAs at the same local time (+ f if active)
+    return o;
+}
+
 template <int D, int G>
 __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
     using S = PfShape<D>;
@@ -488,7 +522,9 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
             pend = 0;
         };
         Seg la = seg_at(a, g_begin, g_end);  // look-ahead cursor (tile g + 1)
-        std::uint64_t oa = decode(load_sid(g_begin - la.ustart, ra)), ob = decode(load_sid(g_begin - la.ustart, rb));
+        UnitOrder lo_ = unit_order(a, la);
+        const int kt0 = lo_.tile(g_begin);
+        std::uint64_t oa = decode(load_sid(kt0, ra)), ob = decode(load_sid(kt0, rb));
         int g = g_begin, s_idx = 0;
         while (g < g_end) {
             const Seg sg = seg_at(a, g, g_end);
@@ -516,9 +552,13 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 const int k = g - g_begin;
                 std::int32_t na = -1, nb = -1;
                 if (g + 1 < g_end) {
-                    if (g + 1 >= la.g1) la = seg_at(a, g + 1, g_end);
-                    na = load_sid(g + 1 - la.ustart, ra);
-                    nb = load_sid(g + 1 - la.ustart, rb);
+                    if (g + 1 >= la.g1) {
+                        la = seg_at(a, g + 1, g_end);
+                        lo_ = unit_order(a, la);
+                    }
+                    const int kt = lo_.tile(g + 1);
+                    na = load_sid(kt, ra);
+                    nb = load_sid(kt, rb);
                 }
 #pragma unroll
                 for (int kv = 0; kv < 2; ++kv) {
@@ -645,6 +685,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
         };
         while (g < g_end) {
             const Seg sg = seg_at(a, g, g_end);
+            const UnitOrder ord = unit_order(a, sg);
             const int tok = (2 * sg.qp + j) * kTQ + tq;
             const bool row_ok = r < kTQ * G && tok < a.chunk;
             const int pos = row_ok ? a.first + tok : -1;  // last key this row may attend
@@ -658,7 +699,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                     if (j == 0) k4_mark(a.dbg, 5, 100 + k);  // softmax 0: has S(k)
                 }
                 const std::uint32_t tS = tmem + lane_base + j * 2 * S::kN + b * S::kN;
-                const int k0 = (g - sg.ustart) * S::kN;
+                const int k0 = ord.tile(g) * S::kN;
                 // the tile's S row in registers (one tcgen05.ld wait), row max
                 // with 8 independent partial maxima; tiles entirely below the
                 // diagonal skip the causal mask

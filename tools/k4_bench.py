@@ -16,7 +16,7 @@ from tests import scenarios as S  # noqa: E402
 
 CHUNK = int(os.environ.get("CHUNK", 512))
 CTX = int(os.environ.get("CTX", 32768))
-REPS, LAYERS = 3, 8
+REPS, LAYERS = int(os.environ.get("REPS", 3)), 8
 root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 peaks = json.load(open(os.path.join(root, "MEASURED_PEAKS.json")))
 dev = msim.Device(0)
