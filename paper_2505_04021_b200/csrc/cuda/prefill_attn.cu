@@ -483,6 +483,9 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
         // src_bytes 0 (zero fill) reads nothing; q is a valid placeholder address
         const char* dummy = reinterpret_cast<const char*>(a.q);
         auto copy_row = [&](std::uint32_t dst_row, const std::uint32_t (&dsw)[kCpl], const char* src, bool ok) {
+#if defined(K4_EXP) && (K4_EXP & 2)  // timing experiment: no K/V copies
+            if (dst_row >= sKV) return;
+#endif
             const char* p = (ok ? src : dummy) + h * 16;
             const int bytes = ok ? 16 : 0;
 #pragma unroll
@@ -698,6 +701,13 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                     k4_stamp(a.trace, j == 0 ? 3 : 5, k);
                     if (j == 0) k4_mark(a.dbg, 5, 100 + k);  // softmax 0: has S(k)
                 }
+#if defined(K4_EXP) && (K4_EXP & 1)  // timing experiment: no softmax
+                if (true) {
+                    tc_fence_before();
+                    mb_arrive(b_pfull + 8 * (2 * j + b));
+                    continue;
+                }
+#endif
                 const std::uint32_t tS = tmem + lane_base + j * 2 * S::kN + b * S::kN;
                 const int k0 = ord.tile(g) * S::kN;
                 // the tile's S row in registers (one tcgen05.ld wait), row max
