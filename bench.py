@@ -141,10 +141,12 @@ class ClockSampler:
         if self._thread:
             self._thread.join(timeout=2.0)
 
-    def summary(self):
-        lo = self.t0 if self.t0 is not None else 0
-        hi = self.t1 if self.t1 is not None else 1 << 62
-        inside = [s for s in self.samples if lo <= s[0] <= hi]
+    def summary(self, windows=None):
+        """Clock record over [mark_start, mark_end], or over a list of
+        (t0_ns, t1_ns) windows (several timed sub-regions)."""
+        if windows is None:
+            windows = [(self.t0 if self.t0 is not None else 0, self.t1 if self.t1 is not None else 1 << 62)]
+        inside = [s for s in self.samples if any(lo <= s[0] <= hi for lo, hi in windows)]
         reasons = set()
         if inside:
             nv = self._nv
@@ -620,7 +622,7 @@ def page_map_summary(st, steps):
                 "cuMemMap": round(st["map_call_ns_total"] / 1e3 / ops, 2),
                 "cuMemCreate": round(st["create_ns_total"] / 1e3 / ops, 2),
                 "cuMemUnmap_steals": round(st["steal_ns_total"] / 1e3 / ops, 2)},
-            "steals_of_premapped": st["caller_steals_clean"],
+            "steals_of_premapped": st["caller_steals_clean"], "reserve_steals": st["reserve_steals"],
             "driver_call_us": {  # raw per-call latency, worker thread, per physical chunk
                 "map_and_access_p50": round(st["drv_map_ns_p50"] / 1e3, 1),
                 "map_and_access_p99": round(st["drv_map_ns_p99"] / 1e3, 1),
@@ -663,6 +665,8 @@ def prefill_c3(chunk=512, ctx=32768, every=8, reps=2, layers=8):
     scale = 1.0 / math.sqrt(D)
     flops = ms = 0.0
     launches = chunks = 0
+    windows, per_chunk = [], []
+    clk = ClockSampler(torch.cuda.current_device()).__enter__()
     while True:
         eng.step()
         eng.append_kv_synthetic(0, L, SEED)
@@ -672,23 +676,33 @@ def prefill_c3(chunk=512, ctx=32768, every=8, reps=2, layers=8):
         if chunks % every == every - 1 or first + n >= ctx:
             eng.prefill_attention(0, q.data_ptr(), o.data_ptr(), scale)  # warm
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t_w = time.monotonic_ns()
             s.record(stream)
             for _ in range(reps):
                 for layer in range(layers):
                     eng.prefill_attention(layer, q.data_ptr(), o.data_ptr(), scale)
             e.record(stream)
             e.synchronize()
+            windows.append((t_w, time.monotonic_ns()))
             ms += s.elapsed_time(e)
-            flops += reps * layers * 4.0 * NQ * D * sum(first + i + 1 for i in range(n))
+            f = reps * layers * 4.0 * NQ * D * sum(first + i + 1 for i in range(n))
+            flops += f
             launches += reps * layers
+            c = clk.summary(windows[-1:])
+            per_chunk.append({"first": first, "tflops": round(f / (s.elapsed_time(e) / 1e3) / 1e12, 1),
+                              "sm_mhz": c["sm_mhz"]})
         chunks += 1
         if first + n >= ctx:
             break
     torch.cuda.synchronize()
+    clk.__exit__(None, None, None)
     achieved = flops / (ms / 1e3) / 1e12
+    sustained = None
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            peak, src = float(json.load(f)["bf16_tflops"]), "measured (burst)"
+            mp = json.load(f)
+        peak, src = float(mp["bf16_tflops"]), "measured (burst)"
+        sustained = mp.get("bf16_tflops_sustained")
     except Exception:
         peak, src = 2250.0, "nominal dense bf16"
     return {"kernel": "k4_prefill (chunked-prefill paged attention, tcgen05.mma + TMEM)",
@@ -696,8 +710,10 @@ def prefill_c3(chunk=512, ctx=32768, every=8, reps=2, layers=8):
                         f"K4 timed on every {every}th chunk x {layers} layers x {reps}",
             "bound": "tensor", "achieved": round(achieved, 1), "peak": peak, "unit": "TFLOP/s",
             "frac": round(achieved / peak, 4), "peak_source": src, "launches_timed": launches,
+            "frac_of_sustained": round(achieved / sustained, 4) if sustained else None,
             "mean_ms_per_launch": round(ms / max(launches, 1), 4),
-            "flops": "causal: 4 * n_q * head_dim * sum over queries of visible keys"}
+            "flops": "causal: 4 * n_q * head_dim * sum over queries of visible keys",
+            "clocks": clk.summary(windows), "per_timed_chunk": per_chunk}
 
 
 def decode_c3(batch=16, ctx=32768, reps=3):

@@ -437,6 +437,7 @@ typedef struct {
     /* raw driver-call latency per physical chunk (worker thread, bounded sample):
      * cuMemMap + cuMemSetAccess, cuMemCreate, cuMemUnmap of a steal */
     double drv_map_ns_p50, drv_map_ns_p99, drv_create_ns_p50, drv_create_ns_p99, drv_unmap_ns_p50, drv_unmap_ns_p99;
+    uint64_t reserve_steals;    /* background steals into the handle reserve (PRISM_VMM_RESERVE_CHUNKS) */
 } prism_device_stats;
 int prism_device_stats_get(const prism_device* d, prism_device_stats* out);
 int prism_device_reset_stats(prism_device* d);

@@ -199,7 +199,7 @@ class DeviceStats(C.Structure):
                                                                  "caller_steals_clean")] + [
         ("wait_ns_total", c_double), ("urgent", c_uint64), ("total_chunks", c_uint64), ("chunk_pages", c_uint64)] + [
         (n, c_double) for n in ("drv_map_ns_p50", "drv_map_ns_p99", "drv_create_ns_p50", "drv_create_ns_p99",
-                                "drv_unmap_ns_p50", "drv_unmap_ns_p99")]
+                                "drv_unmap_ns_p50", "drv_unmap_ns_p99")] + [("reserve_steals", c_uint64)]
 
 
 class EngineDeviceOptions(C.Structure):

@@ -146,6 +146,7 @@ int prism_device_stats_get(const prism_device* d, prism_device_stats* out) {
         out->drv_create_ns_p99 = percentile(s.drv_create_ns, 0.99);
         out->drv_unmap_ns_p50 = percentile(s.drv_unmap_ns, 0.5);
         out->drv_unmap_ns_p99 = percentile(s.drv_unmap_ns, 0.99);
+        out->reserve_steals = s.reserve_steals;
     });
 }
 

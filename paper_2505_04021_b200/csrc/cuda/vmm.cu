@@ -89,6 +89,31 @@ std::chrono::steady_clock::duration premap_steal_age() {
 }
 // Idle chunks moved per steal (one cuMemUnmap over a contiguous run).
 constexpr int kStealBatch = 8;
+// ... and per steal an urgent map waits for (PRISM_VMM_URGENT_STEAL_BATCH).
+int urgent_steal_batch() {
+    static const int n = [] {
+        const char* e = std::getenv("PRISM_VMM_URGENT_STEAL_BATCH");
+        return e ? std::max(1, std::min(kStealBatch, std::atoi(e))) : kStealBatch;
+    }();
+    return n;
+}
+// Background reserve: once an urgent map had to steal (the budget is spent),
+// the worker keeps up to PRISM_VMM_RESERVE_CHUNKS unmapped handles ready by
+// stealing safe idle chunks outside every window while it has nothing else
+// to do, PRISM_VMM_RESERVE_BATCH chunks per cuMemUnmap, so the next urgent
+// maps take a cached handle instead of waiting for an unmap.
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e ? std::atoi(e) : dflt;
+}
+std::uint64_t reserve_chunks() {
+    static const std::uint64_t n = static_cast<std::uint64_t>(std::max(0, env_int("PRISM_VMM_RESERVE_CHUNKS", 8)));
+    return n;
+}
+int reserve_batch() {
+    static const int n = std::max(1, std::min(kStealBatch, env_int("PRISM_VMM_RESERVE_BATCH", 2)));
+    return n;
+}
 // How many in-window idle chunks a steal skips over looking for one outside
 // every look-ahead window (bounds the scan).
 constexpr int kStealScan = 256;
@@ -275,16 +300,21 @@ bool VmmDevice::take_handle(Lock& lk, bool urgent, std::uint64_t& h) {
             const char* e = std::getenv("PRISM_VMM_PREMAP_STEAL");
             return !(e && e[0] == '0');
         }();
-        return premap_steal && steal_for_worker(lk, h, /*premap=*/true);
+        return premap_steal && steal_for_worker(lk, h, StealMode::premap);
     }
-    if (steal_for_worker(lk, h)) return true;
+    if (reserve_chunks() > 0) reserve_wanted_ = true;  // the budget is spent: keep handles ready
+    if (steal_for_worker(lk, h, StealMode::urgent)) return true;
     // Nothing idle is safe to move (the budget shrank under queued maps, or
     // every idle chunk was released inside the open step): past the budget.
     ++stats_.over_budget;
     return create();
 }
 
-bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h, bool premap) {
+bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h, StealMode mode) {
+    // reserve: like premap (safe chunks outside every window only, no fence
+    // waits) but without the idle-age rule
+    const bool premap = mode != StealMode::urgent;
+    const bool need_age = mode == StealMode::premap;
     // Move the highest idle chunk that is safe (look-ahead and never read,
     // or released before a fence that passed), preferring chunks outside
     // every pool's look-ahead window: allocation reuses the lowest unmapped
@@ -298,7 +328,7 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h, bool premap) {
         std::uint64_t pick = 0, fallback = 0;
         int scanned = 0;
         const auto now = Clock::now();
-        const auto aged = [&](const Chunk& v) { return !premap || now - v.idle_at >= premap_steal_age(); };
+        const auto aged = [&](const Chunk& v) { return !need_age || now - v.idle_at >= premap_steal_age(); };
         for (auto it = idle_.rbegin(); it != idle_.rend(); ++it) {
             const Chunk& v = chunks_.find(*it)->second;
             if (!(v.clean || v.epoch < fenced_) || !aged(v)) continue;
@@ -321,7 +351,10 @@ bool VmmDevice::steal_for_worker(Lock& lk, std::uint64_t& h, bool premap) {
             const std::uint64_t res_lo = r == ranges_.begin() ? pick : std::prev(r)->first;
             std::uint64_t lo = pick;
             int n = 1;
-            while (n < kStealBatch && lo >= res_lo + chunk_bytes_) {
+            const int batch = mode == StealMode::premap   ? kStealBatch
+                              : mode == StealMode::reserve ? reserve_batch()
+                                                           : urgent_steal_batch();
+            while (n < batch && lo >= res_lo + chunk_bytes_) {
                 const std::uint64_t va = lo - chunk_bytes_;
                 if (!idle_.count(va)) break;
                 const Chunk& c = chunks_.find(va)->second;
@@ -543,6 +576,23 @@ void VmmDevice::worker_main() {
                 }
                 drop_if_empty(it);
                 hints_.clear();  // no free budget: wait for the next hint
+            }
+            stats_.background_ns_total += ns_since(t0);
+            --worker_busy_;
+            done_cv_.notify_all();
+            continue;
+        }
+        // 2b. background reserve of unmapped handles (PRISM_VMM_RESERVE_CHUNKS)
+        if (reserve_wanted_ && cache_.size() < reserve_chunks()) {
+            ++worker_busy_;
+            const auto t0 = Clock::now();
+            std::uint64_t h = 0;
+            if (steal_for_worker(lk, h, StealMode::reserve)) {
+                cache_.push_back(h);  // the steal counted it in mapped_
+                --mapped_;
+                ++stats_.reserve_steals;
+            } else {
+                reserve_wanted_ = false;  // nothing safe to move: wait for the next urgent steal
             }
             stats_.background_ns_total += ns_since(t0);
             --worker_busy_;

@@ -68,6 +68,7 @@ struct VmmStats {
     std::uint64_t premaps = 0;        // chunks mapped by the look-ahead
     std::uint64_t urgent = 0;         // chunks mapped on demand
     std::uint64_t caller_steals_clean = 0;  // steals that took a look-ahead chunk
+    std::uint64_t reserve_steals = 0;  // background steals into the handle reserve (PRISM_VMM_RESERVE_CHUNKS)
     double map_ns_total = 0.0;        // caller-thread time in logical maps, incl. waits for the worker
     double unmap_ns_total = 0.0;      // caller-thread time in logical unmaps + reclaims
     double steal_ns_total = 0.0;      // cuMemUnmap time of steals (worker)
@@ -183,7 +184,8 @@ private:
     // worker
     void worker_main();
     bool take_handle(Lock& lk, bool urgent, std::uint64_t& h);
-    bool steal_for_worker(Lock& lk, std::uint64_t& h, bool premap = false);
+    enum class StealMode { urgent, premap, reserve };
+    bool steal_for_worker(Lock& lk, std::uint64_t& h, StealMode mode);
     bool map_chunk(Lock& lk, std::uint64_t va, std::uint64_t h, bool urgent);
     void trace(char kind, std::uint32_t n, Clock::time_point t0, double ns);
     void dump_trace() const;
@@ -211,6 +213,7 @@ private:
     std::uint64_t cache_target_ = 0;   // chunks
     std::uint64_t reserve_pending_ = 0; // chunks still to create for reserve_physical() (one-shot)
     std::uint64_t worker_busy_ = 0;
+    bool reserve_wanted_ = false;      // an urgent map stole: keep reserve_chunks() handles cached
     bool stop_ = false;
     std::string failed_;  // first driver error on the worker (reported to callers)
     std::thread worker_;

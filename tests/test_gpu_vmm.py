@@ -285,3 +285,46 @@ def test_released_pool_hands_its_memory_to_the_next_pool(product):
         assert st["pending"] == 0 and st["cached"] == st["total_chunks"], st
     finally:
         dev.close()
+
+
+def test_background_reserve_steals_keep_data_and_budget(product, device):
+    """Once an urgent map had to steal (budget spent), the worker keeps up to
+    PRISM_VMM_RESERVE_CHUNKS (default 8) unmapped handles ready by stealing
+    safe idle chunks in the background; the next urgent maps take those
+    handles. Attention stays exact and the physical budget holds."""
+    cap = 96
+    K = device.chunk_pages()
+    gpu = msim.GpuState(0, cap, lib=product)
+    gpu.ledger.attach_device(device)
+    device.reclaim(True)
+    device.reset_stats()
+    engines = []
+    for mid in ("r0", "r1", "r2"):
+        spec = S.shape_spec("llama3.1-8b", mid, chunk=256, weight_scale=0.0)
+        act = gpu.activate(spec)
+        gpu.finish_activation(act.engine_index)
+        e = gpu.engine(act.engine_index)
+        e.attach_device()
+        engines.append((e, spec))
+    rid = 0
+    budget_chunks = -(-cap // K) + len(engines)
+    for rnd in range(9):
+        e, spec = engines[rnd % 3]
+        for _ in range(4):
+            rid += 1
+            e.push(rid, 300 + 11 * rnd, 16)
+        steps = 0
+        while sum(e.counts()) and steps < 600:
+            e.step()
+            e.append_kv_synthetic(0, spec.n_layers, SEED)
+            steps += 1
+            if steps % 6 == 0:
+                _attn_ok(e, spec)
+        assert sum(e.counts()) == 0
+        assert gpu.ledger.mapped_pages() == 0
+        assert device.stats()["total_chunks"] <= budget_chunks
+    device.quiesce()
+    st = device.stats()
+    assert st["steals"] > 0, st
+    assert st["reserve_steals"] > 0, st
+    assert st["over_budget"] == 0, st

@@ -12,9 +12,12 @@ def main():
     reps = int(os.environ.get("REPS", "3"))
     for i in range(reps):
         r = bench.page_churn_c2()
-        print(json.dumps({"rep": i, "amortised_us_per_page_op": r["amortised_us_per_page_op"],
-                          "breakdown": r["breakdown_us_per_page_op"], "driver_unmaps": r["driver_unmaps"],
-                          "access_calls": r["access_calls"], "wall_s": r["wall_s"]}), flush=True)
+        keys = ("amortised_us_per_page_op", "caller_wait_us_per_page_op", "background_us_per_page_op",
+                "breakdown_us_per_page_op", "urgent_chunks", "steals", "reserve_steals", "driver_unmaps", "driver_creates",
+                "access_calls", "driver_call_us", "wall_s")
+        print(json.dumps({"rep": i, "urgent_steal_batch": os.environ.get("PRISM_VMM_URGENT_STEAL_BATCH", "8"),
+                          "reserve_chunks": os.environ.get("PRISM_VMM_RESERVE_CHUNKS", "8"),
+                          **{k: r[k] for k in keys if k in r}}), flush=True)
 
 
 if __name__ == "__main__":
