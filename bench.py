@@ -1102,12 +1102,6 @@ def main():
         dist.init_process_group(backend, **kw)
     res = gpu_arm(args, rank, world)
     if rank == 0:
-        if world == 1 and not args.no_cpu_baseline:
-            try:
-                # a bounded sample of the reference arm: 3 full C1 steps after 1 warm-up step
-                res["cpu_baseline"] = reference_arm(argparse.Namespace(gpus=1, steps=3, warmup=1))["cpu_baseline"]
-            except Exception as e:  # reported, never substituted for the GPU number
-                res["cpu_baseline"] = {"error": str(e)}
         if world == 1 and not args.no_churn:
             try:
                 res["page_map_c2"] = page_churn_c2_median()
@@ -1146,6 +1140,15 @@ def main():
                 res["serving"] = serving_gpu()
             except Exception as e:
                 res["serving"] = {"error": str(e)}
+        if world == 1 and not args.no_cpu_baseline:
+            # last, so its host work cannot disturb the GPU measurements: the
+            # C2 churn run right after it was the slowest of three on two
+            # boxes (179 / 72 us vs 16-44; the VMM driver calls are host code)
+            try:
+                # a bounded sample of the reference arm: 3 full C1 steps after 1 warm-up step
+                res["cpu_baseline"] = reference_arm(argparse.Namespace(gpus=1, steps=3, warmup=1))["cpu_baseline"]
+            except Exception as e:  # reported, never substituted for the GPU number
+                res["cpu_baseline"] = {"error": str(e)}
         if world == 1 and isinstance(res.get("serving"), dict) and "c2" in res["serving"]:
             # the same C2 page churn served by the two-level scheduler with all
             # kernels (K1/K2/K4/K3 every iteration): the maps' driver calls then

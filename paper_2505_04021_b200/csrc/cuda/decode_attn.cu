@@ -382,7 +382,7 @@ void launch_decode_attention(EngineDeviceImpl& d, int layer, const void* q, void
         launch_k3_streamk(d, a, n_dec);
         return;
     }
-    d.k3_chain = false;
+    d.k3_chain = d.k4_chain = false;
     int max_ctx = 0;
     std::int64_t sum_ctx = 0;
     for (int i = 0; i < n_dec; ++i) {

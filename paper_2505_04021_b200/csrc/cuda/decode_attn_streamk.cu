@@ -699,6 +699,7 @@ void launch_k3_streamk_t(Ctx& d, AttnArgs a, int n_dec) {
         launch_sk_d<64>(d.group, s, d.stream, sms, chained);
     }
     d.k3_chain = true;
+    d.k4_chain = false;
 }
 
 void launch_k3_streamk(EngineDeviceImpl& d, AttnArgs a, int n_dec) { launch_k3_streamk_t(d, a, n_dec); }

@@ -160,6 +160,9 @@ public:
     // stream-K K3 launch (no K1 / K2 / upload / other kernel since): the next
     // K3 may then be launched as a programmatic dependent (PDL) of it.
     bool k3_chain = false;
+    // the same for a K4 launch after this engine's own K4 (PDL chain of
+    // consecutive prefill-attention layers)
+    bool k4_chain = false;
     // K4: key-tile prefix over the Q-tile pairs of the last (first, chunk)
     Staging<std::int32_t> pf_prefix;
     int pf_first = -1, pf_chunk = -1, pf_per_head = 0;
@@ -212,6 +215,9 @@ struct PagedCtx final : PagedOp {
     int sk_total = 0, sk_per_cta = 1, sk_max_parts = 1;
     std::uint64_t sk_launches = 0;  // selects the CTA range counter (alternate launches)
     bool k3_chain = false;
+    // the same for a K4 launch after this engine's own K4 (PDL chain of
+    // consecutive prefill-attention layers)
+    bool k4_chain = false;
     // K4: key-tile prefix over the Q-tile pairs of the last (first, chunk)
     Staging<std::int32_t> pf_prefix;
     int pf_first = -1, pf_chunk = -1, pf_per_head = 0;

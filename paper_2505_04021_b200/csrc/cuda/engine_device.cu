@@ -137,7 +137,7 @@ void EngineDeviceImpl::grow_table(std::int64_t need) {
 }
 
 void EngineDeviceImpl::begin_step(me::Engine&) {
-    k3_chain = false;
+    k3_chain = k4_chain = false;
     // Pages unmapped during earlier steps become reclaimable once the fence
     // recorded here (after every kernel the caller issued for those steps)
     // has passed; see VmmDevice.
@@ -150,7 +150,7 @@ void EngineDeviceImpl::end_step(me::Engine&, const me::IterationOutcome& out, co
                                 std::int32_t prefill_tokens) {
     vmm->defer_access(false);  // pages must be accessible before K2/K3 run
     ++step_serial;
-    k3_chain = false;
+    k3_chain = k4_chain = false;
     // K1: replay this step's allocations / frees on the device slot state.
     const std::int64_t n = pool->mirror->replay(*pool, table, step_slots, opts.max_step_tokens, stream);
     step_tokens = static_cast<int>(n);
@@ -195,7 +195,7 @@ void EngineDeviceImpl::end_step(me::Engine&, const me::IterationOutcome& out, co
 
 float* EngineDeviceImpl::attn_workspace(std::size_t floats) {
     if (floats > workspace_floats) {
-        k3_chain = false;
+        k3_chain = k4_chain = false;
         if (workspace) {
             PRISM_CUDA(cudaStreamSynchronize(stream));
             PRISM_CUDA(cudaFree(workspace));
@@ -208,7 +208,7 @@ float* EngineDeviceImpl::attn_workspace(std::size_t floats) {
 
 int* EngineDeviceImpl::attn_counters(std::size_t n) {
     if (n > counters_n) {
-        k3_chain = false;
+        k3_chain = k4_chain = false;
         if (counters) {
             PRISM_CUDA(cudaStreamSynchronize(stream));
             PRISM_CUDA(cudaFree(counters));

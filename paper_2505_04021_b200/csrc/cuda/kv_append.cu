@@ -91,7 +91,7 @@ void launch_append(EngineDeviceImpl& d, int layer_begin, int layer_end, const vo
         throw std::runtime_error("append_step_kv: bad layer range");
     }
     if (d.step_tokens == 0) return;
-    d.k3_chain = false;
+    d.k3_chain = d.k4_chain = false;
     AppendArgs a{d.geom,  d.step_slots, d.token_meta.dev, static_cast<const uint4*>(k), static_cast<const uint4*>(v),
                  layer_begin, layer_end - layer_begin, d.step_tokens, seed};
     const std::uint64_t work =
@@ -120,7 +120,7 @@ void append_step_kv_synthetic(msim::engine::Engine& eng, int layer_begin, int la
 void synth_decode_q(msim::engine::Engine& eng, int layer, std::uint64_t seed, float q_scale, void* q) {
     EngineDeviceImpl& d = impl_of(eng);
     if (d.step_decodes == 0) return;
-    d.k3_chain = false;
+    d.k3_chain = d.k4_chain = false;
     const std::uint64_t work = static_cast<std::uint64_t>(d.step_decodes) * d.n_q * d.head_dim;
     k_synth_q<<<grid_for(work, 256), 256, 0, d.stream>>>(d.decode_desc.dev, d.step_decodes, d.n_q, d.head_dim, layer,
                                                           seed, q_scale, static_cast<__nv_bfloat16*>(q));
@@ -143,7 +143,7 @@ void PagedCtx::kv_append(int layer_begin, int layer_end, const std::int32_t* slo
         for (std::size_t i = 0; i < token_meta.cap; ++i) token_meta.host[i] = TokenMeta{0, 0, 0};  // all live
         token_meta.upload(token_meta.cap, stream);
     }
-    k3_chain = false;
+    k3_chain = k4_chain = false;
     AppendArgs a{geom, slots, token_meta.dev, static_cast<const uint4*>(k), static_cast<const uint4*>(v),
                  layer_begin, layer_end - layer_begin, n_tok, 0};
     const std::uint64_t work = static_cast<std::uint64_t>(n_tok) * n_kv * (head_dim / 8) * 2 * (layer_end - layer_begin);

@@ -49,7 +49,7 @@ PagedCtx::~PagedCtx() {
 
 float* PagedCtx::attn_workspace(std::size_t floats) {
     if (floats > workspace_floats) {
-        k3_chain = false;
+        k3_chain = k4_chain = false;
         if (workspace) {
             PRISM_CUDA(cudaStreamSynchronize(stream));
             PRISM_CUDA(cudaFree(workspace));
@@ -62,7 +62,7 @@ float* PagedCtx::attn_workspace(std::size_t floats) {
 
 int* PagedCtx::attn_counters(std::size_t n) {
     if (n > counters_n) {
-        k3_chain = false;
+        k3_chain = k4_chain = false;
         if (counters) {
             PRISM_CUDA(cudaStreamSynchronize(stream));
             PRISM_CUDA(cudaFree(counters));
@@ -88,7 +88,7 @@ void PagedCtx::decode_attention(int layer, const std::int32_t* offsets, int n_se
         if (ctx <= 0) throw std::invalid_argument("paged decode_attention: every sequence needs >= 1 token");
         decode_desc.host[b] = DecodeDesc{offsets[b], ctx, 0, static_cast<std::uint64_t>(b)};
     }
-    k3_chain = false;  // the descriptor upload precedes this launch
+    k3_chain = k4_chain = false;  // the descriptor upload precedes this launch
     decode_desc.upload(static_cast<std::size_t>(n_seqs), stream);
     ++step_serial;  // new block tables every call: rebuild the stream-K tile prefix
     AttnArgs a{};

@@ -450,6 +450,12 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
     __syncthreads();
     tc_fence_after();
     const std::uint32_t tmem = *tmem_slot;
+    // PDL (a chained launch of consecutive layers): the next K4 may launch
+    // once every CTA of this one runs; its CTAs take the SMs this launch's
+    // CTAs free and read q / K / V (never written by K4) at once. Global
+    // writes (out, partials, tickets — the workspace and tickets are shared
+    // by consecutive launches) wait for this launch's completion.
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     // K half of local tile k is ring half 2k, its V half 2k + 1
     auto half_slot = [](int idx) { return idx % S::kHalves; };
     auto half_phase = [](int idx) { return static_cast<std::uint32_t>((idx / S::kHalves) & 1); };
@@ -676,6 +682,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
         const int tq = r / G;
         const int row = j * S::kM + r;  // row of the unit (partials)
         int k = 0, g = g_begin;
+        bool pdl_waited = false;
         // PV_j(k) completes phase k >> 1 of pv_done[j][k & 1]. Whenever this
         // warpgroup waits for PV_j(k) (k = its current tile - 1 or its last
         // tile), PV_j(k-2) is complete (it was issued before S_j(k), and MMAs
@@ -786,6 +793,10 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
             // ---- epilogue of the unit segment: O_j complete after PV_j(last)
             wait_pv(k - 1);
             if (j == 0 && r == 0) k4_mark(a.dbg, 7, 100 + k);  // softmax 0: epilogue
+            if (!pdl_waited) {  // first global write of this thread (see launch_dependents)
+                asm volatile("griddepcontrol.wait;\n" ::: "memory");
+                pdl_waited = true;
+            }
             const int u = sg.h * a.n_qp + sg.qp;
             const int first_cta = sg.ustart / a.per_cta, last_cta = (sg.uend - 1) / a.per_cta;
             const int parts = last_cta - first_cta + 1;
@@ -901,28 +912,41 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
 }
 
 template <int D, int G>
-void launch_pf(const PrefillArgs& a, int grid, cudaStream_t stream) {
+void launch_pf(const PrefillArgs& a, int grid, cudaStream_t stream, bool chained) {
     using S = PfShape<D>;
     static bool init = false;
     if (!init) {
         PRISM_CUDA(cudaFuncSetAttribute(k4_prefill<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, S::kSmem));
         init = true;
     }
-    k4_prefill<D, G><<<grid, S::kThreads, S::kSmem, stream>>>(a);
+    // chained: a programmatic dependent of the previous K4 launch on this
+    // stream (its CTAs start on the SMs the previous launch's CTAs free, and
+    // wait for it only before their first global write)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(S::kThreads);
+    cfg.dynamicSmemBytes = S::kSmem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = chained ? 1 : 0;
+    PRISM_CUDA(cudaLaunchKernelEx(&cfg, k4_prefill<D, G>, a));
     PRISM_CUDA(cudaGetLastError());
 }
 
 template <int D>
-void launch_pf_d(int group, const PrefillArgs& a, int grid, cudaStream_t stream) {
+void launch_pf_d(int group, const PrefillArgs& a, int grid, cudaStream_t stream, bool chained) {
     switch (group) {
-        case 1: launch_pf<D, 1>(a, grid, stream); break;
-        case 2: launch_pf<D, 2>(a, grid, stream); break;
-        case 3: launch_pf<D, 3>(a, grid, stream); break;
-        case 4: launch_pf<D, 4>(a, grid, stream); break;
-        case 5: launch_pf<D, 5>(a, grid, stream); break;
-        case 6: launch_pf<D, 6>(a, grid, stream); break;
-        case 7: launch_pf<D, 7>(a, grid, stream); break;
-        case 8: launch_pf<D, 8>(a, grid, stream); break;
+        case 1: launch_pf<D, 1>(a, grid, stream, chained); break;
+        case 2: launch_pf<D, 2>(a, grid, stream, chained); break;
+        case 3: launch_pf<D, 3>(a, grid, stream, chained); break;
+        case 4: launch_pf<D, 4>(a, grid, stream, chained); break;
+        case 5: launch_pf<D, 5>(a, grid, stream, chained); break;
+        case 6: launch_pf<D, 6>(a, grid, stream, chained); break;
+        case 7: launch_pf<D, 7>(a, grid, stream, chained); break;
+        case 8: launch_pf<D, 8>(a, grid, stream, chained); break;
         default: throw std::runtime_error("prefill_attention: unsupported GQA group");
     }
 }
@@ -986,9 +1010,16 @@ void launch_k4(Ctx& d, PrefillArgs a) {
         if (const char* e = std::getenv("PRISM_K4_SMS")) n = std::max(1, std::min(n, std::atoi(e)));  // experiments
         return n;
     }();
+    // PDL only behind this engine's own K4 (PRISM_K4_PDL=0 disables)
+    static const bool pdl = [] {
+        const char* e = std::getenv("PRISM_K4_PDL");
+        return !(e && e[0] == '0');
+    }();
+    bool chained = pdl && d.k4_chain;
     const int tq = 128 / d.group;
     const int n_qp = ((a.chunk + tq - 1) / tq + 1) / 2;
     if (d.pf_first != a.first || d.pf_chunk != a.chunk) {
+        chained = false;  // the prefix upload below precedes this launch
         d.pf_prefix.ensure(static_cast<std::size_t>(n_qp) + 1);
         std::int32_t acc = 0;
         for (int qp = 0; qp < n_qp; ++qp) {
@@ -1016,12 +1047,14 @@ void launch_k4(Ctx& d, PrefillArgs a) {
     a.tickets = d.attn_counters(static_cast<std::size_t>(d.n_kv) * n_qp);
     a.dbg = k4_debug_words();
     a.trace = k4_trace_buf();
-    d.k3_chain = false;
+    chained = chained && d.k4_chain;  // a workspace / counter reallocation breaks the chain
     if (d.head_dim == 128) {
-        launch_pf_d<128>(d.group, a, grid, d.stream);
+        launch_pf_d<128>(d.group, a, grid, d.stream, chained);
     } else {
-        launch_pf_d<64>(d.group, a, grid, d.stream);
+        launch_pf_d<64>(d.group, a, grid, d.stream, chained);
     }
+    d.k3_chain = false;
+    d.k4_chain = true;
 }
 
 void launch_prefill_attention(EngineDeviceImpl& d, int layer, const void* q, void* out, float scale) {

@@ -93,3 +93,61 @@ def test_prefill_long_prefix_rescale(product, device):
     the lazy O rescale in TMEM."""
     n = _run_prefills(product, device, "llama3.1-8b", [2600], chunk=512, q_scale=8.0, layer=30, samples=24)
     assert n > 50
+
+
+@pytest.mark.parametrize("shape", ["qwen2.5-1.5b", "llama3.1-8b"])
+def test_prefill_chained_layers_write_in_order(product, device, shape):
+    """Consecutive K4 launches of an engine form a programmatic-dependent
+    chain: a launch's CTAs start on the SMs its predecessor frees and read
+    q / K / V at once; only their writes (out, partials, tickets — shared by
+    the chain) wait. Back-to-back launches with no synchronisation: (a) every
+    layer into its own out buffer, each equal to its layer's oracle; (b)
+    every layer into ONE shared buffer, repeated, which must end with the
+    last layer's result (write-after-write order across the chain)."""
+    gpu, spec, eng = _engine(product, device, shape, chunk=512)
+    L, nkv, nq, d = spec.n_layers, spec.n_kv_heads, spec.n_q_heads, spec.head_dim
+    eng.push(1, 1400, 2)
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    rng = random.Random(7)
+    scale = 1 / math.sqrt(d)
+    ks, vs = [], []  # per step: [L][tok][nkv][d] (CPU bf16), request 1 only
+    tested = 0
+    while sum(eng.counts()) and tested < 2:
+        eng.step()
+        n_tok, _ = eng.step_info()
+        if n_tok == 0:
+            continue
+        k = (torch.rand((L, n_tok, nkv, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+        v = (torch.rand((L, n_tok, nkv, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+        eng.append_kv(0, L, k.data_ptr(), v.data_ptr())
+        n_pf, first, _ = eng.prefill_info()
+        if not n_pf:
+            continue
+        # one request: the step's rows are its chunk (+ its first output
+        # token's slot on the last chunk), in token order
+        ks.append(k.cpu())
+        vs.append(v.cpu())
+        if first == 0:
+            continue  # test chunks with a prefix (several key tiles, cut units)
+        q = ((torch.rand((L, n_pf, nq, d), generator=gen, device="cuda") * 2 - 1) * 2.0).to(torch.bfloat16)
+        outs = torch.full_like(q, float("nan"))
+        shared = torch.full_like(q[0], float("nan"))
+        for layer in range(L):  # (a)
+            eng.prefill_attention(layer, q[layer].data_ptr(), outs[layer].data_ptr(), scale)
+        for _ in range(3):  # (b)
+            for layer in range(L):
+                eng.prefill_attention(layer, q[layer].data_ptr(), shared.data_ptr(), scale)
+        eng.synchronize()
+        assert not torch.isnan(outs.float()).any(), "a chained K4 left output rows unwritten"
+        kk, vv = torch.cat(ks, dim=1), torch.cat(vs, dim=1)  # [L][ctx][nkv][d]
+        qc, oc, sc = q.cpu(), outs.float().cpu().numpy(), shared.float().cpu().numpy()
+        for layer in (0, L // 2, L - 1):
+            for i in sorted({0, n_pf - 1, *[rng.randrange(n_pf) for _ in range(6)]}):
+                p = first + i
+                ref = oracle.dense_attention(_bits(qc[layer, i]), _bits(kk[layer, :p + 1]), _bits(vv[layer, :p + 1]),
+                                             scale)
+                _close(oc[layer, i], ref)
+                if layer == L - 1:
+                    _close(sc[i], ref)
+        tested += 1
+    assert tested == 2
