@@ -72,6 +72,7 @@ struct PrefillArgs {
     int chunk;                // query tokens
     float scale_log2;
     float rescale_thr;        // lazy-rescale threshold (log2 units; 8)
+    int merge_fast;           // 1: merges of <= 4 parts issue all their loads at once (PRISM_K4_MERGE)
     int n_qp;                 // Q-tile pairs per kv head
     const std::int32_t* qp_tiles;  // [n_qp + 1] key-tile prefix over the pairs (same for every kv head)
     int per_cta;              // key tiles per CTA range
@@ -397,6 +398,8 @@ __device__ __forceinline__ UnitOrder unit_order(const PrefillArgs& a, const Seg&
     o.extra = x > f ? min(x, l) - f - 1 : -1;  // lower CTAs at the same local time (+ f if active)
     return o;
 }
+
+constexpr int kFastParts = 4;  // merges with at most this many parts take the latency-parallel path
 
 template <int D, int G>
 __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
@@ -854,7 +857,68 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                     *merge_flag = last;
                 }
                 asm volatile("bar.sync 1, 256;\n" ::: "memory");
-                if (*merge_flag) {
+                if (*merge_flag && a.merge_fast && parts <= kFastParts) {
+                    __threadfence();
+                    // Latency-parallel combination (the usual case: a unit
+                    // cut into 2-4 parts): every part's (m, l) in one round of
+                    // loads, then per 32-column group all parts' O rows at
+                    // once — 1 + D / 32 dependent L2 round trips instead of
+                    // (2 + D / 32) x parts.
+                    auto slot_of = [&](int cta) { return 2 * cta + (cta * a.per_cta >= sg.ustart ? 0 : 1); };
+                    int sl[kFastParts];
+                    float2 ml[kFastParts];
+#pragma unroll
+                    for (int t = 0; t < kFastParts; ++t) {
+                        sl[t] = slot_of(min(first_cta + t, last_cta));
+                        if (t < parts) ml[t] = __ldcg(a.part_ml + static_cast<std::size_t>(sl[t]) * 256 + row);
+                    }
+                    float mm = -INFINITY;
+#pragma unroll
+                    for (int t = 0; t < kFastParts; ++t)
+                        if (t < parts) mm = fmaxf(mm, ml[t].x);
+                    float ll = 0.f;
+#pragma unroll
+                    for (int t = 0; t < kFastParts; ++t)
+                        if (t < parts) ll += ml[t].x == -INFINITY ? 0.f : ml[t].y * fast_exp2(ml[t].x - mm);
+                    const float inv = ll > 0.f ? 1.f / ll : 0.f;
+                    float wt[kFastParts];
+#pragma unroll
+                    for (int t = 0; t < kFastParts; ++t)
+                        wt[t] = (t < parts && ml[t].x != -INFINITY) ? fast_exp2(ml[t].x - mm) * ml[t].y * inv : 0.f;
+#pragma unroll 1
+                    for (int cg = 0; cg < D / 32; ++cg) {
+                        uint2 h[kFastParts][8];
+#pragma unroll
+                        for (int t = 0; t < kFastParts; ++t)
+#pragma unroll
+                            for (int q = 0; q < 8; ++q)
+                                h[t][q] = t < parts ? __ldcg(a.part_o + (static_cast<std::size_t>(sl[t]) * (D / 4) +
+                                                                         cg * 8 + q) * 256 + row)
+                                                    : make_uint2(0u, 0u);
+                        float4 acc[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                            for (int t = 0; t < kFastParts; ++t) {
+                                const float2 lo = unpack_f16(h[t][q].x), hi = unpack_f16(h[t][q].y);
+                                acc[q].x += wt[t] * lo.x;
+                                acc[q].y += wt[t] * lo.y;
+                                acc[q].z += wt[t] * hi.x;
+                                acc[q].w += wt[t] * hi.y;
+                            }
+                        }
+                        if (row_ok) {
+#pragma unroll
+                            for (int q = 0; q < 8; q += 2) {
+                                *reinterpret_cast<uint4*>(dst + cg * 32 + 4 * q) =
+                                    make_uint4(pack_bf16(acc[q].x, acc[q].y), pack_bf16(acc[q].z, acc[q].w),
+                                               pack_bf16(acc[q + 1].x, acc[q + 1].y),
+                                               pack_bf16(acc[q + 1].z, acc[q + 1].w));
+                            }
+                        }
+                    }
+                } else if (*merge_flag) {
                     __threadfence();
                     // online combination of the parts' (m, l, O) rows
                     auto slot_of = [&](int cta) { return 2 * cta + (cta * a.per_cta >= sg.ustart ? 0 : 1); };
@@ -1057,6 +1121,14 @@ void launch_k4(Ctx& d, PrefillArgs a) {
     d.k4_chain = true;
 }
 
+int k4_merge_fast() {  // PRISM_K4_MERGE=0: the per-part merge loop only (A/B)
+    static const int v = [] {
+        const char* e = std::getenv("PRISM_K4_MERGE");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return v;
+}
+
 void launch_prefill_attention(EngineDeviceImpl& d, int layer, const void* q, void* out, float scale) {
     if (layer < 0 || layer >= d.n_layers) throw std::runtime_error("prefill_attention: bad layer");
     if (d.prefill_chunk <= 0) return;
@@ -1075,6 +1147,7 @@ void launch_prefill_attention(EngineDeviceImpl& d, int layer, const void* q, voi
         return e ? static_cast<float>(std::atof(e)) : 8.f;
     }();
     a.rescale_thr = thr;
+    a.merge_fast = k4_merge_fast();
     launch_k4(d, a);
 }
 
@@ -1099,6 +1172,7 @@ void PagedCtx::prefill_attention(int layer, const std::int32_t* slot_ids, int fi
     a.chunk = n_tokens;
     a.scale_log2 = scale * 1.4426950408889634f;
     a.rescale_thr = 8.f;
+    a.merge_fast = k4_merge_fast();
     launch_k4(*this, a);
 }
 
