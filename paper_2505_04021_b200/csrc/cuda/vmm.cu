@@ -681,6 +681,7 @@ void VmmDevice::quiesce() {
     done_cv_.wait(lk, [&] {
         return !failed_.empty() ||
                (worker_busy_ == 0 && urgent_.empty() && hints_.empty() &&
+                !(reserve_wanted_ && cache_.size() < reserve_chunks()) &&
                 !((cache_.size() < cache_target_ || reserve_pending_ > 0) && total_locked() < budget_chunks()));
     });
     check_failed();
