@@ -73,3 +73,69 @@ def test_two_streams_concurrent_streamk(product):
     finally:
         d1.close()
         d2.close()
+
+
+def _bits(t):
+    return t.contiguous().view(torch.int16).numpy().view(np.uint16)
+
+
+def test_two_streams_concurrent_prefill_chains(product):
+    """K4 programmatic-dependent chains on two streams at once (two
+    VmmDevice instances on one GPU), interleaved launch by launch: each
+    launch is sized for the whole GPU and its CTAs start on SMs as they free
+    up, waiting for their own stream's previous launch only at their first
+    global write. Sampled query tokens of both chains match the fp64
+    oracle."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    d1, d2 = msim.Device(0, lib=product), msim.Device(0, lib=product)
+    L, nq, nkv, d = 32, 28, 4, 128
+    check = (1, L - 1)
+    try:
+        runs = []
+        for dev, name, prompt, seed in ((d1, "p1", 1700, 11), (d2, "p2", 1300, 12)):
+            gpu = msim.GpuState(0, 4000, lib=product)
+            gpu.ledger.attach_device(dev)
+            spec = msim.ModelSpec.llm(name, L, nq, nkv, d, chunk_size=512)
+            act = gpu.activate(spec)
+            gpu.finish_activation(act.engine_index)
+            eng = gpu.engine(act.engine_index)
+            eng.attach_device()
+            eng.push(1, prompt, 2)
+            gen = torch.Generator(device="cuda").manual_seed(seed)
+            ks, vs = [], []
+            with torch.cuda.stream(torch.cuda.ExternalStream(dev.stream())):
+                while True:  # prefill up to the last chunk (a prefix of 1-3 chunks)
+                    eng.step()
+                    n_tok, _ = eng.step_info()
+                    k = (torch.rand((L, n_tok, nkv, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+                    v = (torch.rand((L, n_tok, nkv, d), generator=gen, device="cuda") * 2 - 1).to(torch.bfloat16)
+                    eng.append_kv(0, L, k.data_ptr(), v.data_ptr())
+                    ks.append(k[list(check)].cpu())
+                    vs.append(v[list(check)].cpu())
+                    n_pf, first, _ = eng.prefill_info()
+                    if first + n_pf >= prompt:
+                        break
+                q = ((torch.rand((L, n_pf, nq, d), generator=gen, device="cuda") * 2 - 1) * 2.0).to(torch.bfloat16)
+                o = torch.full_like(q, float("nan"))
+            dev.synchronize()
+            runs.append((gpu, eng, q, o, first, n_pf, torch.cat(ks, dim=1), torch.cat(vs, dim=1)))
+        scale = 1 / math.sqrt(d)
+        for rep in range(3):
+            for layer in range(L):  # interleaved: the two chains overlap on the GPU
+                for _, eng, q, o, *_ in runs:
+                    eng.prefill_attention(layer, q[layer].data_ptr(), o[layer].data_ptr(), scale)
+        d1.synchronize()
+        d2.synchronize()
+        for _, eng, q, o, first, n_pf, kk, vv in runs:
+            assert not torch.isnan(o.float()).any()
+            qc, oc = q.cpu(), o.float().cpu().numpy()
+            for ci, layer in enumerate(check):
+                for i in (0, 7, n_pf // 2, n_pf - 1):
+                    p = first + i
+                    ref = oracle.dense_attention(_bits(qc[layer, i]), _bits(kk[ci, :p + 1]), _bits(vv[ci, :p + 1]), scale)
+                    _close(oc[layer, i], ref)
+        del runs
+    finally:
+        d1.close()
+        d2.close()
