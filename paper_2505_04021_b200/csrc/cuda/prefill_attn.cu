@@ -73,6 +73,8 @@ struct PrefillArgs {
     float scale_log2;
     float rescale_thr;        // lazy-rescale threshold (log2 units; 8)
     int merge_fast;           // 1: merges of <= 4 parts issue all their loads at once (PRISM_K4_MERGE)
+    int perm;                 // 1: CTA b takes range b / 2 (even b) or ceil(grid / 2) + b / 2 (odd b) (PRISM_K4_PERM)
+    int tab_smem;             // 1: the pair prefix is read from a shared-memory copy when it fits (PRISM_K4_TAB=0: global)
     int n_qp;                 // Q-tile pairs per kv head
     const std::int32_t* qp_tiles;  // [n_qp + 1] key-tile prefix over the pairs (same for every kv head)
     int per_cta;              // key tiles per CTA range
@@ -80,18 +82,30 @@ struct PrefillArgs {
     uint2* part_o;            // [2 * grid][D / 4][256] O / l of cut units, fp16 x 4
     float2* part_ml;          // [2 * grid][256] (m, l) of cut units
     int* tickets;             // [n_kv * n_qp], zero between launches
-    unsigned long long* trace;  // PRISM_K4_TRACE: [8][1024] globaltimer stamps of CTA 0, else null
+    unsigned long long* trace;  // PRISM_K4_TRACE: [13][1024] globaltimer stamps of one CTA, else null
+    int trace_cta;            // the traced CTA (PRISM_K4_TRACE_CTA, default 0)
+    unsigned long long* cta_trace;  // PRISM_K4_CTA_TRACE: [grid][4] stamps of this launch, else null
     unsigned* dbg;            // PRISM_K4_DEBUG: host-mapped progress words (CTA 0 only), else null
 };
 
 // timeline stamp (no-op unless PRISM_K4_TRACE): role 0 loader issued tile t,
 // 1 S(t) issued (both Q tiles), 2 / 7 P0(t)·V(t) / P1(t)·V(t) issued,
 // 3 / 5 warpgroup 0 / 1 has S(t), 4 / 6 it posted P(t)
-__device__ __forceinline__ void k4_stamp(unsigned long long* tr, int role, int t) {
-    if (tr && blockIdx.x == 0 && t < 1024) {
+__device__ __forceinline__ void k4_stamp(unsigned long long* tr, int cta, int role, int t) {
+    if (tr && static_cast<int>(blockIdx.x) == cta && t < 1024) {
         unsigned long long ns;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
         tr[role * 1024 + t] = ns;
+    }
+}
+
+// per-CTA launch timeline (no-op unless PRISM_K4_CTA_TRACE): 0 CTA start,
+// 1 the SM id, 2 first-write PDL wait returned (softmax thread 0), 3 CTA end
+__device__ __forceinline__ void k4_cta_stamp(unsigned long long* tr, int k) {
+    if (tr) {
+        unsigned long long ns;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+        tr[blockIdx.x * 4 + k] = ns;
     }
 }
 
@@ -116,7 +130,9 @@ struct PfShape {
     // q_full[2] | q_empty[2] | kv_full[H] | kv_empty[H] | s_full[2][2] | p_full[2][2] | pv_done[2][2] | o_free[2]
     static constexpr int kBars = 4 + 2 * kHalves + 14;
     static constexpr int kOffMisc = kOffBar + kBars * 8;  // TMEM address, merge flag
-    static constexpr int kSmem = kOffMisc + 16 + 1024;    // + alignment slack
+    static constexpr int kOffTab = kOffMisc + 16;         // qp_tiles prefix (when n_qp < kMaxTab)
+    static constexpr int kMaxTab = 384;
+    static constexpr int kSmem = kOffTab + kMaxTab * 4 + 1024;  // + alignment slack
     static constexpr int kThreads = 512;
     static constexpr int kLoaders = 64;       // warps 10-11 (schedulers 2, 3; the MMA warps own 0, 1)
     // setmaxnreg split of the 64K registers: softmax warpgroups 0-1 grow,
@@ -346,20 +362,32 @@ struct Seg {
     int h, qp, ustart, uend, g0, g1;
 };
 
-__device__ __forceinline__ Seg seg_at(const PrefillArgs& a, int g, int g_end) {
-    const int per_head = __ldg(a.qp_tiles + a.n_qp);
+// tab: the key-tile prefix over the Q-tile pairs (a.qp_tiles), copied to
+// shared memory at kernel start when it fits: the binary search is a chain
+// of dependent loads that every role runs at every segment switch (from
+// global memory: ~1.5 us of L2 round trips on the critical path each time)
+// (tab: 32-bit shared address of the copy, 0 = read a.qp_tiles)
+__device__ __forceinline__ int tab_at(const PrefillArgs& a, std::uint32_t tab, int i) {
+    if (!tab) return __ldg(a.qp_tiles + i);
+    int v;
+    asm volatile("ld.shared.s32 %0, [%1];\n" : "=r"(v) : "r"(tab + 4u * static_cast<std::uint32_t>(i)));
+    return v;
+}
+
+__device__ __forceinline__ Seg seg_at(const PrefillArgs& a, std::uint32_t tab, int g, int g_end) {
+    const int per_head = tab_at(a, tab, a.n_qp);
     Seg s;
     s.h = g / per_head;
     const int r = g - s.h * per_head;
-    int lo = 0, hi = a.n_qp;  // largest qp with qp_tiles[qp] <= r
+    int lo = 0, hi = a.n_qp;  // largest qp with tab[qp] <= r
     while (hi - lo > 1) {
         const int mid = (lo + hi) >> 1;
-        if (__ldg(a.qp_tiles + mid) <= r) lo = mid;
+        if (tab_at(a, tab, mid) <= r) lo = mid;
         else hi = mid;
     }
     s.qp = lo;
-    s.ustart = s.h * per_head + __ldg(a.qp_tiles + lo);
-    s.uend = s.h * per_head + __ldg(a.qp_tiles + lo + 1);
+    s.ustart = s.h * per_head + tab_at(a, tab, lo);
+    s.uend = s.h * per_head + tab_at(a, tab, lo + 1);
     s.g0 = g;
     s.g1 = min(s.uend, g_end);
     return s;
@@ -376,7 +404,7 @@ __device__ __forceinline__ Seg seg_at(const PrefillArgs& a, int g, int g_end) {
 // the 126 MB L2). Online softmax and the part merge are order-free: only the
 // causal mask needs the tile, and it takes it from here. Units inside one
 // range keep the identity order.
-// (per segment constants: the CTA is x = blockIdx.x, its local time is g - x * per_cta)
+// (per segment constants: the CTA range is x = range_id(), its local time is g - x * per_cta)
 struct UnitOrder {
     int ustart, base, af, bl, nm, extra;  // base = x * per_cta; nm < 0: identity order
     __device__ __forceinline__ int tile(int g) const {
@@ -386,8 +414,17 @@ struct UnitOrder {
     }
 };
 
+// The CTA's stream-K range index (blockIdx.x, or the interleaved order of
+// PRISM_K4_PERM, which puts neighbouring ranges on CTAs launched apart)
+__device__ __forceinline__ int range_id(const PrefillArgs& a) {
+    const int b = static_cast<int>(blockIdx.x);
+    if (!a.perm) return b;
+    const int h = (static_cast<int>(gridDim.x) + 1) / 2;
+    return (b & 1) ? h + (b >> 1) : (b >> 1);
+}
+
 __device__ __forceinline__ UnitOrder unit_order(const PrefillArgs& a, const Seg& s) {
-    const int P = a.per_cta, x = static_cast<int>(blockIdx.x);
+    const int P = a.per_cta, x = range_id(a);
     const int f = s.ustart / P, l = (s.uend - 1) / P;
     UnitOrder o;
     o.ustart = s.ustart;
@@ -410,9 +447,11 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
     unsigned char* smem = smem_raw + ((1024u - (saddr(smem_raw) & 1023u)) & 1023u);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     constexpr int kTQ = S::kM / G;  // query tokens per Q tile
-    const int g_begin = blockIdx.x * a.per_cta;
+    const int rid = range_id(a);
+    const int g_begin = rid * a.per_cta;
     const int g_end = min(a.total, g_begin + a.per_cta);
     if (g_begin >= g_end) return;
+    if (tid == 0) k4_cta_stamp(a.cta_trace, 0);
     const int n_kv = a.g.n_kv, n_q = n_kv * G;
 
     const std::uint32_t sQ = saddr(smem + S::kOffQ);
@@ -443,6 +482,12 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
         for (int j = 0; j < 2; ++j) mb_init(b_ofree + 8 * j, 128);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
+    const bool tab_in_smem = a.tab_smem && a.n_qp + 1 <= S::kMaxTab;
+    if (tab_in_smem) {
+        std::int32_t* tab_s = reinterpret_cast<std::int32_t*>(smem + S::kOffTab);
+        for (int i = tid; i <= a.n_qp; i += S::kThreads) tab_s[i] = __ldg(a.qp_tiles + i);
+    }
+    const std::uint32_t tab = tab_in_smem ? saddr(smem + S::kOffTab) : 0u;
     if (warp == 12) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(saddr(tmem_slot)),
                      "n"(S::kTmemCols)
@@ -459,6 +504,11 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
     // writes (out, partials, tickets — the workspace and tickets are shared
     // by consecutive launches) wait for this launch's completion.
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    if (tid == 0 && a.cta_trace) {  // slot 1: the SM this CTA runs on
+        unsigned sm;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+        a.cta_trace[blockIdx.x * 4 + 1] = sm;
+    }
     // K half of local tile k is ring half 2k, its V half 2k + 1
     auto half_slot = [](int idx) { return idx % S::kHalves; };
     auto half_phase = [](int idx) { return static_cast<std::uint32_t>((idx / S::kHalves) & 1); };
@@ -533,13 +583,13 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
             for (int i = pend - 1; i >= 0; --i) arrive_half(last_idx - i, (qbits >> i) & 1u, (qsel >> i) & 1u);
             pend = 0;
         };
-        Seg la = seg_at(a, g_begin, g_end);  // look-ahead cursor (tile g + 1)
+        Seg la = seg_at(a, tab, g_begin, g_end);  // look-ahead cursor (tile g + 1)
         UnitOrder lo_ = unit_order(a, la);
         const int kt0 = lo_.tile(g_begin);
         std::uint64_t oa = decode(load_sid(kt0, ra)), ob = decode(load_sid(kt0, rb));
         int g = g_begin, s_idx = 0;
         while (g < g_end) {
-            const Seg sg = seg_at(a, g, g_end);
+            const Seg sg = seg_at(a, tab, g, g_end);
             // Q pair of the unit into buffer s_idx & 1 (the next segment's Q
             // loads while this one computes): rows of tile j = token (r / G) x
             // head (r % G), padding rows zero; committed with the segment's
@@ -565,7 +615,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 std::int32_t na = -1, nb = -1;
                 if (g + 1 < g_end) {
                     if (g + 1 >= la.g1) {
-                        la = seg_at(a, g + 1, g_end);
+                        la = seg_at(a, tab, g + 1, g_end);
                         lo_ = unit_order(a, la);
                     }
                     const int kt = lo_.tile(g + 1);
@@ -592,7 +642,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                     }
                 }
                 if (lane == 0 && w == 0) {
-                    k4_stamp(a.trace, 0, k);
+                    k4_stamp(a.trace, a.trace_cta, 0, k);
                     k4_mark(a.dbg, 1, 100 + k);  // loader: tile issued
                 }
                 oa = decode(na);
@@ -619,20 +669,20 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
             };
             const std::uint32_t s_col = tmem + j * 2 * S::kN, o_col = tmem + S::kColO + j * D;
             // S_j(k) = Q_j · K(k)ᵀ into S buffer (j, k & 1): two tiles ahead of P_j·V
-            Seg sc = seg_at(a, g_begin, g_end);
+            Seg sc = seg_at(a, tab, g_begin, g_end);
             int sc_idx = 0;
             auto issue_s = [&](int k) {
                 const int g = g_begin + k;
                 if (g >= sc.g1) {  // a new unit segment: its Q pair
-                    sc = seg_at(a, g, g_end);
+                    sc = seg_at(a, tab, g, g_end);
                     ++sc_idx;
                 }
                 const unsigned qb = static_cast<unsigned>(sc_idx & 1);
                 if (g == sc.g0) mb_wait(b_qfull + 8 * qb, (sc_idx >> 1) & 1);
                 const std::uint32_t dq = desc_lo(sQ + (2 * qb + j) * S::kQB, 16);
-                if (j == 0 && lane == 0) k4_stamp(a.trace, 11, k);
+                if (j == 0 && lane == 0) k4_stamp(a.trace, a.trace_cta, 11, k);
                 wait_half(2 * k);
-                if (j == 0 && lane == 0) k4_stamp(a.trace, 12, k);
+                if (j == 0 && lane == 0) k4_stamp(a.trace, a.trace_cta, 12, k);
                 const std::uint32_t dk = desc_lo(sKV + half_slot(2 * k) * S::kHalfB, 16);
                 static_assert(S::kM * 128 / 16 == 1024 && S::kN * 128 / 16 == 512, "descriptor steps in tc_mma_s_tile");
                 tc_mma_s_tile<D>(s_col + (k & 1) * S::kN, desc_of(dq), desc_of(dk), idesc_s);
@@ -640,35 +690,35 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 tc_commit_e(b_kvempty + 8 * half_slot(2 * k));
                 if (g + 1 == sc.g1) tc_commit_e(b_qempty + 8 * qb);  // last S of the segment: its Q buffer is free
                 if (lane == 0) {
-                    if (j == 0) k4_stamp(a.trace, 1, k);
+                    if (j == 0) k4_stamp(a.trace, a.trace_cta, 1, k);
                     k4_mark(a.dbg, 2 + j, 100 + k);  // MMA warp j: S(k) issued
                 }
             };
             issue_s(0);
             if (n > 1) issue_s(1);
-            Seg pc = seg_at(a, g_begin, g_end);
+            Seg pc = seg_at(a, tab, g_begin, g_end);
             int pc_idx = 0;
             for (int k = 0; k < n; ++k) {
                 const int g = g_begin + k;
                 if (g >= pc.g1) {
-                    pc = seg_at(a, g, g_end);
+                    pc = seg_at(a, tab, g, g_end);
                     ++pc_idx;
                 }
                 const bool fresh = g == pc.g0;
                 // O_j (+)= P_j(k) · V(k), P_j in S buffer (j, k & 1)
-                if (j == 0 && lane == 0) k4_stamp(a.trace, 8, k);
+                if (j == 0 && lane == 0) k4_stamp(a.trace, a.trace_cta, 8, k);
                 mb_wait(b_pfull + 8 * (2 * j + (k & 1)), (k >> 1) & 1);
                 if (fresh && pc_idx > 0) mb_wait(b_ofree + 8 * j, (pc_idx - 1) & 1);
-                if (j == 0 && lane == 0) k4_stamp(a.trace, 9, k);
+                if (j == 0 && lane == 0) k4_stamp(a.trace, a.trace_cta, 9, k);
                 wait_half(2 * k + 1);
-                if (j == 0 && lane == 0) k4_stamp(a.trace, 10, k);
+                if (j == 0 && lane == 0) k4_stamp(a.trace, a.trace_cta, 10, k);
                 const std::uint32_t dv = desc_lo(sKV + half_slot(2 * k + 1) * S::kHalfB, S::kN * 128);
                 static_assert(S::kN == 64, "four K=16 steps in tc_mma_pv_tile");
                 tc_mma_pv_tile(o_col, s_col + (k & 1) * S::kN, desc_of(dv), idesc_o, fresh ? 0u : 1u);
                 tc_commit_e(b_pvdone + 8 * (2 * j + (k & 1)));
                 tc_commit_e(b_kvempty + 8 * half_slot(2 * k + 1));
                 if (lane == 0) {
-                    k4_stamp(a.trace, j == 0 ? 2 : 7, k);
+                    k4_stamp(a.trace, a.trace_cta, j == 0 ? 2 : 7, k);
                     if (j == 0) k4_mark(a.dbg, 4, 100 + k);  // MMA warp 0: P·V(k) issued
                 }
                 if (k + 2 < n) issue_s(k + 2);
@@ -697,7 +747,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
             tc_fence_after();
         };
         while (g < g_end) {
-            const Seg sg = seg_at(a, g, g_end);
+            const Seg sg = seg_at(a, tab, g, g_end);
             const UnitOrder ord = unit_order(a, sg);
             const int tok = (2 * sg.qp + j) * kTQ + tq;
             const bool row_ok = r < kTQ * G && tok < a.chunk;
@@ -708,7 +758,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 mb_wait(b_sfull + 8 * (2 * j + b), (k >> 1) & 1);
                 tc_fence_after();
                 if (r == 0) {
-                    k4_stamp(a.trace, j == 0 ? 3 : 5, k);
+                    k4_stamp(a.trace, a.trace_cta, j == 0 ? 3 : 5, k);
                     if (j == 0) k4_mark(a.dbg, 5, 100 + k);  // softmax 0: has S(k)
                 }
 #if defined(K4_EXP) && (K4_EXP & 1)  // timing experiment: no softmax
@@ -789,7 +839,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 tc_fence_before();
                 mb_arrive(b_pfull + 8 * (2 * j + b));
                 if (r == 0) {
-                    k4_stamp(a.trace, j == 0 ? 4 : 6, k);
+                    k4_stamp(a.trace, a.trace_cta, j == 0 ? 4 : 6, k);
                     if (j == 0) k4_mark(a.dbg, 6, 100 + k);  // softmax 0: posted P(k)
                 }
             }
@@ -799,8 +849,10 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
             if (!pdl_waited) {  // first global write of this thread (see launch_dependents)
                 asm volatile("griddepcontrol.wait;\n" ::: "memory");
                 pdl_waited = true;
+                if (tid == 0) k4_cta_stamp(a.cta_trace, 2);
             }
             const int u = sg.h * a.n_qp + sg.qp;
+            if (r == 0 && j == 0) k4_stamp(a.trace, a.trace_cta, 13, k - 1);  // epilogue: O complete
             const int first_cta = sg.ustart / a.per_cta, last_cta = (sg.uend - 1) / a.per_cta;
             const int parts = last_cta - first_cta + 1;
             __nv_bfloat16* dst =
@@ -827,7 +879,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
             } else {
                 // publish this CTA's partial of the unit (slot 2c: the range's
                 // first segment, 2c + 1: its last), then the last publisher merges
-                const int slot = 2 * static_cast<int>(blockIdx.x) + (sg.g0 == g_begin ? 0 : 1);
+                const int slot = 2 * rid + (sg.g0 == g_begin ? 0 : 1);
                 // O / l: |values| <= max |V|, so fp16 keeps 2^-11 relative
                 // precision in half the bytes of an fp32 partial
                 const float inv_l = l_run > 0.f ? 1.f / l_run : 0.f;
@@ -847,6 +899,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 // the barrier orders every thread's partial stores before
                 // thread 0's gpu-scope release (fence + ticket), which is
                 // cumulative over them (the usual semaphore pattern)
+                if (r == 0 && j == 0) k4_stamp(a.trace, a.trace_cta, 14, k - 1);  // partial stored
                 asm volatile("bar.sync 1, 256;\n" ::: "memory");
                 if (tid == 0) {
                     __threadfence();
@@ -857,6 +910,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                     *merge_flag = last;
                 }
                 asm volatile("bar.sync 1, 256;\n" ::: "memory");
+                if (r == 0 && j == 0) k4_stamp(a.trace, a.trace_cta, 15, k - 1);  // ticket taken
                 if (*merge_flag && a.merge_fast && parts <= kFastParts) {
                     __threadfence();
                     // Latency-parallel combination (the usual case: a unit
@@ -968,6 +1022,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
         tc_fence_before();
     }
     __syncthreads();
+    if (tid == 0) k4_cta_stamp(a.cta_trace, 3);
     if (warp == 12) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(S::kTmemCols)
@@ -1034,7 +1089,8 @@ static unsigned* k4_debug_words() {
 // while the kernel runs; 0 words when debugging is off.
 static unsigned long long* k4_trace_buf() {
     static unsigned long long* dev = [] {
-        if (!std::getenv("PRISM_K4_TRACE")) return static_cast<unsigned long long*>(nullptr);
+        if (!std::getenv("PRISM_K4_TRACE") && !std::getenv("PRISM_K4_CTA_TRACE"))
+            return static_cast<unsigned long long*>(nullptr);
         unsigned long long* p = nullptr;
         PRISM_CUDA(cudaMalloc(&p, 16 * 1024 * sizeof(unsigned long long)));
         PRISM_CUDA(cudaMemset(p, 0, 16 * 1024 * sizeof(unsigned long long)));
@@ -1110,7 +1166,19 @@ void launch_k4(Ctx& d, PrefillArgs a) {
     a.part_ml = reinterpret_cast<float2*>(ws + slots * 256 * d.head_dim);
     a.tickets = d.attn_counters(static_cast<std::size_t>(d.n_kv) * n_qp);
     a.dbg = k4_debug_words();
-    a.trace = k4_trace_buf();
+    // PRISM_K4_TRACE: tile stamps of CTA 0 (rows 0-12 of the buffer);
+    // PRISM_K4_CTA_TRACE: per-CTA timelines of 5 consecutive launches in
+    // rows 13-15 ([launch % 5][CTA < 148][4])
+    static const bool tile_trace = std::getenv("PRISM_K4_TRACE") != nullptr;
+    static const bool cta_trace = std::getenv("PRISM_K4_CTA_TRACE") != nullptr;
+    static unsigned long long cta_launch = 0;
+    static const int trace_cta = [] {
+        const char* e = std::getenv("PRISM_K4_TRACE_CTA");
+        return e ? std::atoi(e) : 0;
+    }();
+    a.trace = tile_trace ? k4_trace_buf() : nullptr;
+    a.trace_cta = trace_cta;
+    a.cta_trace = (cta_trace && grid <= 148) ? k4_trace_buf() + 13 * 1024 + (cta_launch++ % 5) * 148 * 4 : nullptr;
     chained = chained && d.k4_chain;  // a workspace / counter reallocation breaks the chain
     if (d.head_dim == 128) {
         launch_pf_d<128>(d.group, a, grid, d.stream, chained);
@@ -1119,6 +1187,22 @@ void launch_k4(Ctx& d, PrefillArgs a) {
     }
     d.k3_chain = false;
     d.k4_chain = true;
+}
+
+int k4_tab_smem() {  // PRISM_K4_TAB=0: seg_at reads the prefix from global memory (A/B)
+    static const int v = [] {
+        const char* e = std::getenv("PRISM_K4_TAB");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return v;
+}
+
+int k4_perm() {  // PRISM_K4_PERM=1: interleaved CTA -> range order (experiment)
+    static const int v = [] {
+        const char* e = std::getenv("PRISM_K4_PERM");
+        return (e && e[0] == '1') ? 1 : 0;
+    }();
+    return v;
 }
 
 int k4_merge_fast() {  // PRISM_K4_MERGE=0: the per-part merge loop only (A/B)
@@ -1148,6 +1232,8 @@ void launch_prefill_attention(EngineDeviceImpl& d, int layer, const void* q, voi
     }();
     a.rescale_thr = thr;
     a.merge_fast = k4_merge_fast();
+    a.perm = k4_perm();
+    a.tab_smem = k4_tab_smem();
     launch_k4(d, a);
 }
 
@@ -1173,6 +1259,8 @@ void PagedCtx::prefill_attention(int layer, const std::int32_t* slot_ids, int fi
     a.scale_log2 = scale * 1.4426950408889634f;
     a.rescale_thr = 8.f;
     a.merge_fast = k4_merge_fast();
+    a.perm = k4_perm();
+    a.tab_smem = k4_tab_smem();
     launch_k4(*this, a);
 }
 

@@ -38,7 +38,7 @@ while True:
 for _ in range(3):
     eng.prefill_attention(0, q.data_ptr(), o.data_ptr(), 1 / math.sqrt(128))
 eng.synchronize()
-R = 13
+R = 16
 SHOW = [int(x) for x in os.environ.get('SHOW', '').split(',') if x]
 buf = (C.c_uint64 * (R * 1024))()
 got = C.c_int32()
@@ -46,7 +46,8 @@ lib.call("prism_debug_k4_trace", buf, R * 1024, C.byref(got))
 tr = [list(buf[r * 1024:(r + 1) * 1024]) for r in range(R)]
 n_tiles = max(i for i in range(1024) if tr[1][i]) + 1
 t0 = min(x for row in tr for x in row[:n_tiles] if x)
-names = ["load", "S_iss", "PV0_is", "w0_S", "w0_P", "w1_S", "w1_P", "PV1_is", "m_it", "m_P", "m_V", "s_beg", "s_K"]
+names = ["load", "S_iss", "PV0_is", "w0_S", "w0_P", "w1_S", "w1_P", "PV1_is", "m_it", "m_P", "m_V", "s_beg", "s_K",
+         "e_O", "e_st", "e_tk"]  # e_*: epilogue after tile t (O complete, partial stored, ticket taken)
 print("tile " + " ".join(f"{n:>7s}" for n in names) + "   (us from first stamp)")
 for t in range(n_tiles):
     row = [(tr[r][t] - t0) / 1e3 if tr[r][t] else float("nan") for r in range(R)]
