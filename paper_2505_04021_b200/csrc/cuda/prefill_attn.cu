@@ -74,6 +74,7 @@ struct PrefillArgs {
     float rescale_thr;        // lazy-rescale threshold (log2 units; 8)
     int merge_fast;           // 1: merges of <= 4 parts issue all their loads at once (PRISM_K4_MERGE)
     int perm;                 // 1: CTA b takes range b / 2 (even b) or ceil(grid / 2) + b / 2 (odd b) (PRISM_K4_PERM)
+    int early_ticket;         // 1: a mid-range partial's ticket is a release atomic checked at the next epilogue (PRISM_K4_EARLY)
     int tab_smem;             // 1: the pair prefix is read from a shared-memory copy when it fits (PRISM_K4_TAB=0: global)
     int n_qp;                 // Q-tile pairs per kv head
     const std::int32_t* qp_tiles;  // [n_qp + 1] key-tile prefix over the pairs (same for every kv head)
@@ -734,6 +735,128 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
         const std::uint32_t tO = tmem + lane_base + S::kColO + j * D;
         const int tq = r / G;
         const int row = j * S::kM + r;  // row of the unit (partials)
+        // Merge of a cut unit by the last of its parts to publish: every
+        // part's (m, l, O / l) from the workspace, combined into `out`.
+        auto merge_unit = [&](const Seg& ps) {
+            const int first_cta = ps.ustart / a.per_cta, last_cta = (ps.uend - 1) / a.per_cta;
+            const int parts = last_cta - first_cta + 1;
+            const int tok = (2 * ps.qp + j) * kTQ + tq;
+            const bool row_ok = r < kTQ * G && tok < a.chunk;
+            __nv_bfloat16* dst =
+                row_ok ? a.out + (static_cast<std::size_t>(tok) * n_q + static_cast<std::size_t>(ps.h) * G + r % G) * D
+                       : nullptr;
+            if (a.merge_fast && parts <= kFastParts) {
+                __threadfence();
+                // Latency-parallel combination (the usual case: a unit
+                // cut into 2-4 parts): every part's (m, l) in one round of
+                // loads, then per 32-column group all parts' O rows at
+                // once — 1 + D / 32 dependent L2 round trips instead of
+                // (2 + D / 32) x parts.
+                auto slot_of = [&](int cta) { return 2 * cta + (cta * a.per_cta >= ps.ustart ? 0 : 1); };
+                int sl[kFastParts];
+                float2 ml[kFastParts];
+#pragma unroll
+                for (int t = 0; t < kFastParts; ++t) {
+                    sl[t] = slot_of(min(first_cta + t, last_cta));
+                    if (t < parts) ml[t] = __ldcg(a.part_ml + static_cast<std::size_t>(sl[t]) * 256 + row);
+                }
+                float mm = -INFINITY;
+#pragma unroll
+                for (int t = 0; t < kFastParts; ++t)
+                    if (t < parts) mm = fmaxf(mm, ml[t].x);
+                float ll = 0.f;
+#pragma unroll
+                for (int t = 0; t < kFastParts; ++t)
+                    if (t < parts) ll += ml[t].x == -INFINITY ? 0.f : ml[t].y * fast_exp2(ml[t].x - mm);
+                const float inv = ll > 0.f ? 1.f / ll : 0.f;
+                float wt[kFastParts];
+#pragma unroll
+                for (int t = 0; t < kFastParts; ++t)
+                    wt[t] = (t < parts && ml[t].x != -INFINITY) ? fast_exp2(ml[t].x - mm) * ml[t].y * inv : 0.f;
+#pragma unroll 1
+                for (int cg = 0; cg < D / 32; ++cg) {
+                    uint2 h[kFastParts][8];
+#pragma unroll
+                    for (int t = 0; t < kFastParts; ++t)
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            h[t][q] = t < parts ? __ldcg(a.part_o + (static_cast<std::size_t>(sl[t]) * (D / 4) +
+                                                                     cg * 8 + q) * 256 + row)
+                                                : make_uint2(0u, 0u);
+                    float4 acc[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) {
+                        acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                        for (int t = 0; t < kFastParts; ++t) {
+                            const float2 lo = unpack_f16(h[t][q].x), hi = unpack_f16(h[t][q].y);
+                            acc[q].x += wt[t] * lo.x;
+                            acc[q].y += wt[t] * lo.y;
+                            acc[q].z += wt[t] * hi.x;
+                            acc[q].w += wt[t] * hi.y;
+                        }
+                    }
+                    if (row_ok) {
+#pragma unroll
+                        for (int q = 0; q < 8; q += 2) {
+                            *reinterpret_cast<uint4*>(dst + cg * 32 + 4 * q) =
+                                make_uint4(pack_bf16(acc[q].x, acc[q].y), pack_bf16(acc[q].z, acc[q].w),
+                                           pack_bf16(acc[q + 1].x, acc[q + 1].y),
+                                           pack_bf16(acc[q + 1].z, acc[q + 1].w));
+                        }
+                    }
+                }
+            } else {
+                __threadfence();
+                // online combination of the parts' (m, l, O) rows
+                auto slot_of = [&](int cta) { return 2 * cta + (cta * a.per_cta >= ps.ustart ? 0 : 1); };
+                float mm = -INFINITY;
+                for (int cta = first_cta; cta <= last_cta; ++cta)
+                    mm = fmaxf(mm, __ldcg(a.part_ml + static_cast<std::size_t>(slot_of(cta)) * 256 + row).x);
+                float ll = 0.f;
+                for (int cta = first_cta; cta <= last_cta; ++cta) {
+                    const float2 ml = __ldcg(a.part_ml + static_cast<std::size_t>(slot_of(cta)) * 256 + row);
+                    ll += ml.x == -INFINITY ? 0.f : ml.y * fast_exp2(ml.x - mm);
+                }
+                const float inv = ll > 0.f ? 1.f / ll : 0.f;
+#pragma unroll 1
+                for (int cg = 0; cg < D / 32; ++cg) {
+                    float4 acc[8];
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    for (int cta = first_cta; cta <= last_cta; ++cta) {
+                        const int sl = slot_of(cta);
+                        const float2 pml = __ldcg(a.part_ml + static_cast<std::size_t>(sl) * 256 + row);
+                        // the partial is O / l: weight by l
+                        const float wt = pml.x == -INFINITY ? 0.f : fast_exp2(pml.x - mm) * pml.y * inv;
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            const uint2 h4 =
+                                __ldcg(a.part_o + (static_cast<std::size_t>(sl) * (D / 4) + cg * 8 + q) * 256 + row);
+                            const float2 lo = unpack_f16(h4.x), hi = unpack_f16(h4.y);
+                            acc[q].x += wt * lo.x;
+                            acc[q].y += wt * lo.y;
+                            acc[q].z += wt * hi.x;
+                            acc[q].w += wt * hi.y;
+                        }
+                    }
+                    if (row_ok) {
+#pragma unroll
+                        for (int q = 0; q < 8; q += 2) {
+                            *reinterpret_cast<uint4*>(dst + cg * 32 + 4 * q) =
+                                make_uint4(pack_bf16(acc[q].x, acc[q].y), pack_bf16(acc[q].z, acc[q].w),
+                                           pack_bf16(acc[q + 1].x, acc[q + 1].y),
+                                           pack_bf16(acc[q + 1].z, acc[q + 1].w));
+                        }
+                    }
+                }
+            }
+        };
+        // a mid-range cut unit whose ticket was taken early (release atomic,
+        // result checked at the range's next epilogue)
+        bool pend = false;
+        int pend_old = 0;
+        Seg pend_seg{};
         int k = 0, g = g_begin;
         bool pdl_waited = false;
         // PV_j(k) completes phase k >> 1 of pv_done[j][k & 1]. Whenever this
@@ -851,6 +974,22 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 pdl_waited = true;
                 if (tid == 0) k4_cta_stamp(a.cta_trace, 2);
             }
+            if (pend) {
+                if (tid == 0) {
+                    const int pu = pend_seg.h * a.n_qp + pend_seg.qp;
+                    const int pparts = (pend_seg.uend - 1) / a.per_cta - pend_seg.ustart / a.per_cta + 1;
+                    const int last = pend_old == pparts - 1;
+                    if (last) {
+                        __threadfence();  // acquire side: the other parts' partials
+                        a.tickets[pu] = 0;
+                    }
+                    *merge_flag = last;
+                }
+                asm volatile("bar.sync 1, 256;\n" ::: "memory");
+                if (*merge_flag) merge_unit(pend_seg);
+                asm volatile("bar.sync 1, 256;\n" ::: "memory");  // merge_flag is rewritten below
+                pend = false;
+            }
             const int u = sg.h * a.n_qp + sg.qp;
             if (r == 0 && j == 0) k4_stamp(a.trace, a.trace_cta, 13, k - 1);  // epilogue: O complete
             const int first_cta = sg.ustart / a.per_cta, last_cta = (sg.uend - 1) / a.per_cta;
@@ -901,6 +1040,19 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 // cumulative over them (the usual semaphore pattern)
                 if (r == 0 && j == 0) k4_stamp(a.trace, a.trace_cta, 14, k - 1);  // partial stored
                 asm volatile("bar.sync 1, 256;\n" ::: "memory");
+                if (sg.g1 < g_end && a.early_ticket) {
+                    // more of this range follows: thread 0 takes the ticket with
+                    // a release atomic (cumulative over the barrier) and nobody
+                    // waits for its result here; the range's next epilogue
+                    // checks it and merges the unit if this part was the last
+                    if (tid == 0) {
+                        asm volatile("atom.add.release.gpu.global.s32 %0, [%1], 1;\n"
+                                     : "=r"(pend_old) : "l"(a.tickets + u) : "memory");
+                    }
+                    pend = true;
+                    pend_seg = sg;
+                    continue;
+                }
                 if (tid == 0) {
                     __threadfence();
                     const int prev = atomicAdd(a.tickets + u, 1);
@@ -911,112 +1063,7 @@ __global__ void __launch_bounds__(512, 1) k4_prefill(PrefillArgs a) {
                 }
                 asm volatile("bar.sync 1, 256;\n" ::: "memory");
                 if (r == 0 && j == 0) k4_stamp(a.trace, a.trace_cta, 15, k - 1);  // ticket taken
-                if (*merge_flag && a.merge_fast && parts <= kFastParts) {
-                    __threadfence();
-                    // Latency-parallel combination (the usual case: a unit
-                    // cut into 2-4 parts): every part's (m, l) in one round of
-                    // loads, then per 32-column group all parts' O rows at
-                    // once — 1 + D / 32 dependent L2 round trips instead of
-                    // (2 + D / 32) x parts.
-                    auto slot_of = [&](int cta) { return 2 * cta + (cta * a.per_cta >= sg.ustart ? 0 : 1); };
-                    int sl[kFastParts];
-                    float2 ml[kFastParts];
-#pragma unroll
-                    for (int t = 0; t < kFastParts; ++t) {
-                        sl[t] = slot_of(min(first_cta + t, last_cta));
-                        if (t < parts) ml[t] = __ldcg(a.part_ml + static_cast<std::size_t>(sl[t]) * 256 + row);
-                    }
-                    float mm = -INFINITY;
-#pragma unroll
-                    for (int t = 0; t < kFastParts; ++t)
-                        if (t < parts) mm = fmaxf(mm, ml[t].x);
-                    float ll = 0.f;
-#pragma unroll
-                    for (int t = 0; t < kFastParts; ++t)
-                        if (t < parts) ll += ml[t].x == -INFINITY ? 0.f : ml[t].y * fast_exp2(ml[t].x - mm);
-                    const float inv = ll > 0.f ? 1.f / ll : 0.f;
-                    float wt[kFastParts];
-#pragma unroll
-                    for (int t = 0; t < kFastParts; ++t)
-                        wt[t] = (t < parts && ml[t].x != -INFINITY) ? fast_exp2(ml[t].x - mm) * ml[t].y * inv : 0.f;
-#pragma unroll 1
-                    for (int cg = 0; cg < D / 32; ++cg) {
-                        uint2 h[kFastParts][8];
-#pragma unroll
-                        for (int t = 0; t < kFastParts; ++t)
-#pragma unroll
-                            for (int q = 0; q < 8; ++q)
-                                h[t][q] = t < parts ? __ldcg(a.part_o + (static_cast<std::size_t>(sl[t]) * (D / 4) +
-                                                                         cg * 8 + q) * 256 + row)
-                                                    : make_uint2(0u, 0u);
-                        float4 acc[8];
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                            for (int t = 0; t < kFastParts; ++t) {
-                                const float2 lo = unpack_f16(h[t][q].x), hi = unpack_f16(h[t][q].y);
-                                acc[q].x += wt[t] * lo.x;
-                                acc[q].y += wt[t] * lo.y;
-                                acc[q].z += wt[t] * hi.x;
-                                acc[q].w += wt[t] * hi.y;
-                            }
-                        }
-                        if (row_ok) {
-#pragma unroll
-                            for (int q = 0; q < 8; q += 2) {
-                                *reinterpret_cast<uint4*>(dst + cg * 32 + 4 * q) =
-                                    make_uint4(pack_bf16(acc[q].x, acc[q].y), pack_bf16(acc[q].z, acc[q].w),
-                                               pack_bf16(acc[q + 1].x, acc[q + 1].y),
-                                               pack_bf16(acc[q + 1].z, acc[q + 1].w));
-                            }
-                        }
-                    }
-                } else if (*merge_flag) {
-                    __threadfence();
-                    // online combination of the parts' (m, l, O) rows
-                    auto slot_of = [&](int cta) { return 2 * cta + (cta * a.per_cta >= sg.ustart ? 0 : 1); };
-                    float mm = -INFINITY;
-                    for (int cta = first_cta; cta <= last_cta; ++cta)
-                        mm = fmaxf(mm, __ldcg(a.part_ml + static_cast<std::size_t>(slot_of(cta)) * 256 + row).x);
-                    float ll = 0.f;
-                    for (int cta = first_cta; cta <= last_cta; ++cta) {
-                        const float2 ml = __ldcg(a.part_ml + static_cast<std::size_t>(slot_of(cta)) * 256 + row);
-                        ll += ml.x == -INFINITY ? 0.f : ml.y * fast_exp2(ml.x - mm);
-                    }
-                    const float inv = ll > 0.f ? 1.f / ll : 0.f;
-#pragma unroll 1
-                    for (int cg = 0; cg < D / 32; ++cg) {
-                        float4 acc[8];
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) acc[q] = make_float4(0.f, 0.f, 0.f, 0.f);
-                        for (int cta = first_cta; cta <= last_cta; ++cta) {
-                            const int sl = slot_of(cta);
-                            const float2 pml = __ldcg(a.part_ml + static_cast<std::size_t>(sl) * 256 + row);
-                            // the partial is O / l: weight by l
-                            const float wt = pml.x == -INFINITY ? 0.f : fast_exp2(pml.x - mm) * pml.y * inv;
-#pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                const uint2 h4 =
-                                    __ldcg(a.part_o + (static_cast<std::size_t>(sl) * (D / 4) + cg * 8 + q) * 256 + row);
-                                const float2 lo = unpack_f16(h4.x), hi = unpack_f16(h4.y);
-                                acc[q].x += wt * lo.x;
-                                acc[q].y += wt * lo.y;
-                                acc[q].z += wt * hi.x;
-                                acc[q].w += wt * hi.y;
-                            }
-                        }
-                        if (row_ok) {
-#pragma unroll
-                            for (int q = 0; q < 8; q += 2) {
-                                *reinterpret_cast<uint4*>(dst + cg * 32 + 4 * q) =
-                                    make_uint4(pack_bf16(acc[q].x, acc[q].y), pack_bf16(acc[q].z, acc[q].w),
-                                               pack_bf16(acc[q + 1].x, acc[q + 1].y),
-                                               pack_bf16(acc[q + 1].z, acc[q + 1].w));
-                            }
-                        }
-                    }
-                }
+                if (*merge_flag) merge_unit(sg);
             }
         }
         tc_fence_before();
@@ -1189,6 +1236,14 @@ void launch_k4(Ctx& d, PrefillArgs a) {
     d.k4_chain = true;
 }
 
+int k4_early_ticket() {  // PRISM_K4_EARLY=0: every ticket taken and checked at once (A/B)
+    static const int v = [] {
+        const char* e = std::getenv("PRISM_K4_EARLY");
+        return (e && e[0] == '0') ? 0 : 1;
+    }();
+    return v;
+}
+
 int k4_tab_smem() {  // PRISM_K4_TAB=0: seg_at reads the prefix from global memory (A/B)
     static const int v = [] {
         const char* e = std::getenv("PRISM_K4_TAB");
@@ -1234,6 +1289,7 @@ void launch_prefill_attention(EngineDeviceImpl& d, int layer, const void* q, voi
     a.merge_fast = k4_merge_fast();
     a.perm = k4_perm();
     a.tab_smem = k4_tab_smem();
+    a.early_ticket = k4_early_ticket();
     launch_k4(d, a);
 }
 
@@ -1261,6 +1317,7 @@ void PagedCtx::prefill_attention(int layer, const std::int32_t* slot_ids, int fi
     a.merge_fast = k4_merge_fast();
     a.perm = k4_perm();
     a.tab_smem = k4_tab_smem();
+    a.early_ticket = k4_early_ticket();
     launch_k4(*this, a);
 }
 
