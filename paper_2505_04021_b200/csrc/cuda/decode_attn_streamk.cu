@@ -642,11 +642,34 @@ void launch_k3_streamk_t(Ctx& d, AttnArgs a, int n_dec) {
         d.sk_total = acc;
         d.sk_prefix.upload(static_cast<std::size_t>(n_pairs) + 1, d.stream);
         d.sk_step = d.step_serial;
+        // CTAs per SM: every CTA range ends in a cut pair (a partial, a
+        // ticket and a merge on the critical path), so small launches want
+        // few, long ranges; big ones want the resident CTAs for memory-level
+        // parallelism. Chosen by key tiles per SM (tools/k3_per_sm_sweep.sh,
+        // DESIGN §4): < 35 -> 1; 35-70 -> 1 for head_dim 128 with groups >= 6
+        // (the MMA-heavier tiles), else 2; >= 70 -> 2 for head_dim 64, the
+        // occupancy (3) for head_dim 128. PRISM_SK_PER_SM caps it (A/B).
         static const int per_sm_cap = [] {
-            const char* e = std::getenv("PRISM_SK_PER_SM");  // experiments
+            const char* e = std::getenv("PRISM_SK_PER_SM");
             return e ? std::max(1, std::atoi(e)) : 1 << 30;
         }();
-        const int per_sm = std::min(per_sm_cap, d.head_dim == 128 ? occupancy_sk_d<128>(d.group) : occupancy_sk_d<64>(d.group));
+        static const bool per_sm_auto = [] {
+            const char* e = std::getenv("PRISM_SK_PER_SM_AUTO");  // 0: always the occupancy (A/B)
+            return !(e && e[0] == '0');
+        }();
+        const int occ = d.head_dim == 128 ? occupancy_sk_d<128>(d.group) : occupancy_sk_d<64>(d.group);
+        int want = occ;
+        if (per_sm_auto) {
+            const int tps = d.sk_total / sms;
+            if (tps < 35) {
+                want = 1;
+            } else if (tps < 70) {
+                want = (d.head_dim == 128 && d.group >= 6) ? 1 : 2;
+            } else {
+                want = d.head_dim == 64 ? 2 : occ;
+            }
+        }
+        const int per_sm = std::max(1, std::min({per_sm_cap, occ, want}));
         const int slots = sms * per_sm;
         d.sk_per_cta = std::max(1, (d.sk_total + slots - 1) / slots);
         // the first pair of every CTA range
