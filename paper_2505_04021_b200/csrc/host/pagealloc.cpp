@@ -190,12 +190,15 @@ using detail::Access;
 using detail::kNone;
 using detail::PoolState;
 
-// Look-ahead window handed to VmmDevice::premap when a pool grows: twice the
-// pages the growing call mapped, within [128, 256] pages (16-32 physical
-// chunks of 8). 128 pages are ~32 decode steps of runway for a C1 pool, so
-// the worker rides out the multi-10-ms periods in which VMM calls stall
-// (tools/vmm_trace_summary.py); look-ahead only ever uses free budget.
-constexpr std::uint64_t kPremapMin = 128;
+// Look-ahead window handed to VmmDevice::premap when a pool grows: 256 pages
+// (32 physical chunks of 8, 512 MiB) past the pool's mapped pages. That is
+// ~64 decode steps of runway for a C1 pool (4 new pages per step), so the
+// worker rides out the periods in which VMM calls stall: a 128-page window
+// ran dry in one bench run whose cuMemSetAccess calls averaged ~6 ms (p99
+// 70 ms) and the engine thread waited ~100 ms inside the timed region.
+// Look-ahead only ever uses free budget (and at most kMaxCleanPages mapped
+// ahead on a device).
+constexpr std::uint64_t kPremapMin = 256;
 constexpr std::uint64_t kPremapMax = 256;
 
 // PRISM_PREMAP=0 turns the look-ahead off (A/B measurements).

@@ -96,14 +96,14 @@ def test_worker_premaps_the_next_pages(product, device):
     worker thread, which maps their physical chunks ahead of need: the
     pool's next maps need no driver call."""
     K = device.chunk_pages()
-    gpu = msim.GpuState(0, 200, lib=product)
+    gpu = msim.GpuState(0, 400, lib=product)
     gpu.ledger.attach_device(device)
     pool = msim.alloc_kvcache(gpu.ledger, "pm", 131072, 400)  # 16 tokens per page
     device.reset_stats()
     first = msim.alloc_kv(pool, gpu.ledger, 16)  # maps page 0 (urgent chunk), hints the next pages
     device.quiesce()
     st = device.stats()
-    ahead = {p // K for p in range(1, 129)} - {0}
+    ahead = {p // K for p in range(1, 257)} - {0}  # the 256-page look-ahead window
     assert st["maps"] == 1 and st["urgent"] == 1 and st["premaps"] == len(ahead), st
     grow = msim.alloc_kv(pool, gpu.ledger, 8 * 16)  # pages 1..8
     st = device.stats()
