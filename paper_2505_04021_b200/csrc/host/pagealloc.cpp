@@ -198,8 +198,13 @@ using detail::PoolState;
 // 70 ms) and the engine thread waited ~100 ms inside the timed region.
 // Look-ahead only ever uses free budget (and at most kMaxCleanPages mapped
 // ahead on a device).
-constexpr std::uint64_t kPremapMin = 256;
-constexpr std::uint64_t kPremapMax = 256;
+std::uint64_t premap_pages() {  // PRISM_PREMAP_PAGES overrides the window (A/B)
+    static const std::uint64_t n = [] {
+        const char* e = std::getenv("PRISM_PREMAP_PAGES");
+        return e ? static_cast<std::uint64_t>(std::max(1, std::atoi(e))) : std::uint64_t{256};
+    }();
+    return n;
+}
 
 // PRISM_PREMAP=0 turns the look-ahead off (A/B measurements).
 bool premap_enabled() {
@@ -418,7 +423,7 @@ AllocResult detail::alloc_kv_into(KvPool& pool, PhysicalLedger& ledger, std::uin
         // The pool is growing: its next maps will be the following lowest
         // unmapped pages. Hand them to the device's worker thread to map
         // (and make accessible) ahead of time, so those maps become revives.
-        const std::uint64_t ahead = !premap_enabled() ? 0 : std::min<std::uint64_t>(kPremapMax, std::max<std::uint64_t>(kPremapMin, 2 * new_pages));
+        const std::uint64_t ahead = !premap_enabled() ? 0 : premap_pages();
         vas.clear();
         for (std::uint64_t k = 0; k < ahead && p != kNone; ++k) {
             vas.push_back(s.va + static_cast<std::uint64_t>(p) * s.dev->page_bytes());
