@@ -693,6 +693,10 @@ std::uint64_t VmmDevice::total_handles() const {
     Lock lk(mu_);
     return total_locked();
 }
+std::uint64_t VmmDevice::pool_count() const {
+    Lock lk(mu_);
+    return ranges_.size();
+}
 std::uint64_t VmmDevice::buffered_handles() const {
     Lock lk(mu_);
     return buffer_pages_;

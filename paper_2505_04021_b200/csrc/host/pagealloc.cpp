@@ -198,12 +198,17 @@ using detail::PoolState;
 // 70 ms) and the engine thread waited ~100 ms inside the timed region.
 // Look-ahead only ever uses free budget (and at most kMaxCleanPages mapped
 // ahead on a device).
-std::uint64_t premap_pages() {  // PRISM_PREMAP_PAGES overrides the window (A/B)
-    static const std::uint64_t n = [] {
+// With more pools on the device the deeper window holds budget that other
+// models then steal back (scheduler-driven C2 / C5 runs: 2-10x the
+// engine-thread cost per page op at 256 pages vs 128), so the window is 256
+// pages with at most two pools and 128 beyond; PRISM_PREMAP_PAGES fixes it.
+std::uint64_t premap_pages(std::uint64_t pools) {
+    static const std::uint64_t fixed = [] {
         const char* e = std::getenv("PRISM_PREMAP_PAGES");
-        return e ? static_cast<std::uint64_t>(std::max(1, std::atoi(e))) : std::uint64_t{256};
+        return e ? static_cast<std::uint64_t>(std::max(1, std::atoi(e))) : std::uint64_t{0};
     }();
-    return n;
+    if (fixed) return fixed;
+    return pools <= 2 ? 256 : 128;
 }
 
 // PRISM_PREMAP=0 turns the look-ahead off (A/B measurements).
@@ -423,7 +428,7 @@ AllocResult detail::alloc_kv_into(KvPool& pool, PhysicalLedger& ledger, std::uin
         // The pool is growing: its next maps will be the following lowest
         // unmapped pages. Hand them to the device's worker thread to map
         // (and make accessible) ahead of time, so those maps become revives.
-        const std::uint64_t ahead = !premap_enabled() ? 0 : premap_pages();
+        const std::uint64_t ahead = !premap_enabled() ? 0 : premap_pages(s.dev->pool_count());
         vas.clear();
         for (std::uint64_t k = 0; k < ahead && p != kNone; ++k) {
             vas.push_back(s.va + static_cast<std::uint64_t>(p) * s.dev->page_bytes());

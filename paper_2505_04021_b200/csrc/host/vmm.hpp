@@ -137,6 +137,7 @@ public:
     std::uint64_t cached_handles() const;    // created, unmapped chunks
     std::uint64_t pending_unmaps() const;    // idle (mapped, unreferenced) chunks
     std::uint64_t total_handles() const;     // all chunks
+    std::uint64_t pool_count() const;        // reserved VA ranges (KV pools on this device)
     // Wait until the worker has no queued / in-flight work.
     void quiesce();
 
